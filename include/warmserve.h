@@ -1,0 +1,191 @@
+/*
+ * warmserve.h — C-ABI of the B200-native universal-GPU-worker data path.
+ *
+ * The reference (prewarmsim, /root/reference/pkg) is a pure-Python simulator
+ * with no FFI; its drop-in seam is the Python `Cluster` object protocol plus
+ * the memswitch / planning functions. Each entry point below
+ * cites the reference interface it replaces. The Python package
+ * `paper_2512_09472_b200` binds these with ctypes and re-exposes the
+ * reference's Cluster protocol on top (INTEGRATION.md shows the binding).
+ *
+ * Conventions: plain pointers and sizes only; every function returns a
+ * WS_* status (0 = ok) and writes results through out-pointers;
+ * ws_last_error() returns the thread's last error text. Device pointers are
+ * CUDA device addresses; `stream` arguments are cudaStream_t passed as void*.
+ * Single writer: all pool/ledger calls for one pool come from one host thread
+ * (cluster.py:200-201); only the internal unmap worker runs concurrently.
+ */
+#ifndef WARMSERVE_H_
+#define WARMSERVE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to ClusterError / ValueError by the mirror) ---- */
+#define WS_OK 0
+#define WS_ERR_INVALID 1          /* ValueError in the reference               */
+#define WS_ERR_INSUFFICIENT 2     /* "insufficient pages" cluster.py:259-263    */
+#define WS_ERR_DUPLICATE 3        /* "already holds a slot" cluster.py:255-258  */
+#define WS_ERR_NO_SLOT 4          /* unknown slot id                            */
+#define WS_ERR_STATE 5            /* op illegal in the pool's current state     */
+#define WS_ERR_CUDA 6             /* CUDA runtime / driver failure              */
+#define WS_ERR_NO_DEVICE 7        /* device op on a ledger-only pool            */
+#define WS_ERR_KV_BUSY 8          /* KV shrink would drop live blocks           */
+
+const char* ws_last_error(void);
+int ws_version(int* major, int* minor);
+
+/* ======================================================================
+ * Planning math — bit-exact float64 restatements of the reference's
+ * analytic model, used by the worker to size prewarm prefixes and by the
+ * engine adapter. All verified against golden vectors of the reference.
+ * ==================================================================== */
+
+/* cluster.py:145-166 required_prewarm_layers(spec, bandwidth, ref_input_tokens) */
+int ws_required_prewarm_layers(int64_t weight_bytes, int32_t parallelism, int32_t layers,
+                               double prefill_a_ms, double prefill_b_ms, double bandwidth,
+                               int32_t ref_input_tokens, int32_t* k_out);
+
+/* cluster.py:169-182 catchup_stall_ms(spec, layers_loaded, bandwidth, ref_input_tokens) */
+int ws_catchup_stall_ms(int64_t weight_bytes, int32_t parallelism, int32_t layers,
+                        double prefill_a_ms, double prefill_b_ms, int32_t layers_loaded,
+                        double bandwidth, int32_t ref_input_tokens, double* stall_out);
+
+/* cluster.py:185-197 reservation_target(M, C, R, K) = max(M*R/C, K + M/C) */
+int ws_reservation_target(double kv_capacity_bytes, int32_t max_batch, int32_t inflight,
+                          double kv_used_bytes, double* target_out);
+
+/* cluster.py:79-83 ModelSpec.partition_bytes / partition_pages */
+int ws_partition_pages(int64_t weight_bytes, int32_t parallelism, int64_t page_size,
+                       int64_t* partition_bytes_out, int64_t* partition_pages_out);
+
+typedef struct ws_transfer_plan {
+  int64_t total_bytes;
+  double bandwidth;          /* bytes / ms */
+  int64_t chunk_pages;
+  int64_t page_size;
+  int64_t n_chunks;
+  double first_chunk_map_ms;
+  double finish_ms;
+  double critical_path_stall_ms;
+} ws_transfer_plan;
+
+/* memswitch.py:59-98 pipelined_load + kernels.py:68-77 pipeline_finish */
+int ws_pipelined_load(int64_t total_bytes, double bandwidth, double map_ms_per_page,
+                      int64_t chunk_pages, int64_t page_size, ws_transfer_plan* out);
+
+/* memswitch.py:101-117 background_kv_mapping */
+int ws_background_kv_mapping(int64_t pages, double map_ms_per_page, double consumption_rate,
+                             double* stall_out);
+
+/* ======================================================================
+ * Page pool — one per GPU worker. Replaces the page ledger of
+ * GpuWorker (cluster.py:110-129) and the physical effects of the Cluster
+ * operations that touch it. device < 0 gives a ledger-only pool (host
+ * bookkeeping, identical page identities, no CUDA calls).
+ *
+ * Device pools pre-create every physical 2 MiB page with cuMemCreate and
+ * alias all of them into one "page window" VA at init, so converting pages
+ * between weight slots and the KV cache never calls the driver on the
+ * critical path; slot VAs (one reservation per prewarm slot, weights at its
+ * start — PAPER.md:420-453) are mapped at prewarm time and unmapped by a
+ * background worker (engine.py:615-632 async-unmap contract).
+ *
+ * Page identity rules (documented, deterministic; the reference pins only
+ * counts): a new slot takes the lowest-id free pages; promotion turns every
+ * free page into KV; a KV shrink returns the highest-id KV pages, migrating
+ * any live KV block that sits on one of them to the lowest-id unallocated
+ * KV page that stays.
+ * ==================================================================== */
+typedef struct ws_pool ws_pool;
+
+typedef struct ws_pool_counts {
+  int64_t total_pages;
+  int64_t free_pages;        /* cluster.py:127-129 */
+  int64_t slot_pages;        /* cluster.py:123-125 */
+  int64_t kv_pages_mapped;   /* cluster.py:118     */
+  int64_t kv_pages_used;     /* cluster.py:119     */
+  int64_t kv_capacity_pages; /* cluster.py:120     */
+  int64_t kv_pages_allocated;/* pages holding live KV blocks of open sequences */
+  int64_t n_slots;
+  int64_t pending_unmaps;
+} ws_pool_counts;
+
+int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out);
+int ws_pool_destroy(ws_pool* pool);
+int ws_pool_counts_get(ws_pool* pool, ws_pool_counts* out);
+/* Host copy of the page-ownership map: -1 free, -2 KV, >=0 owning slot id. */
+int ws_pool_owner_map(ws_pool* pool, int32_t* out, int64_t n);
+/* Device copy of the same map (device pools only), for parity checks. */
+int ws_pool_device_owner_map(ws_pool* pool, int32_t* host_out, int64_t n);
+/* Base of the page window (page p lives at base + p*page_size). */
+int ws_pool_window(ws_pool* pool, void** base_out);
+/* Measured driver cost of the last slot map / init (ms), for the μ report. */
+int ws_pool_timing(ws_pool* pool, double* init_ms, double* last_map_ms_per_page,
+                   double* last_unmap_ms_per_page);
+/* Wait for the background unmap worker to drain. */
+int ws_pool_sync_unmaps(ws_pool* pool);
+
+/* begin_prewarm (cluster.py:245-274): reserve a slot VA, take `pages` pages.
+ * map_now=1 maps all of them before returning (device pools); map_now=0 lets
+ * the caller drive ws_slot_map_chunk() from the pipelined loader. */
+int ws_slot_create(ws_pool* pool, int64_t slot_id, int64_t pages, int32_t map_now, void** va_out);
+/* Map pages [first, first+count) of the slot into its VA (memswitch.py:78-88
+ * per-chunk map step). */
+int ws_slot_map_chunk(ws_pool* pool, int64_t slot_id, int64_t first, int64_t count);
+/* evict_slot (cluster.py:276-289): pages return to the free list now, the
+ * slot VA is unmapped asynchronously after `fence_stream` drains (may be NULL). */
+int ws_slot_evict(ws_pool* pool, int64_t slot_id, void* fence_stream);
+int ws_slot_info(ws_pool* pool, int64_t slot_id, int64_t* pages_out, int64_t* mapped_out, void** va_out);
+int ws_slot_pages(ws_pool* pool, int64_t slot_id, int32_t* ids_out, int64_t cap, int64_t* n_out);
+
+/* promote_to_dedicated KV step (cluster.py:332-338): every free page becomes
+ * KV; capacity = mapped = the resulting KV page count. */
+int ws_kv_map_all(ws_pool* pool, void* stream, int64_t* kv_pages_out);
+/* reclaim_on_completion (cluster.py:351-365) page math + the shrink. */
+int ws_kv_reclaim(ws_pool* pool, int32_t inflight, int32_t max_batch, double kv_used_bytes,
+                  void* stream, int64_t* freed_bytes_out);
+/* Set kv_pages_mapped to an explicit count (grow from free / shrink). */
+int ws_kv_resize(ws_pool* pool, int64_t kv_pages, void* stream);
+/* release_instance KV step (cluster.py:377-381): all KV pages to free. */
+int ws_kv_release(ws_pool* pool, void* stream);
+
+/* ---- sequences on the paged KV pool (block = one page) ---- */
+/* Device block-table matrix [max_seqs, max_blocks] of int32 page ids. */
+int ws_pool_seq_config(ws_pool* pool, int32_t max_seqs, int32_t max_blocks);
+int ws_seq_open(ws_pool* pool, int32_t* seq_out);
+/* Ensure blocks for `n_blocks` total blocks; allocates lowest-id free KV pages. */
+int ws_seq_reserve(ws_pool* pool, int32_t seq, int32_t n_blocks, void* stream);
+int ws_seq_close(ws_pool* pool, int32_t seq);
+int ws_seq_blocks(ws_pool* pool, int32_t seq, int32_t* ids_out, int32_t cap, int32_t* n_out);
+int ws_pool_block_tables(ws_pool* pool, int32_t** dev_out, int32_t* max_blocks_out);
+
+/* Time (ms, CUDA events on `stream`) of the last switch kernel launch. */
+int ws_pool_last_switch(ws_pool* pool, double* kernel_ms_out, int64_t* entries_out);
+
+/* ======================================================================
+ * Layer streaming — the copy side of activate_instance(): copy byte ranges
+ * (layers k..L of a prewarmed slot) from pinned host memory or a peer
+ * device into the slot on a copy stream, one CUDA event per range; the
+ * compute stream waits per layer (engine.py:526-538 "cold" branch and
+ * cluster.py:169-182 catch-up semantics made physical).
+ * ==================================================================== */
+typedef struct ws_streamer ws_streamer;
+int ws_streamer_create(int32_t max_ranges, ws_streamer** out);
+int ws_streamer_destroy(ws_streamer* s);
+/* Enqueue copies of ranges[i] = {dst_offset, src_offset, bytes} (int64 x3). */
+int ws_streamer_start(ws_streamer* s, void* dst_base, const void* src_base, const int64_t* ranges,
+                      int32_t n_ranges, void* copy_stream);
+/* Make `stream` wait until range i has landed (no-op if i >= started). */
+int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream);
+/* ms from start to each range's completion (after sync). */
+int ws_streamer_times(ws_streamer* s, float* ms_out, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WARMSERVE_H_ */

@@ -1,0 +1,152 @@
+"""ctypes binding of the in-tree native library (include/warmserve.h).
+
+The library is the product path: if it is missing this module raises at
+import time — there is no Python or CPU fallback for anything it provides.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libwarmserve.so"
+
+WS_OK = 0
+WS_ERR_INVALID = 1
+WS_ERR_INSUFFICIENT = 2
+WS_ERR_DUPLICATE = 3
+WS_ERR_NO_SLOT = 4
+WS_ERR_STATE = 5
+WS_ERR_CUDA = 6
+WS_ERR_NO_DEVICE = 7
+WS_ERR_KV_BUSY = 8
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(no CPU fallback exists)"
+    )
+
+lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+
+i32, i64, f64, f32 = C.c_int32, C.c_int64, C.c_double, C.c_float
+vp = C.c_void_p
+P = C.POINTER
+
+
+class TransferPlanC(C.Structure):
+    _fields_ = [
+        ("total_bytes", i64),
+        ("bandwidth", f64),
+        ("chunk_pages", i64),
+        ("page_size", i64),
+        ("n_chunks", i64),
+        ("first_chunk_map_ms", f64),
+        ("finish_ms", f64),
+        ("critical_path_stall_ms", f64),
+    ]
+
+
+class PoolCounts(C.Structure):
+    _fields_ = [
+        ("total_pages", i64),
+        ("free_pages", i64),
+        ("slot_pages", i64),
+        ("kv_pages_mapped", i64),
+        ("kv_pages_used", i64),
+        ("kv_capacity_pages", i64),
+        ("kv_pages_allocated", i64),
+        ("n_slots", i64),
+        ("pending_unmaps", i64),
+    ]
+
+
+# name -> argtypes; every function returns int status.
+SIGNATURES: dict[str, list] = {
+    "ws_version": [P(C.c_int), P(C.c_int)],
+    "ws_required_prewarm_layers": [i64, i32, i32, f64, f64, f64, i32, P(i32)],
+    "ws_catchup_stall_ms": [i64, i32, i32, f64, f64, i32, f64, i32, P(f64)],
+    "ws_reservation_target": [f64, i32, i32, f64, P(f64)],
+    "ws_partition_pages": [i64, i32, i64, P(i64), P(i64)],
+    "ws_pipelined_load": [i64, f64, f64, i64, i64, P(TransferPlanC)],
+    "ws_background_kv_mapping": [i64, f64, f64, P(f64)],
+    "ws_pool_create": [i32, i64, i64, P(vp)],
+    "ws_pool_destroy": [vp],
+    "ws_pool_counts_get": [vp, P(PoolCounts)],
+    "ws_pool_owner_map": [vp, P(i32), i64],
+    "ws_pool_device_owner_map": [vp, P(i32), i64],
+    "ws_pool_window": [vp, P(vp)],
+    "ws_pool_timing": [vp, P(f64), P(f64), P(f64)],
+    "ws_pool_sync_unmaps": [vp],
+    "ws_slot_create": [vp, i64, i64, i32, P(vp)],
+    "ws_slot_map_chunk": [vp, i64, i64, i64],
+    "ws_slot_evict": [vp, i64, vp],
+    "ws_slot_info": [vp, i64, P(i64), P(i64), P(vp)],
+    "ws_slot_pages": [vp, i64, P(i32), i64, P(i64)],
+    "ws_kv_map_all": [vp, vp, P(i64)],
+    "ws_kv_reclaim": [vp, i32, i32, f64, vp, P(i64)],
+    "ws_kv_resize": [vp, i64, vp],
+    "ws_kv_release": [vp, vp],
+    "ws_pool_seq_config": [vp, i32, i32],
+    "ws_seq_open": [vp, P(i32)],
+    "ws_seq_reserve": [vp, i32, i32, vp],
+    "ws_seq_close": [vp, i32],
+    "ws_seq_blocks": [vp, i32, P(i32), i32, P(i32)],
+    "ws_pool_block_tables": [vp, P(vp), P(i32)],
+    "ws_pool_last_switch": [vp, P(f64), P(i64)],
+    "ws_streamer_create": [i32, P(vp)],
+    "ws_streamer_destroy": [vp],
+    "ws_streamer_start": [vp, vp, vp, P(i64), i32, vp],
+    "ws_streamer_wait": [vp, i32, vp],
+    "ws_streamer_times": [vp, P(f32), i32],
+}
+
+lib.ws_last_error.restype = C.c_char_p
+lib.ws_last_error.argtypes = []
+
+
+def _bind(name, argtypes):
+    fn = getattr(lib, name)
+    fn.argtypes = argtypes
+    fn.restype = C.c_int
+    return fn
+
+
+fns = {}
+
+
+def register(sigs: dict) -> None:
+    for name, argtypes in sigs.items():
+        fns[name] = _bind(name, argtypes)
+
+
+register(SIGNATURES)
+
+
+def call(name: str, *args) -> None:
+    rc = fns[name](*args)
+    if rc != WS_OK:
+        raise NativeError(rc, lib.ws_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return lib.ws_last_error().decode(errors="replace")
+
+
+def declared_symbols() -> list[str]:
+    """Every function include/warmserve.h declares (for the export test)."""
+    import re
+
+    hdr = Path(__file__).resolve().parent.parent / "include"
+    names = []
+    for h in sorted(hdr.glob("*.h")):
+        names += re.findall(r"^\s*(?:int|const char\*)\s+(ws_\w+)\s*\(", h.read_text(), re.M)
+    return names

@@ -1,0 +1,60 @@
+#include "driver.h"
+
+#include <cuda_runtime.h>
+#include <mutex>
+#include <string>
+
+#include "common.h"
+
+namespace ws {
+
+namespace {
+thread_local std::string g_err;
+Driver g_drv;
+bool g_ok = false;
+std::once_flag g_once;
+std::string g_load_err;
+
+template <typename F>
+bool load(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) {
+    g_load_err = std::string("driver entry point ") + name + " unavailable: " +
+                 cudaGetErrorString(e);
+    return false;
+  }
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+const Driver* driver() {
+  std::call_once(g_once, [] {
+    g_ok = load("cuMemCreate", &g_drv.cuMemCreate) && load("cuMemRelease", &g_drv.cuMemRelease) &&
+           load("cuMemAddressReserve", &g_drv.cuMemAddressReserve) &&
+           load("cuMemAddressFree", &g_drv.cuMemAddressFree) && load("cuMemMap", &g_drv.cuMemMap) &&
+           load("cuMemUnmap", &g_drv.cuMemUnmap) && load("cuMemSetAccess", &g_drv.cuMemSetAccess) &&
+           load("cuMemGetAllocationGranularity", &g_drv.cuMemGetAllocationGranularity) &&
+           load("cuTensorMapEncodeTiled", &g_drv.cuTensorMapEncodeTiled) &&
+           load("cuGetErrorString", &g_drv.cuGetErrorString);
+  });
+  if (!g_ok) {
+    set_error(g_load_err);
+    return nullptr;
+  }
+  return &g_drv;
+}
+
+}  // namespace ws
+
+extern "C" const char* ws_last_error(void) { return ws::last_error(); }
+extern "C" int ws_version(int* major, int* minor) {
+  *major = 0;
+  *minor = 1;
+  return WS_OK;
+}

@@ -1,0 +1,701 @@
+// Per-GPU page pool: the page ledger of a universal worker and the CUDA VMM
+// pages behind it.
+//
+// Host ledger (single writer, mutated synchronously before device work is
+// enqueued — cluster.py:200-201) replaces GpuWorker's page counters
+// (cluster.py:110-129) and adds page identities. Device pools own every
+// physical 2 MiB page (cuMemCreate at init), alias them all into
+// one page-window VA so KV blocks address physical pages directly (weight<->KV
+// conversion needs no driver call), map each prewarm slot's pages into its own
+// VA reservation (weights at the slot start) and unmap
+// evicted slots on a background worker (async-unmap contract,
+// engine.py:615-632).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+#include "driver.h"
+#include "switch.cuh"
+
+using ws::kOwnerFree;
+using ws::kOwnerKV;
+
+namespace {
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+struct Slot {
+  std::vector<int32_t> pages;  // slot page j -> physical page id
+  int64_t mapped = 0;          // pages [0, mapped) mapped into the slot VA
+  int va = -1;                 // index into ws_pool::vas
+};
+
+struct VaRange {
+  CUdeviceptr base = 0;
+  bool busy = false;
+};
+
+struct UnmapJob {
+  int va;
+  CUdeviceptr base;  // copied at enqueue: ws_pool::vas may grow concurrently
+  int64_t mapped;
+  cudaEvent_t fence;
+};
+
+#define DRV(expr)                                                           \
+  do {                                                                      \
+    CUresult _r = (expr);                                                   \
+    if (_r != CUDA_SUCCESS) {                                               \
+      const char* _s = "?";                                                 \
+      if (ws::driver()) ws::driver()->cuGetErrorString(_r, &_s);            \
+      WS_FAIL(WS_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, _s, __FILE__, __LINE__); \
+    }                                                                       \
+  } while (0)
+
+}  // namespace
+
+struct ws_pool {
+  int dev = -1;
+  int64_t n = 0, page = 0;
+  // ---- host ledger ----
+  std::vector<int32_t> owner;   // -1 free, -2 KV, >=0 slot id
+  std::vector<int32_t> kv_seq;  // KV page -> sequence holding a block on it (-1 none)
+  std::vector<int32_t> kv_blk;  //          -> block index in that sequence
+  std::unordered_map<int64_t, Slot> slots;
+  int64_t n_free = 0, n_slot = 0, n_kv = 0, kv_cap = 0, kv_used = 0, n_alloc = 0;
+  // ---- sequences / block tables ----
+  int32_t max_seqs = 0, max_blocks = 0;
+  std::vector<int32_t> seq_len;
+  std::vector<char> seq_live;
+  int32_t* bt_host = nullptr;  // pinned on device pools
+  int32_t* bt_dev = nullptr;
+  // ---- device ----
+  const ws::Driver* drv = nullptr;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  CUdeviceptr window = 0;
+  int32_t* owner_dev = nullptr;
+  char* stage_host = nullptr;  // pinned staging for switch lists
+  char* stage_dev = nullptr;
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev = nullptr, sw_start = nullptr, sw_stop = nullptr;
+  bool sw_recorded = false;
+  int64_t sw_entries = 0;
+  std::vector<VaRange> vas;
+  // ---- background unmap worker ----
+  std::mutex mu;
+  std::condition_variable cv, cv_done;
+  std::deque<UnmapJob> jobs;
+  std::thread worker;
+  bool stop = false;
+  int64_t pending = 0;
+  double init_ms = 0, map_ms_per_page = 0, unmap_ms_per_page = 0;
+
+  bool on_device() const { return dev >= 0; }
+  CUdeviceptr va_base(int i) const { return vas[i].base; }
+};
+
+namespace {
+
+int check_pool(ws_pool* p) {
+  if (!p) WS_FAIL(WS_ERR_INVALID, "null pool");
+  return WS_OK;
+}
+
+// Apply a switch on the device: rules + explicit writes + migrations.
+int device_switch(ws_pool* p, const ws::SwitchRules& rules, const std::vector<int32_t>& set_pages,
+                  int32_t set_owner, const std::vector<ws::Migration>& migs, cudaStream_t stream) {
+  if (!p->on_device()) return WS_OK;
+  WS_CUDA(cudaSetDevice(p->dev));
+  size_t n_set = set_pages.size();
+  size_t need = n_set * 8 + migs.size() * sizeof(ws::Migration) + 64;
+  if (need > p->stage_bytes) WS_FAIL(WS_ERR_INVALID, "switch staging overflow");
+  // The staging buffer is reused: wait until the previous upload consumed it.
+  WS_CUDA(cudaEventSynchronize(p->stage_ev));
+  int32_t* h_pages = reinterpret_cast<int32_t*>(p->stage_host);
+  int32_t* h_owner = h_pages + n_set;
+  ws::Migration* h_migs = reinterpret_cast<ws::Migration*>(
+      p->stage_host + ((n_set * 8 + 15) / 16) * 16);
+  if (n_set) {
+    memcpy(h_pages, set_pages.data(), n_set * 4);
+    for (size_t i = 0; i < n_set; ++i) h_owner[i] = set_owner;
+  }
+  if (!migs.empty()) memcpy(h_migs, migs.data(), migs.size() * sizeof(ws::Migration));
+  size_t used = (size_t)((char*)(h_migs + migs.size()) - p->stage_host);
+  WS_CUDA(cudaEventRecord(p->sw_start, stream));
+  if (n_set || !migs.empty())
+    WS_CUDA(cudaMemcpyAsync(p->stage_dev, p->stage_host, used, cudaMemcpyHostToDevice, stream));
+  WS_CUDA(cudaEventRecord(p->stage_ev, stream));
+  ws::SwitchArgs a{};
+  a.owner = p->owner_dev;
+  a.n_pages = p->n;
+  a.rules = rules;
+  a.set_pages = reinterpret_cast<const int32_t*>(p->stage_dev);
+  a.set_owner = a.set_pages + n_set;
+  a.n_set = (int32_t)n_set;
+  a.migs = reinterpret_cast<const ws::Migration*>(p->stage_dev + ((char*)h_migs - p->stage_host));
+  a.n_mig = (int32_t)migs.size();
+  a.window = reinterpret_cast<char*>(p->window);
+  a.page_size = p->page;
+  a.block_tables = p->bt_dev;
+  a.max_blocks = p->max_blocks;
+  ws::launch_switch(a, stream);
+  WS_CUDA(cudaGetLastError());
+  WS_CUDA(cudaEventRecord(p->sw_stop, stream));
+  p->sw_recorded = true;
+  p->sw_entries = (int64_t)n_set + (int64_t)migs.size() + (rules.n ? p->n : 0);
+  return WS_OK;
+}
+
+ws::SwitchRules one_rule(int32_t from, int32_t to) {
+  ws::SwitchRules r{};
+  r.n = 1;
+  r.from[0] = from;
+  r.to[0] = to;
+  return r;
+}
+
+void unmap_worker(ws_pool* p) {
+  cudaSetDevice(p->dev);
+  for (;;) {
+    UnmapJob job;
+    {
+      std::unique_lock<std::mutex> lk(p->mu);
+      p->cv.wait(lk, [&] { return p->stop || !p->jobs.empty(); });
+      if (p->jobs.empty()) return;
+      job = p->jobs.front();
+      p->jobs.pop_front();
+    }
+    if (job.fence) {
+      cudaEventSynchronize(job.fence);
+      cudaEventDestroy(job.fence);
+    }
+    double t0 = now_ms();
+    for (int64_t j = 0; j < job.mapped; ++j) p->drv->cuMemUnmap(job.base + j * p->page, p->page);
+    double t1 = now_ms();
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (job.mapped) p->unmap_ms_per_page = (t1 - t0) / (double)job.mapped;
+    p->vas[job.va].busy = false;
+    p->pending -= 1;
+    p->cv_done.notify_all();
+  }
+}
+
+int acquire_va(ws_pool* p, int* out) {
+  std::lock_guard<std::mutex> lk(p->mu);
+  for (size_t i = 0; i < p->vas.size(); ++i)
+    if (!p->vas[i].busy) {
+      p->vas[i].busy = true;
+      *out = (int)i;
+      return WS_OK;
+    }
+  VaRange r;
+  DRV(p->drv->cuMemAddressReserve(&r.base, (size_t)(p->n * p->page), (size_t)p->page, 0, 0));
+  r.busy = true;
+  p->vas.push_back(r);
+  *out = (int)p->vas.size() - 1;
+  return WS_OK;
+}
+
+int map_range(ws_pool* p, Slot& s, int64_t first, int64_t count) {
+  if (first != s.mapped) WS_FAIL(WS_ERR_INVALID, "slot pages must be mapped in order");
+  if (first + count > (int64_t)s.pages.size()) WS_FAIL(WS_ERR_INVALID, "map beyond slot");
+  if (!p->on_device() || count == 0) {
+    s.mapped += count;
+    return WS_OK;
+  }
+  double t0 = now_ms();
+  CUdeviceptr base = p->va_base(s.va);
+  for (int64_t j = first; j < first + count; ++j)
+    DRV(p->drv->cuMemMap(base + j * p->page, (size_t)p->page, 0, p->handles[s.pages[j]], 0));
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = p->dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  DRV(p->drv->cuMemSetAccess(base + first * p->page, (size_t)(count * p->page), &acc, 1));
+  p->map_ms_per_page = (now_ms() - t0) / (double)count;
+  s.mapped += count;
+  return WS_OK;
+}
+
+// Remove n KV pages (highest ids), relocating live blocks. Host ledger first,
+// then one switch launch.
+int kv_shrink(ws_pool* p, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return WS_OK;
+  if (n > p->n_kv) WS_FAIL(WS_ERR_INVALID, "shrink %lld > kv %lld", (long long)n, (long long)p->n_kv);
+  std::vector<int32_t> victims;
+  victims.reserve(n);
+  for (int64_t q = p->n - 1; q >= 0 && (int64_t)victims.size() < n; --q)
+    if (p->owner[q] == kOwnerKV) victims.push_back((int32_t)q);
+  int32_t lowest_victim = victims.back();
+  std::vector<ws::Migration> migs;
+  int64_t cursor = 0;
+  for (auto it = victims.rbegin(); it != victims.rend(); ++it) {  // ascending page order
+    const int32_t v = *it;
+    if (p->kv_seq[v] < 0) continue;
+    while (cursor < lowest_victim && !(p->owner[cursor] == kOwnerKV && p->kv_seq[cursor] < 0)) ++cursor;
+    if (cursor >= lowest_victim)
+      WS_FAIL(WS_ERR_KV_BUSY, "KV shrink by %lld pages would drop live blocks", (long long)n);
+    migs.push_back({v, (int32_t)cursor, p->kv_seq[v], p->kv_blk[v]});
+    ++cursor;
+  }
+  for (const auto& m : migs) {
+    p->kv_seq[m.dst] = m.seq;
+    p->kv_blk[m.dst] = m.block;
+    p->bt_host[(int64_t)m.seq * p->max_blocks + m.block] = m.dst;
+  }
+  for (int32_t v : victims) {
+    p->owner[v] = kOwnerFree;
+    p->kv_seq[v] = -1;
+    p->kv_blk[v] = -1;
+  }
+  p->n_kv -= n;
+  p->n_free += n;
+  ws::SwitchRules none{};
+  return device_switch(p, none, victims, kOwnerFree, migs, stream);
+}
+
+int kv_grow(ws_pool* p, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return WS_OK;
+  if (n > p->n_free) WS_FAIL(WS_ERR_INSUFFICIENT, "insufficient pages (need %lld, free %lld)",
+                             (long long)n, (long long)p->n_free);
+  std::vector<int32_t> got;
+  for (int64_t q = 0; q < p->n && (int64_t)got.size() < n; ++q)
+    if (p->owner[q] == kOwnerFree) got.push_back((int32_t)q);
+  for (int32_t q : got) p->owner[q] = kOwnerKV;
+  p->n_free -= n;
+  p->n_kv += n;
+  ws::SwitchRules none{};
+  return device_switch(p, none, got, kOwnerKV, {}, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out) {
+  if (total_pages < 1 || page_size < 1) WS_FAIL(WS_ERR_INVALID, "pool needs pages and a page size");
+  if (total_pages > (int64_t)INT32_MAX) WS_FAIL(WS_ERR_INVALID, "too many pages");
+  ws_pool* p = new ws_pool();
+  p->dev = device;
+  p->n = total_pages;
+  p->page = page_size;
+  p->owner.assign(total_pages, kOwnerFree);
+  p->kv_seq.assign(total_pages, -1);
+  p->kv_blk.assign(total_pages, -1);
+  p->n_free = total_pages;
+  if (device >= 0) {
+    double t0 = now_ms();
+    auto fail = [&](int code) {
+      ws_pool_destroy(p);
+      return code;
+    };
+    p->drv = ws::driver();
+    if (!p->drv) return fail(WS_ERR_NO_DEVICE);
+    if (cudaSetDevice(device) != cudaSuccess || cudaFree(0) != cudaSuccess) {
+      ws::set_error("cudaSetDevice failed");
+      return fail(WS_ERR_NO_DEVICE);
+    }
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    size_t gran = 0;
+    if (p->drv->cuMemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) !=
+            CUDA_SUCCESS ||
+        page_size % (int64_t)gran != 0) {
+      ws::set_error("page size is not a multiple of the VMM granularity");
+      return fail(WS_ERR_INVALID);
+    }
+    if (p->drv->cuMemAddressReserve(&p->window, (size_t)(total_pages * page_size), (size_t)page_size,
+                                    0, 0) != CUDA_SUCCESS) {
+      ws::set_error("cuMemAddressReserve(window) failed");
+      return fail(WS_ERR_CUDA);
+    }
+    p->handles.resize(total_pages);
+    for (int64_t i = 0; i < total_pages; ++i) {
+      CUresult r = p->drv->cuMemCreate(&p->handles[i], (size_t)page_size, &prop, 0);
+      if (r == CUDA_SUCCESS) r = p->drv->cuMemMap(p->window + i * page_size, (size_t)page_size, 0,
+                                                  p->handles[i], 0);
+      if (r != CUDA_SUCCESS) {
+        p->handles.resize(i + (r == CUDA_SUCCESS ? 1 : 0));
+        ws::set_error("cuMemCreate/cuMemMap of the page window failed (out of HBM?)");
+        return fail(WS_ERR_CUDA);
+      }
+    }
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (p->drv->cuMemSetAccess(p->window, (size_t)(total_pages * page_size), &acc, 1) !=
+        CUDA_SUCCESS) {
+      ws::set_error("cuMemSetAccess(window) failed");
+      return fail(WS_ERR_CUDA);
+    }
+    p->stage_bytes = (size_t)total_pages * 24 + 4096;
+    if (cudaMalloc(&p->owner_dev, total_pages * 4) != cudaSuccess ||
+        cudaMemcpy(p->owner_dev, p->owner.data(), total_pages * 4, cudaMemcpyHostToDevice) !=
+            cudaSuccess ||
+        cudaHostAlloc(&p->stage_host, p->stage_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaMalloc(&p->stage_dev, p->stage_bytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->stage_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreate(&p->sw_start) != cudaSuccess || cudaEventCreate(&p->sw_stop) != cudaSuccess) {
+      ws::set_error("pool device buffers allocation failed");
+      return fail(WS_ERR_CUDA);
+    }
+    cudaEventRecord(p->stage_ev, 0);
+    p->worker = std::thread(unmap_worker, p);
+    p->init_ms = now_ms() - t0;
+  }
+  *out = p;
+  return WS_OK;
+}
+
+int ws_pool_destroy(ws_pool* p) {
+  if (!p) return WS_OK;
+  if (p->worker.joinable()) {
+    {
+      std::lock_guard<std::mutex> lk(p->mu);
+      p->stop = true;
+    }
+    p->cv.notify_all();
+    p->worker.join();
+  }
+  if (p->on_device() && p->drv) {
+    cudaSetDevice(p->dev);
+    cudaDeviceSynchronize();
+    for (auto& kv : p->slots)
+      for (int64_t j = 0; j < kv.second.mapped; ++j)
+        p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
+    for (auto& v : p->vas) p->drv->cuMemAddressFree(v.base, (size_t)(p->n * p->page));
+    for (size_t i = 0; i < p->handles.size(); ++i) p->drv->cuMemUnmap(p->window + i * p->page, p->page);
+    for (auto h : p->handles) p->drv->cuMemRelease(h);
+    if (p->window) p->drv->cuMemAddressFree(p->window, (size_t)(p->n * p->page));
+    if (p->owner_dev) cudaFree(p->owner_dev);
+    if (p->stage_dev) cudaFree(p->stage_dev);
+    if (p->stage_host) cudaFreeHost(p->stage_host);
+    if (p->bt_dev) cudaFree(p->bt_dev);
+    if (p->bt_host) cudaFreeHost(p->bt_host);
+    for (cudaEvent_t e : {p->stage_ev, p->sw_start, p->sw_stop})
+      if (e) cudaEventDestroy(e);
+  } else if (p->bt_host) {
+    free(p->bt_host);
+  }
+  delete p;
+  return WS_OK;
+}
+
+int ws_pool_counts_get(ws_pool* p, ws_pool_counts* o) {
+  if (int e = check_pool(p)) return e;
+  o->total_pages = p->n;
+  o->free_pages = p->n_free;
+  o->slot_pages = p->n_slot;
+  o->kv_pages_mapped = p->n_kv;
+  o->kv_pages_used = p->kv_used;
+  o->kv_capacity_pages = p->kv_cap;
+  o->kv_pages_allocated = p->n_alloc;
+  o->n_slots = (int64_t)p->slots.size();
+  std::lock_guard<std::mutex> lk(p->mu);
+  o->pending_unmaps = p->pending;
+  return WS_OK;
+}
+
+int ws_pool_owner_map(ws_pool* p, int32_t* out, int64_t n) {
+  if (int e = check_pool(p)) return e;
+  if (n < p->n) WS_FAIL(WS_ERR_INVALID, "buffer too small");
+  memcpy(out, p->owner.data(), p->n * 4);
+  return WS_OK;
+}
+
+int ws_pool_device_owner_map(ws_pool* p, int32_t* out, int64_t n) {
+  if (int e = check_pool(p)) return e;
+  if (!p->on_device()) WS_FAIL(WS_ERR_NO_DEVICE, "ledger-only pool");
+  if (n < p->n) WS_FAIL(WS_ERR_INVALID, "buffer too small");
+  WS_CUDA(cudaSetDevice(p->dev));
+  WS_CUDA(cudaDeviceSynchronize());
+  WS_CUDA(cudaMemcpy(out, p->owner_dev, p->n * 4, cudaMemcpyDeviceToHost));
+  return WS_OK;
+}
+
+int ws_pool_window(ws_pool* p, void** base) {
+  if (int e = check_pool(p)) return e;
+  if (!p->on_device()) WS_FAIL(WS_ERR_NO_DEVICE, "ledger-only pool");
+  *base = reinterpret_cast<void*>(p->window);
+  return WS_OK;
+}
+
+int ws_pool_timing(ws_pool* p, double* init_ms, double* map_pp, double* unmap_pp) {
+  if (int e = check_pool(p)) return e;
+  std::lock_guard<std::mutex> lk(p->mu);
+  *init_ms = p->init_ms;
+  *map_pp = p->map_ms_per_page;
+  *unmap_pp = p->unmap_ms_per_page;
+  return WS_OK;
+}
+
+int ws_pool_sync_unmaps(ws_pool* p) {
+  if (int e = check_pool(p)) return e;
+  std::unique_lock<std::mutex> lk(p->mu);
+  p->cv_done.wait(lk, [&] { return p->pending == 0; });
+  return WS_OK;
+}
+
+int ws_slot_create(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map_now, void** va_out) {
+  if (int e = check_pool(p)) return e;
+  if (slot_id < 0 || slot_id > INT32_MAX) WS_FAIL(WS_ERR_INVALID, "slot id out of range");
+  if (p->slots.count(slot_id)) WS_FAIL(WS_ERR_DUPLICATE, "already holds slot %lld", (long long)slot_id);
+  if (pages < 0) WS_FAIL(WS_ERR_INVALID, "negative page count");
+  if (pages > p->n_free)
+    WS_FAIL(WS_ERR_INSUFFICIENT, "insufficient pages (need %lld, free %lld)", (long long)pages,
+            (long long)p->n_free);
+  Slot s;
+  s.pages.reserve(pages);
+  for (int64_t q = 0; q < p->n && (int64_t)s.pages.size() < pages; ++q)
+    if (p->owner[q] == kOwnerFree) s.pages.push_back((int32_t)q);
+  if (p->on_device()) {
+    WS_CUDA(cudaSetDevice(p->dev));
+    if (int e = acquire_va(p, &s.va)) return e;
+  }
+  for (int32_t q : s.pages) p->owner[q] = (int32_t)slot_id;
+  p->n_free -= pages;
+  p->n_slot += pages;
+  Slot& ref = p->slots[slot_id] = std::move(s);
+  ws::SwitchRules none{};
+  if (int e = device_switch(p, none, ref.pages, (int32_t)slot_id, {}, 0)) return e;
+  if (map_now)
+    if (int e = map_range(p, ref, 0, pages)) return e;
+  if (va_out) *va_out = p->on_device() ? reinterpret_cast<void*>(p->va_base(ref.va)) : nullptr;
+  return WS_OK;
+}
+
+int ws_slot_map_chunk(ws_pool* p, int64_t slot_id, int64_t first, int64_t count) {
+  if (int e = check_pool(p)) return e;
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  return map_range(p, it->second, first, count);
+}
+
+int ws_slot_evict(ws_pool* p, int64_t slot_id, void* fence_stream) {
+  if (int e = check_pool(p)) return e;
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  Slot s = std::move(it->second);
+  p->slots.erase(it);
+  for (int32_t q : s.pages) p->owner[q] = kOwnerFree;
+  p->n_free += (int64_t)s.pages.size();
+  p->n_slot -= (int64_t)s.pages.size();
+  if (!p->on_device()) return WS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(fence_stream);
+  if (int e = device_switch(p, one_rule((int32_t)slot_id, kOwnerFree), {}, 0, {}, st)) return e;
+  UnmapJob job{s.va, p->va_base(s.va), s.mapped, nullptr};
+  WS_CUDA(cudaEventCreateWithFlags(&job.fence, cudaEventDisableTiming));
+  WS_CUDA(cudaEventRecord(job.fence, st));
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->jobs.push_back(job);
+    p->pending += 1;
+  }
+  p->cv.notify_all();
+  return WS_OK;
+}
+
+int ws_slot_info(ws_pool* p, int64_t slot_id, int64_t* pages, int64_t* mapped, void** va) {
+  if (int e = check_pool(p)) return e;
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  if (pages) *pages = (int64_t)it->second.pages.size();
+  if (mapped) *mapped = it->second.mapped;
+  if (va) *va = p->on_device() ? reinterpret_cast<void*>(p->va_base(it->second.va)) : nullptr;
+  return WS_OK;
+}
+
+int ws_slot_pages(ws_pool* p, int64_t slot_id, int32_t* ids, int64_t cap, int64_t* n_out) {
+  if (int e = check_pool(p)) return e;
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  int64_t n = (int64_t)it->second.pages.size();
+  *n_out = n;
+  if (ids) memcpy(ids, it->second.pages.data(), std::min(n, cap) * 4);
+  return WS_OK;
+}
+
+int ws_kv_map_all(ws_pool* p, void* stream, int64_t* kv_out) {
+  if (int e = check_pool(p)) return e;
+  for (int64_t q = 0; q < p->n; ++q)
+    if (p->owner[q] == kOwnerFree) p->owner[q] = kOwnerKV;
+  p->n_kv += p->n_free;
+  p->n_free = 0;
+  p->kv_cap = p->n_kv;
+  if (kv_out) *kv_out = p->n_kv;
+  return device_switch(p, one_rule(kOwnerFree, kOwnerKV), {}, 0, {},
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ws_kv_reclaim(ws_pool* p, int32_t inflight, int32_t max_batch, double kv_used_bytes,
+                  void* stream, int64_t* freed_out) {
+  if (int e = check_pool(p)) return e;
+  // cluster.py:358-363. capacity is an exact integer byte count; `used` is
+  // min(kv_used, capacity), whichever type wins in the reference.
+  const int64_t cap_bytes = p->kv_cap * p->page;
+  const double used = (double)cap_bytes < kv_used_bytes ? (double)cap_bytes : kv_used_bytes;
+  // The reference records kv_pages_used before Eq. 1 validates its inputs.
+  p->kv_used = (int64_t)std::ceil(used / (double)p->page);
+  if (inflight < 0 || inflight > max_batch)
+    WS_FAIL(WS_ERR_INVALID, "inflight %d outside [0, %d]", inflight, max_batch);
+  if (used < 0) WS_FAIL(WS_ERR_INVALID, "kv_used %.17g outside [0, %lld]", used, (long long)cap_bytes);
+  // Eq. 1 with M an exact integer: M*R is exact, then one rounding per op.
+  const double expect = (double)(cap_bytes * (int64_t)inflight) / (double)max_batch;
+  const double buffer = used + (double)cap_bytes / (double)max_batch;
+  const double target = expect >= buffer ? expect : buffer;
+  const double reserved = (double)(p->n_kv * p->page);
+  int64_t freed = (int64_t)std::floor((reserved - target) / (double)p->page);
+  if (freed < 0) freed = 0;
+  if (int e = kv_shrink(p, freed, reinterpret_cast<cudaStream_t>(stream))) return e;
+  *freed_out = freed * p->page;
+  return WS_OK;
+}
+
+int ws_kv_resize(ws_pool* p, int64_t kv_pages, void* stream) {
+  if (int e = check_pool(p)) return e;
+  if (kv_pages < 0) WS_FAIL(WS_ERR_INVALID, "negative KV size");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (kv_pages < p->n_kv) return kv_shrink(p, p->n_kv - kv_pages, st);
+  return kv_grow(p, kv_pages - p->n_kv, st);
+}
+
+int ws_kv_release(ws_pool* p, void* stream) {
+  if (int e = check_pool(p)) return e;
+  if (p->n_alloc) WS_FAIL(WS_ERR_KV_BUSY, "KV release with %lld live blocks", (long long)p->n_alloc);
+  for (int64_t q = 0; q < p->n; ++q)
+    if (p->owner[q] == kOwnerKV) p->owner[q] = kOwnerFree;
+  p->n_free += p->n_kv;
+  p->n_kv = p->kv_cap = p->kv_used = 0;
+  return device_switch(p, one_rule(kOwnerKV, kOwnerFree), {}, 0, {},
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- sequences
+
+int ws_pool_seq_config(ws_pool* p, int32_t max_seqs, int32_t max_blocks) {
+  if (int e = check_pool(p)) return e;
+  if (max_seqs < 1 || max_blocks < 1) WS_FAIL(WS_ERR_INVALID, "bad sequence table shape");
+  if (p->n_alloc) WS_FAIL(WS_ERR_STATE, "sequences still hold KV blocks");
+  size_t bytes = (size_t)max_seqs * max_blocks * 4;
+  if (p->on_device()) {
+    WS_CUDA(cudaSetDevice(p->dev));
+    if (p->bt_dev) cudaFree(p->bt_dev);
+    if (p->bt_host) cudaFreeHost(p->bt_host);
+    p->bt_dev = nullptr;
+    p->bt_host = nullptr;
+    WS_CUDA(cudaHostAlloc(&p->bt_host, bytes, cudaHostAllocDefault));
+    WS_CUDA(cudaMalloc(&p->bt_dev, bytes));
+    WS_CUDA(cudaMemset(p->bt_dev, 0xff, bytes));
+  } else {
+    free(p->bt_host);
+    p->bt_host = static_cast<int32_t*>(malloc(bytes));
+  }
+  memset(p->bt_host, 0xff, bytes);
+  p->max_seqs = max_seqs;
+  p->max_blocks = max_blocks;
+  p->seq_len.assign(max_seqs, 0);
+  p->seq_live.assign(max_seqs, 0);
+  return WS_OK;
+}
+
+int ws_seq_open(ws_pool* p, int32_t* seq_out) {
+  if (int e = check_pool(p)) return e;
+  for (int32_t s = 0; s < p->max_seqs; ++s)
+    if (!p->seq_live[s]) {
+      p->seq_live[s] = 1;
+      p->seq_len[s] = 0;
+      *seq_out = s;
+      return WS_OK;
+    }
+  WS_FAIL(WS_ERR_INSUFFICIENT, "no free sequence rows (max %d)", p->max_seqs);
+}
+
+int ws_seq_reserve(ws_pool* p, int32_t seq, int32_t n_blocks, void* stream) {
+  if (int e = check_pool(p)) return e;
+  if (seq < 0 || seq >= p->max_seqs || !p->seq_live[seq]) WS_FAIL(WS_ERR_INVALID, "bad sequence %d", seq);
+  if (n_blocks > p->max_blocks) WS_FAIL(WS_ERR_INVALID, "sequence exceeds %d blocks", p->max_blocks);
+  int32_t have = p->seq_len[seq];
+  if (n_blocks <= have) return WS_OK;
+  std::vector<int32_t> got;
+  for (int64_t q = 0; q < p->n && (int32_t)got.size() < n_blocks - have; ++q)
+    if (p->owner[q] == kOwnerKV && p->kv_seq[q] < 0) got.push_back((int32_t)q);
+  if ((int32_t)got.size() < n_blocks - have)
+    WS_FAIL(WS_ERR_INSUFFICIENT, "insufficient pages (need %d KV blocks, free %d)", n_blocks - have,
+            (int)got.size());
+  int32_t* row = p->bt_host + (int64_t)seq * p->max_blocks;
+  for (int32_t i = 0; i < (int32_t)got.size(); ++i) {
+    p->kv_seq[got[i]] = seq;
+    p->kv_blk[got[i]] = have + i;
+    row[have + i] = got[i];
+  }
+  p->n_alloc += (int64_t)got.size();
+  p->seq_len[seq] = n_blocks;
+  if (p->on_device()) {
+    WS_CUDA(cudaSetDevice(p->dev));
+    WS_CUDA(cudaMemcpyAsync(p->bt_dev + (int64_t)seq * p->max_blocks + have, row + have,
+                            (size_t)(n_blocks - have) * 4, cudaMemcpyHostToDevice,
+                            reinterpret_cast<cudaStream_t>(stream)));
+  }
+  return WS_OK;
+}
+
+int ws_seq_close(ws_pool* p, int32_t seq) {
+  if (int e = check_pool(p)) return e;
+  if (seq < 0 || seq >= p->max_seqs || !p->seq_live[seq]) WS_FAIL(WS_ERR_INVALID, "bad sequence %d", seq);
+  int32_t* row = p->bt_host + (int64_t)seq * p->max_blocks;
+  for (int32_t i = 0; i < p->seq_len[seq]; ++i) {
+    p->kv_seq[row[i]] = -1;
+    p->kv_blk[row[i]] = -1;
+    row[i] = -1;
+  }
+  p->n_alloc -= p->seq_len[seq];
+  p->seq_len[seq] = 0;
+  p->seq_live[seq] = 0;
+  return WS_OK;  // stale device entries are never read: the row is dead
+}
+
+int ws_seq_blocks(ws_pool* p, int32_t seq, int32_t* ids, int32_t cap, int32_t* n_out) {
+  if (int e = check_pool(p)) return e;
+  if (seq < 0 || seq >= p->max_seqs) WS_FAIL(WS_ERR_INVALID, "bad sequence %d", seq);
+  *n_out = p->seq_len[seq];
+  if (ids) memcpy(ids, p->bt_host + (int64_t)seq * p->max_blocks, std::min(cap, p->seq_len[seq]) * 4);
+  return WS_OK;
+}
+
+int ws_pool_block_tables(ws_pool* p, int32_t** dev_out, int32_t* max_blocks_out) {
+  if (int e = check_pool(p)) return e;
+  *dev_out = p->bt_dev;
+  *max_blocks_out = p->max_blocks;
+  return WS_OK;
+}
+
+int ws_pool_last_switch(ws_pool* p, double* kernel_ms, int64_t* entries) {
+  if (int e = check_pool(p)) return e;
+  if (!p->on_device() || !p->sw_recorded) {
+    *kernel_ms = 0;
+    *entries = 0;
+    return WS_OK;
+  }
+  WS_CUDA(cudaEventSynchronize(p->sw_stop));
+  float ms = 0;
+  WS_CUDA(cudaEventElapsedTime(&ms, p->sw_start, p->sw_stop));
+  *kernel_ms = ms;
+  *entries = p->sw_entries;
+  return WS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Layer streamer: the copy half of a cold activation. Copies layers k..L of a
+// prewarmed slot from pinned host memory (PCIe Gen5) or a peer GPU's HBM
+// (NVLink 5, cudaMemcpyDefault resolves peer addresses) on a DMA copy engine,
+// recording one event per layer so the compute stream waits layer by layer —
+// the physical form of catch-up streaming (cluster.py:169-182,
+// engine.py:513-538). No SM cycles are spent on the copy.
+#include <vector>
+
+#include "common.h"
+
+struct ws_streamer {
+  std::vector<cudaEvent_t> done;  // per range, timing-enabled
+  cudaEvent_t start = nullptr;
+  int32_t started = 0;
+};
+
+extern "C" {
+
+int ws_streamer_create(int32_t max_ranges, ws_streamer** out) {
+  if (max_ranges < 1) WS_FAIL(WS_ERR_INVALID, "streamer needs at least one range");
+  ws_streamer* s = new ws_streamer();
+  s->done.resize(max_ranges, nullptr);
+  if (cudaEventCreate(&s->start) != cudaSuccess) {
+    delete s;
+    WS_FAIL(WS_ERR_CUDA, "cudaEventCreate failed");
+  }
+  for (auto& e : s->done)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      ws_streamer_destroy(s);
+      WS_FAIL(WS_ERR_CUDA, "cudaEventCreate failed");
+    }
+  *out = s;
+  return WS_OK;
+}
+
+int ws_streamer_destroy(ws_streamer* s) {
+  if (!s) return WS_OK;
+  if (s->start) cudaEventDestroy(s->start);
+  for (auto e : s->done)
+    if (e) cudaEventDestroy(e);
+  delete s;
+  return WS_OK;
+}
+
+int ws_streamer_start(ws_streamer* s, void* dst_base, const void* src_base, const int64_t* ranges,
+                      int32_t n, void* copy_stream) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  if (n < 0 || n > (int32_t)s->done.size()) WS_FAIL(WS_ERR_INVALID, "too many ranges");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(copy_stream);
+  WS_CUDA(cudaEventRecord(s->start, st));
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t dst_off = ranges[3 * i], src_off = ranges[3 * i + 1], bytes = ranges[3 * i + 2];
+    if (bytes > 0)
+      WS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst_base) + dst_off,
+                              static_cast<const char*>(src_base) + src_off, (size_t)bytes,
+                              cudaMemcpyDefault, st));
+    WS_CUDA(cudaEventRecord(s->done[i], st));
+  }
+  s->started = n;
+  return WS_OK;
+}
+
+int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  if (i < 0 || i >= s->started) return WS_OK;
+  WS_CUDA(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), s->done[i], 0));
+  return WS_OK;
+}
+
+int ws_streamer_times(ws_streamer* s, float* ms_out, int32_t n) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  for (int32_t i = 0; i < n && i < s->started; ++i) {
+    WS_CUDA(cudaEventSynchronize(s->done[i]));
+    WS_CUDA(cudaEventElapsedTime(&ms_out[i], s->start, s->done[i]));
+  }
+  return WS_OK;
+}
+
+}  // extern "C"
