@@ -184,6 +184,60 @@ int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream);
 /* ms from start to each range's completion (after sync). */
 int ws_streamer_times(ws_streamer* s, float* ms_out, int32_t n);
 
+/* ======================================================================
+ * Model forward on the paged pool — the compute half of
+ * activate_instance() and the prefill/decode the reference models with
+ * LatencyModel (engine.py:97-116, a18) and _kv_used_bytes (engine.py:391-404).
+ * Llama-family decoder (RMSNorm, RoPE rotate_half, GQA, SwiGLU), bf16
+ * weights, fp32 residual stream, sm_100a kernels.
+ * ==================================================================== */
+typedef struct ws_model_config {
+  int32_t layers, hidden, ffn, heads, kv_heads, head_dim, vocab;
+  float rope_theta, rms_eps;
+  int32_t qkv_bias;       /* Qwen2.5-style q/k/v biases */
+  int32_t max_positions;  /* RoPE table length */
+} ws_model_config;
+
+/* Weight layout of one (TP-partition of a) model inside its slot: byte
+ * offsets, every tensor 256-byte aligned. offsets_out receives
+ * [embed, final_norm, lm_head, total] then per layer
+ * [begin, attn_norm, wqkv, bqkv(-1 if none), wo, ffn_norm, wgu, wdown, end]
+ * (4 + 9*layers int64). Layer l occupies [begin, end) contiguously, in
+ * order, so layers k..L-1 + final_norm + lm_head form one suffix range. */
+int ws_model_layout(const ws_model_config* cfg, int64_t* offsets_out, int64_t n);
+/* Tokens per KV block (one pool page) and KV bytes per token (engine.py a19). */
+int ws_model_kv_geometry(const ws_model_config* cfg, int64_t page_size, int32_t* tokens_per_block,
+                         int64_t* kv_bytes_per_token);
+
+typedef struct ws_model ws_model;
+int ws_model_create(const ws_model_config* cfg, int32_t device, ws_model** out);
+int ws_model_destroy(ws_model* m);
+int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* bytes_out);
+/* 0 = tensor-core GEMM (default), 1 = legacy mma.sync baseline (tests / A-B). */
+int ws_model_set_gemm(ws_model* m, int32_t impl);
+
+/* Prefill `rows` new tokens of sequence `seq` (positions pos0..pos0+rows-1;
+ * blocks must be reserved). `weights` is the slot VA. If `streamer` is set,
+ * layer l >= first_streamed waits for range (l - first_streamed) and the
+ * final norm + lm_head wait for range (layers - first_streamed): the
+ * layer-streamed cold start. Writes last-row logits (fp32 [vocab]) and the
+ * greedy next token. */
+int ws_model_prefill(ws_model* m, ws_pool* pool, const void* weights, int32_t seq,
+                     const int32_t* tokens_dev, int32_t rows, int32_t pos0, ws_streamer* streamer,
+                     int32_t first_streamed, void* workspace, float* logits_dev,
+                     int32_t* next_token_dev, void* stream);
+
+/* One decode step for n sequences: seqs/pos/tokens are device int32[n];
+ * max_ctx >= max(pos)+1 bounds the split-K grid. logits fp32 [n, vocab]. */
+int ws_model_decode(ws_model* m, ws_pool* pool, const void* weights, const int32_t* seqs_dev,
+                    const int32_t* pos_dev, const int32_t* tokens_dev, int32_t n, int32_t max_ctx,
+                    void* workspace, float* logits_dev, int32_t* next_tokens_dev, void* stream);
+
+/* Standalone GEMM entry for tests/bench: C = A[M,K] * B[N,K]^T, epilogue
+ * 0 bf16, 1 bf16+bias, 2 fp32 accumulate, 3 fp32 store; impl as above. */
+int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
+            void* C, const void* bias, int32_t impl, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,89 @@
+"""TEST INFRASTRUCTURE ONLY — CPU fp32 logits oracle for the worker's forward.
+
+The reference has no model forward (logits are "parity
+unpinned" with respect to the reference). This oracle restates a
+Llama-family decoder in fp32 on the CPU — RMSNorm, rotate_half RoPE, causal
+GQA attention, SwiGLU — reading the SAME bf16 weight bytes the GPU uses,
+upcast to fp32, laid out by ``ws_model_layout``. It is pinned against
+HF ``transformers`` LlamaForCausalLM in tests/test_oracle_llama.py.
+
+The RoPE angle for pair i at position p is p * theta**(-2i/head_dim) in
+float64, rounded to fp32 cos/sin (the same table the device uses).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+
+def rope_table(head_dim: int, theta: float, n_pos: int) -> tuple[torch.Tensor, torch.Tensor]:
+    half = head_dim // 2
+    inv = np.array([float(theta) ** (-2.0 * i / head_dim) for i in range(half)], dtype=np.float64)
+    ang = np.arange(n_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return torch.from_numpy(np.cos(ang).astype(np.float32)), torch.from_numpy(np.sin(ang).astype(np.float32))
+
+
+def unpack(cfg, layout, flat_bf16: torch.Tensor) -> dict:
+    """Slice the flat bf16 weight image into fp32 tensors by name."""
+    out = {}
+    for name, off, shape in layout.tensors():
+        n = int(np.prod(shape))
+        out[name] = flat_bf16[off // 2: off // 2 + n].view(*shape).float()
+    return out
+
+
+def _rms(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
+
+
+def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    # x: [S, heads, hd]; rotate_half pairs (i, i + hd/2)
+    half = x.shape[-1] // 2
+    a, b = x[..., :half], x[..., half:]
+    c, s = cos[:, None, :], sin[:, None, :]
+    return torch.cat([a * c - b * s, b * c + a * s], dim=-1)
+
+
+def forward(cfg, w: dict, tokens, pos0: int = 0, past: list | None = None):
+    """Logits [S, vocab] for tokens at positions pos0.. with optional past
+    K/V (list per layer of (k [P, kvh, hd], v)). Returns (logits, new_past)."""
+    tokens = torch.as_tensor(tokens, dtype=torch.long)
+    S = tokens.numel()
+    H, KV, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
+    cos, sin = rope_table(hd, cfg.rope_theta, pos0 + S)
+    cos, sin = cos[pos0:], sin[pos0:]
+    x = w["embed"][tokens]
+    new_past = []
+    for l in range(cfg.layers):
+        h = _rms(x, w[f"l{l}.attn_norm"], cfg.rms_eps)
+        qkv = h @ w[f"l{l}.wqkv"].T
+        if f"l{l}.bqkv" in w:
+            qkv = qkv + w[f"l{l}.bqkv"]
+        q = qkv[:, : H * hd].view(S, H, hd)
+        k = qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd)
+        v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+        q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+        if past is not None:
+            k = torch.cat([past[l][0], k], 0)
+            v = torch.cat([past[l][1], v], 0)
+        new_past.append((k, v))
+        T = k.shape[0]
+        g = H // KV
+        kk = k.repeat_interleave(g, dim=1)  # [T, H, hd]
+        vv = v.repeat_interleave(g, dim=1)
+        sc = torch.einsum("shd,thd->hst", q, kk) / math.sqrt(hd)
+        qpos = torch.arange(pos0, pos0 + S)[:, None]
+        kpos = torch.arange(T)[None, :]
+        sc = sc.masked_fill((kpos > qpos)[None], float("-inf"))
+        p = torch.softmax(sc, dim=-1)
+        o = torch.einsum("hst,thd->shd", p, vv).reshape(S, H * hd)
+        x = x + o @ w[f"l{l}.wo"].T
+        h = _rms(x, w[f"l{l}.ffn_norm"], cfg.rms_eps)
+        gu = h @ w[f"l{l}.wgu"].T
+        gate, up = gu[:, : cfg.ffn], gu[:, cfg.ffn:]
+        x = x + (torch.nn.functional.silu(gate) * up) @ w[f"l{l}.wdown"].T
+    h = _rms(x, w["final_norm"], cfg.rms_eps)
+    return h @ w["lm_head"].T, new_past

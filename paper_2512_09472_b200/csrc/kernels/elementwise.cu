@@ -1,0 +1,209 @@
+// HBM-bound per-token kernels: embedding gather, RMSNorm, SwiGLU, RoPE +
+// paged KV append, argmax. Each moves 16-byte vectors with one row (or one
+// token x head) per CTA/warp; grids cover all rows so every SM streams.
+#include "../common.h"
+#include "device.cuh"
+#include "ops.cuh"
+
+namespace ws {
+namespace {
+
+using namespace dev;
+
+// x[r, :] = float(E[tok[r], :])
+__global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ tok,
+                                                    const bf16* __restrict__ table,
+                                                    float* __restrict__ x, int d) {
+  const int r = blockIdx.x;
+  const int64_t t = tok[r];
+  const uint4* src = reinterpret_cast<const uint4*>(table + t * d);
+  float4* dst = reinterpret_cast<float4*>(x + (int64_t)r * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    uint4 v = __ldg(src + i);
+    float2 a = unpack_bf16x2(v.x), b = unpack_bf16x2(v.y), c = unpack_bf16x2(v.z),
+           e = unpack_bf16x2(v.w);
+    dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+    dst[2 * i + 1] = make_float4(c.x, c.y, e.x, e.y);
+  }
+}
+
+// out = bf16(x * rsqrt(mean(x^2) + eps) * w), fp32 math. One CTA per row.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const float* __restrict__ x,
+                                                          const bf16* __restrict__ w,
+                                                          bf16* __restrict__ out, int d, float eps) {
+  const int r = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)r * d);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d / 4; i += kThreads) {
+    float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[kThreads / 32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  const uint2* wr = reinterpret_cast<const uint2*>(w);
+  uint2* orow = reinterpret_cast<uint2*>(out + (int64_t)r * d);
+  for (int i = threadIdx.x; i < d / 4; i += kThreads) {
+    float4 v = xr[i];
+    uint2 wv = __ldg(wr + i);
+    float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
+    uint2 o;
+    o.x = pack_bf16x2(v.x * inv * w0.x, v.y * inv * w0.y);
+    o.y = pack_bf16x2(v.z * inv * w1.x, v.w * inv * w1.y);
+    orow[i] = o;
+  }
+}
+
+// act[r, j] = silu(g) * u with g = gu[r, j], u = gu[r, ffn + j].
+__global__ void __launch_bounds__(256) silu_mul_kernel(const bf16* __restrict__ gu,
+                                                       bf16* __restrict__ act, int ffn) {
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 8-element group
+  if (i >= ffn / 8) return;
+  const uint4 g = __ldg(reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn) + i);
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn + ffn) + i);
+  const uint32_t* gp = &g.x;
+  const uint32_t* up = &u.x;
+  uint4 o;
+  uint32_t* op = &o.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 gv = unpack_bf16x2(gp[k]), uv = unpack_bf16x2(up[k]);
+    float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
+    op[k] = pack_bf16x2(s0 * uv.x, s1 * uv.y);
+  }
+  reinterpret_cast<uint4*>(act + (int64_t)r * ffn)[i] = o;
+}
+
+// One warp per (row, head slot); head slots: [0,H) q heads, [H, H+KV) k heads,
+// [H+KV, H+2KV) v heads. rotate_half RoPE on q and k (pairs i, i+hd/2),
+// k and v written to the paged cache.
+__global__ void __launch_bounds__(256) rope_kv_kernel(bf16* __restrict__ qkv,
+                                                      const float2* __restrict__ rope, KvGeom kv,
+                                                      int layer, int rows, int heads,
+                                                      const int32_t* __restrict__ seq_arr,
+                                                      const int32_t* __restrict__ pos_arr, int seq0,
+                                                      int pos0) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int slots = heads + 2 * kv.kv_heads;
+  const int r = warp / slots, hs = warp % slots;
+  if (r >= rows) return;
+  const int hd = kv.head_dim, half = hd / 2;
+  const int pos = pos_arr ? pos_arr[r] : pos0 + r;
+  const int seq = seq_arr ? seq_arr[r] : seq0;
+  bf16* vec = qkv + (int64_t)r * slots * hd + (int64_t)hs * hd;
+  const bool is_v = hs >= heads + kv.kv_heads;
+  const float2* cs = rope + (int64_t)pos * half;
+  bf16* dst = nullptr;
+  if (hs >= heads) {
+    const int kind = is_v ? 1 : 0;
+    const int h = is_v ? hs - heads - kv.kv_heads : hs - heads;
+    const int32_t page = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
+    dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page * kv.page_size) + kv.plane(layer, kind, h) +
+          (int64_t)(pos % kv.tpb) * hd;
+  }
+  for (int i = lane; i < half; i += 32) {
+    float a = bf2f(vec[i]), b = bf2f(vec[i + half]);
+    if (!is_v) {
+      const float2 c = cs[i];  // (cos, sin)
+      const float ra = a * c.x - b * c.y, rb = b * c.x + a * c.y;
+      a = ra;
+      b = rb;
+      vec[i] = f2bf(a);
+      vec[i + half] = f2bf(b);
+    }
+    if (dst) {
+      dst[i] = f2bf(a);
+      dst[i + half] = f2bf(b);
+    }
+  }
+}
+
+// Row-wise argmax over fp32 logits (first index on ties, like torch.argmax).
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V,
+                                                      int32_t* __restrict__ out) {
+  const int r = blockIdx.x;
+  const float* row = logits + (int64_t)r * V;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    float v = row[i];
+    if (v > best || (v == best && i < idx)) {
+      best = v;
+      idx = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x / 32;
+    best = threadIdx.x < nw ? sb[threadIdx.x] : -INFINITY;
+    idx = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ob > best || (ob == best && oi < idx)) {
+        best = ob;
+        idx = oi;
+      }
+    }
+    if (threadIdx.x == 0) out[r] = idx;
+  }
+}
+
+}  // namespace
+
+void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n, int d, cudaStream_t st) {
+  embed_kernel<<<n, 256, 0, st>>>(tokens, table, x, d);
+}
+
+void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, float eps,
+                    cudaStream_t st) {
+  if (d >= 2048)
+    rmsnorm_kernel<512><<<rows, 512, 0, st>>>(x, w, out, d, eps);
+  else
+    rmsnorm_kernel<128><<<rows, 128, 0, st>>>(x, w, out, d, eps);
+}
+
+void launch_silu_mul(const bf16* gu, bf16* act, int rows, int ffn, cudaStream_t st) {
+  dim3 grid((ffn / 8 + 255) / 256, rows);
+  silu_mul_kernel<<<grid, 256, 0, st>>>(gu, act, ffn);
+}
+
+void launch_rope_kv(bf16* qkv, const float2* rope, const KvGeom& kv, int layer, int rows, int heads,
+                    const int32_t* seq, const int32_t* pos, int seq0, int pos0, cudaStream_t st) {
+  const int64_t warps = (int64_t)rows * (heads + 2 * kv.kv_heads);
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  rope_kv_kernel<<<blocks, 256, 0, st>>>(qkv, rope, kv, layer, rows, heads, seq, pos, seq0, pos0);
+}
+
+void launch_argmax(const float* logits, int M, int V, int32_t* out, float*, cudaStream_t st) {
+  argmax_kernel<<<M, 1024, 0, st>>>(logits, V, out);
+}
+
+}  // namespace ws

@@ -1,0 +1,70 @@
+// Launchers of the model kernels. All activations are row-major with the
+// feature dimension contiguous; weights are [out, in] row-major (K-major for
+// both GEMM operands). The residual stream is fp32; everything a GEMM reads is
+// bf16.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ws {
+
+using bf16 = __nv_bfloat16;
+
+// Paged KV cache geometry: block = one pool page holding `tpb` tokens of every
+// layer; inside a page: [layer][k|v][kv_head][tpb][head_dim] bf16.
+struct KvGeom {
+  char* window;          // page window base (page p at window + p*page_size)
+  int64_t page_size;
+  const int32_t* block_tables;  // [max_seqs, max_blocks]
+  int32_t max_blocks;
+  int32_t tpb;           // tokens per block
+  int32_t layers, kv_heads, head_dim;
+
+  __host__ __device__ int64_t head_stride() const { return (int64_t)tpb * head_dim; }
+  // element offset of (layer, kind, head, slot 0) inside a page
+  __host__ __device__ int64_t plane(int layer, int kind, int head) const {
+    return (((int64_t)layer * 2 + kind) * kv_heads + head) * head_stride();
+  }
+};
+
+void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n_tokens, int d,
+                  cudaStream_t st);
+void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, float eps,
+                    cudaStream_t st);
+void launch_silu_mul(const bf16* gu, bf16* act, int rows, int ffn, cudaStream_t st);
+
+// q,k rotated in place inside qkv ([rows, (H+2KV)*hd]); k,v appended to the
+// paged cache at positions pos[r] of sequence seq[r] (both device arrays), or
+// pos0 + r / seq0 when the arrays are null (single-sequence prefill).
+void launch_rope_kv(bf16* qkv, const float2* rope_table, const KvGeom& kv, int layer, int rows,
+                    int heads, const int32_t* seq, const int32_t* pos, int seq0, int pos0,
+                    cudaStream_t st);
+
+// Causal GQA attention of one sequence's `rows` new queries (positions
+// pos0..pos0+rows-1) over its paged KV [0, pos0+rows). out: [rows, H*hd].
+void launch_attn_prefill(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq,
+                         int rows, int pos0, int heads, float scale, cudaStream_t st);
+
+// One query token per sequence: seqs[i] at position pos[i] (context pos+1,
+// its own K/V already appended). scratch: decode_scratch_floats() floats.
+void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,
+                        const int32_t* seqs, const int32_t* pos, int n_seqs, int heads,
+                        int max_ctx, float scale, float* scratch, cudaStream_t st);
+int decode_scratch_floats(int n_seqs, int heads, int head_dim, int max_ctx);
+
+// C[M,N] = A[M,K] * B[N,K]^T with epilogue:
+enum class Epi { kStoreBf16 = 0, kBiasBf16 = 1, kAddF32 = 2, kStoreF32 = 3 };
+// Dispatch: M >= 16 -> tensor-core GEMM, else the skinny GEMV.
+void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
+                 const bf16* bias, cudaStream_t st);
+// Legacy mma.sync GEMM (baseline + parity reference for the tcgen05 kernel).
+void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
+                     const bf16* bias, cudaStream_t st);
+// Skinny GEMM for M <= 16 (decode / lm_head rows): weight-streaming, HBM bound.
+void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
+                 const bf16* bias, cudaStream_t st);
+// Logits (fp32) for M rows and their argmax.
+void launch_argmax(const float* logits, int M, int V, int32_t* out, float* scratch, cudaStream_t st);
+
+}  // namespace ws

@@ -1,0 +1,330 @@
+// Llama-family forward on the paged pool: the compute half of
+// activate_instance() and the prefill/decode entry points.
+//
+// Weights live in the slot VA (contiguous per layer, layout below); KV lives
+// in pool pages addressed through the block tables; activations live in a
+// caller-provided workspace. The layer loop is host C++ issuing one stream of
+// kernels; for a layer-streamed cold start each layer first waits on the copy
+// event of its weights (ws_streamer_wait), so compute of resident layers
+// overlaps the copy of the rest (cluster.py:145-182).
+#include <cmath>
+#include <vector>
+
+#include "common.h"
+#include "kernels/ops.cuh"
+
+namespace ws {
+int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_tables,
+                 int32_t* max_blocks);
+}
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+  int64_t embed, final_norm, lm_head, total;
+  struct L {
+    int64_t begin, attn_norm, wqkv, bqkv, wo, ffn_norm, wgu, wdown, end;
+  };
+  std::vector<L> layers;
+};
+
+int qkv_dim(const ws_model_config& c) { return (c.heads + 2 * c.kv_heads) * c.head_dim; }
+
+bool valid_cfg(const ws_model_config& c) {
+  return c.layers > 0 && c.hidden > 0 && c.ffn > 0 && c.heads > 0 && c.kv_heads > 0 &&
+         c.heads % c.kv_heads == 0 && (c.head_dim == 64 || c.head_dim == 96 || c.head_dim == 128) &&
+         c.vocab > 0 && c.hidden % 32 == 0 && c.ffn % 32 == 0 && c.max_positions > 0 &&
+         c.heads / c.kv_heads <= 8;
+}
+
+Layout make_layout(const ws_model_config& c) {
+  Layout L;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    int64_t at = off;
+    off = align_up(off + bytes);
+    return at;
+  };
+  const int64_t d = c.hidden, q = qkv_dim(c), o = (int64_t)c.heads * c.head_dim;
+  L.embed = take((int64_t)c.vocab * d * 2);
+  for (int l = 0; l < c.layers; ++l) {
+    Layout::L x;
+    x.begin = off;
+    x.attn_norm = take(d * 2);
+    x.wqkv = take(q * d * 2);
+    x.bqkv = c.qkv_bias ? take(q * 2) : -1;
+    x.wo = take(d * o * 2);
+    x.ffn_norm = take(d * 2);
+    x.wgu = take(2 * (int64_t)c.ffn * d * 2);
+    x.wdown = take(d * c.ffn * 2);
+    x.end = off;
+    L.layers.push_back(x);
+  }
+  L.final_norm = take(d * 2);
+  L.lm_head = take((int64_t)c.vocab * d * 2);
+  L.total = off;
+  return L;
+}
+
+struct Workspace {
+  int64_t x, h, qkv, attn, gu, act, hl, seqs, scratch, total;
+};
+
+int decode_cap(int max_tokens) { return max_tokens < 256 ? max_tokens : 256; }
+
+Workspace make_ws(const ws_model_config& c, int T) {
+  Workspace w;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    int64_t at = off;
+    off = align_up(off + bytes);
+    return at;
+  };
+  const int64_t d = c.hidden;
+  w.x = take((int64_t)T * d * 4);
+  w.h = take((int64_t)T * d * 2);
+  w.qkv = take((int64_t)T * qkv_dim(c) * 2);
+  w.attn = take((int64_t)T * c.heads * c.head_dim * 2);
+  w.gu = take((int64_t)T * 2 * c.ffn * 2);
+  w.act = take((int64_t)T * c.ffn * 2);
+  w.hl = take((int64_t)T * d * 2);
+  w.seqs = take(4 * 4);
+  w.scratch = take((int64_t)ws::decode_scratch_floats(decode_cap(T), c.heads, c.head_dim,
+                                                      c.max_positions) * 4);
+  w.total = off;
+  return w;
+}
+
+}  // namespace
+
+struct ws_model {
+  ws_model_config cfg;
+  Layout layout;
+  int device = 0;
+  float2* rope = nullptr;  // [max_positions, head_dim/2] (cos, sin)
+  int gemm_impl = 0;
+};
+
+namespace {
+
+void gemm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N, int K, ws::Epi e,
+          void* C, const ws::bf16* bias, cudaStream_t st) {
+  if (m->gemm_impl == 1 && M >= 16)
+    ws::launch_gemm_mma(A, B, M, N, K, e, C, bias, st);
+  else
+    ws::launch_gemm(A, B, M, N, K, e, C, bias, st);
+}
+
+int kv_geom(ws_model* m, ws_pool* pool, ws::KvGeom* g) {
+  int32_t* bt;
+  if (int e = ws::pool_kv_view(pool, &g->window, &g->page_size, &bt, &g->max_blocks)) return e;
+  g->block_tables = bt;
+  int64_t kvb = 0;
+  if (int e = ws_model_kv_geometry(&m->cfg, g->page_size, &g->tpb, &kvb)) return e;
+  g->layers = m->cfg.layers;
+  g->kv_heads = m->cfg.kv_heads;
+  g->head_dim = m->cfg.head_dim;
+  return WS_OK;
+}
+
+template <typename T>
+const T* W(const void* base, int64_t off) {
+  return reinterpret_cast<const T*>(static_cast<const char*>(base) + off);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ws_model_layout(const ws_model_config* cfg, int64_t* out, int64_t n) {
+  if (!cfg || !valid_cfg(*cfg)) WS_FAIL(WS_ERR_INVALID, "invalid model config");
+  if (n < 4 + 9 * (int64_t)cfg->layers) WS_FAIL(WS_ERR_INVALID, "layout buffer too small");
+  Layout L = make_layout(*cfg);
+  out[0] = L.embed;
+  out[1] = L.final_norm;
+  out[2] = L.lm_head;
+  out[3] = L.total;
+  for (int l = 0; l < cfg->layers; ++l) {
+    const auto& x = L.layers[l];
+    int64_t* o = out + 4 + 9 * l;
+    o[0] = x.begin; o[1] = x.attn_norm; o[2] = x.wqkv; o[3] = x.bqkv; o[4] = x.wo;
+    o[5] = x.ffn_norm; o[6] = x.wgu; o[7] = x.wdown; o[8] = x.end;
+  }
+  return WS_OK;
+}
+
+int ws_model_kv_geometry(const ws_model_config* cfg, int64_t page_size, int32_t* tpb,
+                         int64_t* kv_bytes_per_token) {
+  if (!cfg || !valid_cfg(*cfg)) WS_FAIL(WS_ERR_INVALID, "invalid model config");
+  const int64_t per_tok = (int64_t)cfg->layers * 2 * cfg->kv_heads * cfg->head_dim * 2;
+  if (kv_bytes_per_token) *kv_bytes_per_token = per_tok;
+  if (tpb) {
+    if (page_size < per_tok) WS_FAIL(WS_ERR_INVALID, "a page cannot hold one token of KV");
+    *tpb = (int32_t)(page_size / per_tok);
+  }
+  return WS_OK;
+}
+
+int ws_model_create(const ws_model_config* cfg, int32_t device, ws_model** out) {
+  if (!cfg || !valid_cfg(*cfg)) WS_FAIL(WS_ERR_INVALID, "invalid model config");
+  ws_model* m = new ws_model();
+  m->cfg = *cfg;
+  m->layout = make_layout(*cfg);
+  m->device = device;
+  const int half = cfg->head_dim / 2;
+  std::vector<float2> tab((size_t)cfg->max_positions * half);
+  for (int i = 0; i < half; ++i) {
+    const double inv = std::pow((double)cfg->rope_theta, -2.0 * i / (double)cfg->head_dim);
+    for (int p = 0; p < cfg->max_positions; ++p) {
+      const double a = (double)p * inv;
+      tab[(size_t)p * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  }
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaMalloc(&m->rope, tab.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    delete m;
+    WS_FAIL(WS_ERR_CUDA, "RoPE table upload failed");
+  }
+  *out = m;
+  return WS_OK;
+}
+
+int ws_model_destroy(ws_model* m) {
+  if (!m) return WS_OK;
+  if (m->rope) cudaFree(m->rope);
+  delete m;
+  return WS_OK;
+}
+
+int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* bytes) {
+  if (!m || max_tokens < 1) WS_FAIL(WS_ERR_INVALID, "bad workspace request");
+  *bytes = make_ws(m->cfg, max_tokens).total;
+  return WS_OK;
+}
+
+int ws_model_set_gemm(ws_model* m, int32_t impl) {
+  if (!m || impl < 0 || impl > 1) WS_FAIL(WS_ERR_INVALID, "gemm impl must be 0 or 1");
+  m->gemm_impl = impl;
+  return WS_OK;
+}
+
+int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
+                     const int32_t* tokens, int32_t rows, int32_t pos0, ws_streamer* streamer,
+                     int32_t first_streamed, void* workspace, float* logits, int32_t* next_token,
+                     void* stream) {
+  using namespace ws;
+  if (!m || !wts || !workspace || rows < 1) WS_FAIL(WS_ERR_INVALID, "bad prefill arguments");
+  const ws_model_config& c = m->cfg;
+  if (pos0 + rows > c.max_positions) WS_FAIL(WS_ERR_INVALID, "positions exceed the RoPE table");
+  KvGeom kv;
+  if (int e = kv_geom(m, pool, &kv)) return e;
+  if ((pos0 + rows + kv.tpb - 1) / kv.tpb > kv.max_blocks) WS_FAIL(WS_ERR_INVALID, "sequence too long");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Workspace w = make_ws(c, rows);
+  char* wsb = static_cast<char*>(workspace);
+  float* x = reinterpret_cast<float*>(wsb + w.x);
+  bf16* h = reinterpret_cast<bf16*>(wsb + w.h);
+  bf16* qkv = reinterpret_cast<bf16*>(wsb + w.qkv);
+  bf16* attn = reinterpret_cast<bf16*>(wsb + w.attn);
+  bf16* gu = reinterpret_cast<bf16*>(wsb + w.gu);
+  bf16* act = reinterpret_cast<bf16*>(wsb + w.act);
+  bf16* hl = reinterpret_cast<bf16*>(wsb + w.hl);
+  const int d = c.hidden, q = qkv_dim(c), o = c.heads * c.head_dim;
+  const float scale = 1.0f / std::sqrt((float)c.head_dim);
+  const Layout& L = m->layout;
+
+  launch_embed(tokens, W<bf16>(wts, L.embed), x, rows, d, st);
+  for (int l = 0; l < c.layers; ++l) {
+    if (streamer && l >= first_streamed)
+      if (int e = ws_streamer_wait(streamer, l - first_streamed, stream)) return e;
+    const auto& Ly = L.layers[l];
+    launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
+    gemm(m, h, W<bf16>(wts, Ly.wqkv), rows, q, d, c.qkv_bias ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv,
+         c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, st);
+    launch_rope_kv(qkv, m->rope, kv, l, rows, c.heads, nullptr, nullptr, seq, pos0, st);
+    launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
+    gemm(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, Epi::kAddF32, x, nullptr, st);
+    launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, rows, d, c.rms_eps, st);
+    gemm(m, h, W<bf16>(wts, Ly.wgu), rows, 2 * c.ffn, d, Epi::kStoreBf16, gu, nullptr, st);
+    launch_silu_mul(gu, act, rows, c.ffn, st);
+    gemm(m, act, W<bf16>(wts, Ly.wdown), rows, d, c.ffn, Epi::kAddF32, x, nullptr, st);
+  }
+  if (streamer && c.layers >= first_streamed)
+    if (int e = ws_streamer_wait(streamer, c.layers - first_streamed, stream)) return e;
+  launch_rmsnorm(x + (int64_t)(rows - 1) * d, W<bf16>(wts, L.final_norm), hl, 1, d, c.rms_eps, st);
+  launch_gemv(hl, W<bf16>(wts, L.lm_head), 1, c.vocab, d, Epi::kStoreF32, logits, nullptr, st);
+  launch_argmax(logits, 1, c.vocab, next_token, nullptr, st);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* seqs,
+                    const int32_t* pos, const int32_t* tokens, int32_t n, int32_t max_ctx,
+                    void* workspace, float* logits, int32_t* next_tokens, void* stream) {
+  using namespace ws;
+  if (!m || !wts || !workspace || n < 1) WS_FAIL(WS_ERR_INVALID, "bad decode arguments");
+  const ws_model_config& c = m->cfg;
+  if (n > 256) WS_FAIL(WS_ERR_INVALID, "decode batch above 256");
+  if (max_ctx > c.max_positions) WS_FAIL(WS_ERR_INVALID, "context exceeds the RoPE table");
+  KvGeom kv;
+  if (int e = kv_geom(m, pool, &kv)) return e;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Workspace w = make_ws(c, n);
+  char* wsb = static_cast<char*>(workspace);
+  float* x = reinterpret_cast<float*>(wsb + w.x);
+  bf16* h = reinterpret_cast<bf16*>(wsb + w.h);
+  bf16* qkv = reinterpret_cast<bf16*>(wsb + w.qkv);
+  bf16* attn = reinterpret_cast<bf16*>(wsb + w.attn);
+  bf16* gu = reinterpret_cast<bf16*>(wsb + w.gu);
+  bf16* act = reinterpret_cast<bf16*>(wsb + w.act);
+  bf16* hl = reinterpret_cast<bf16*>(wsb + w.hl);
+  float* scratch = reinterpret_cast<float*>(wsb + w.scratch);
+  const int d = c.hidden, q = qkv_dim(c), o = c.heads * c.head_dim;
+  const float scale = 1.0f / std::sqrt((float)c.head_dim);
+  const Layout& L = m->layout;
+
+  launch_embed(tokens, W<bf16>(wts, L.embed), x, n, d, st);
+  for (int l = 0; l < c.layers; ++l) {
+    const auto& Ly = L.layers[l];
+    launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, n, d, c.rms_eps, st);
+    gemm(m, h, W<bf16>(wts, Ly.wqkv), n, q, d, c.qkv_bias ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv,
+         c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, st);
+    launch_rope_kv(qkv, m->rope, kv, l, n, c.heads, seqs, pos, 0, 0, st);
+    launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
+    gemm(m, attn, W<bf16>(wts, Ly.wo), n, d, o, Epi::kAddF32, x, nullptr, st);
+    launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
+    gemm(m, h, W<bf16>(wts, Ly.wgu), n, 2 * c.ffn, d, Epi::kStoreBf16, gu, nullptr, st);
+    launch_silu_mul(gu, act, n, c.ffn, st);
+    gemm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, Epi::kAddF32, x, nullptr, st);
+  }
+  launch_rmsnorm(x, W<bf16>(wts, L.final_norm), hl, n, d, c.rms_eps, st);
+  gemm(m, hl, W<bf16>(wts, L.lm_head), n, c.vocab, d, Epi::kStoreF32, logits, nullptr, st);
+  launch_argmax(logits, n, c.vocab, next_tokens, nullptr, st);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epi, void* C,
+            const void* bias, int32_t impl, void* stream) {
+  using namespace ws;
+  if (M < 1 || N < 1 || K < 32 || K % 32 || epi < 0 || epi > 3) WS_FAIL(WS_ERR_INVALID, "bad GEMM shape");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bf16* a = static_cast<const bf16*>(A);
+  const bf16* b = static_cast<const bf16*>(B);
+  const bf16* bi = static_cast<const bf16*>(bias);
+  if (impl == 1 && M >= 16)
+    launch_gemm_mma(a, b, M, N, K, (Epi)epi, C, bi, st);
+  else if (impl == 2)
+    launch_gemv(a, b, M, N, K, (Epi)epi, C, bi, st);
+  else
+    launch_gemm(a, b, M, N, K, (Epi)epi, C, bi, st);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+}  // extern "C"

@@ -699,3 +699,17 @@ int ws_pool_last_switch(ws_pool* p, double* kernel_ms, int64_t* entries) {
 }
 
 }  // extern "C"
+
+namespace ws {
+// Internal accessor for the model driver (not part of the C-ABI).
+int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_tables,
+                 int32_t* max_blocks) {
+  if (!p || !p->on_device()) WS_FAIL(WS_ERR_NO_DEVICE, "model forward needs a device pool");
+  if (!p->bt_dev) WS_FAIL(WS_ERR_STATE, "sequence table not configured (ws_pool_seq_config)");
+  *window = reinterpret_cast<char*>(p->window);
+  *page_size = p->page;
+  *block_tables = p->bt_dev;
+  *max_blocks = p->max_blocks;
+  return WS_OK;
+}
+}  // namespace ws

@@ -1,0 +1,293 @@
+"""UniversalWorker — the north_star worker API on one B200:
+
+    prewarm(model, layers)      prewarmed-weight pool with layer-granular residency
+    switch_memory(model)        weight<->KV switch (VMM pages + switch kernel)
+    activate_instance(model, …) layer-streamed cold-start prefill -> first token
+    prefill(...) / decode(...)  on the paged KV pool
+
+It composes the reference-protocol ``Cluster`` (ledger, role machine — the
+reference engine can drive the same object) with the native model forward
+and the layer streamer. Host-side bookkeeping follows the reference:
+slot.layers_loaded / weight_bytes_loaded / required_prewarm_layers
+(cluster.py:97-107, engine.py:658-686); activation timing decomposes like the
+reference's startup breakdown (engine.py:557-597) but every term is measured.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as N
+from .cluster import Cluster, InstanceState, ModelSpec, PrewarmSlot, Role, required_prewarm_layers
+from .devmem import view
+from .models import PAGE, ModelConfig, model_spec
+
+
+@dataclass
+class ModelEntry:
+    cfg: ModelConfig
+    spec: ModelSpec
+    layout: object
+    host: torch.Tensor | None  # pinned bf16 image: cold-start source
+    handle: C.c_void_p
+    peer: torch.Tensor | None = None  # optional peer-device image (NVLink source)
+
+
+@dataclass
+class ActivationResult:
+    model: str
+    token: int
+    ttft_ms: float                 # host clock: call -> first token on host
+    device_ms: float               # CUDA events: switch start -> token ready
+    switch_ms: float               # host clock of the memory switch (ledger + kernel launch)
+    switch_kernel_ms: float
+    streamed_layers: int
+    streamed_bytes: int
+    stream_ms: float               # copy stream: start -> last layer landed
+    evicted: list = field(default_factory=list)
+    seq: int = -1
+
+
+class UniversalWorker:
+    def __init__(self, device: int = 0, pool_pages: int = 12288, page_size: int = PAGE,
+                 max_seqs: int = 64, max_tokens: int = 4096, bandwidth_gbs: float = 55.0):
+        torch.cuda.set_device(device)
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        bw = bandwidth_gbs * 1e9 / 1e3  # bytes/ms, the reference's unit
+        self.cluster = Cluster(1, 1, pool_pages, page_size, bw, devices={0: device})
+        self.cluster.map_on_prewarm = False
+        self.gpu = self.cluster.gpu(0)
+        self.compute = torch.cuda.Stream(self.dev)
+        self.copy = torch.cuda.Stream(self.dev)
+        self.gpu.stream = self.compute.cuda_stream
+        self.page_size = page_size
+        self.max_tokens = max_tokens
+        N.call("ws_pool_seq_config", self.gpu.pool, max_seqs, pool_pages)
+        self.models: dict[str, ModelEntry] = {}
+        self.instance = None
+        self.active_model: str | None = None
+        st = C.c_void_p()
+        N.call("ws_streamer_create", 512, C.byref(st))
+        self.streamer = st
+        self._ws = None
+        self._ws_bytes = 0
+        self.logits = None
+        self.next_tok = torch.zeros(256, dtype=torch.int32, device=self.dev)
+        self.open_seqs: set[int] = set()
+
+    # ------------------------------------------------------------ models
+    def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32) -> ModelEntry:
+        h = C.c_void_p()
+        N.call("ws_model_create", C.byref(cfg.c()), self.device, C.byref(h))
+        spec = model_spec(cfg, max_batch=max_batch)
+        e = ModelEntry(cfg, spec, cfg.layout(), host_weights, h)
+        self.models[cfg.name] = e
+        need = C.c_int64()
+        N.call("ws_model_workspace_bytes", h, self.max_tokens, C.byref(need))
+        if need.value > self._ws_bytes:
+            self._ws = torch.empty(need.value, dtype=torch.uint8, device=self.dev)
+            self._ws_bytes = need.value
+        v = max(m.cfg.vocab for m in self.models.values())
+        if self.logits is None or self.logits.numel() < 256 * v:
+            self.logits = torch.empty(256 * v, dtype=torch.float32, device=self.dev)
+        return e
+
+    def set_gemm_impl(self, impl: int) -> None:
+        for e in self.models.values():
+            N.call("ws_model_set_gemm", e.handle, impl)
+
+    def slot(self, name: str) -> PrewarmSlot | None:
+        return self.gpu.slots.get(name)
+
+    def weights_ptr(self, name: str) -> int:
+        return self.slot(name).va
+
+    def slot_view(self, name: str) -> torch.Tensor:
+        e = self.models[name]
+        return view(self.slot(name).va, (e.layout.total // 2,), torch.bfloat16, self.device)
+
+    # ------------------------------------------------------------ prewarm
+    def prewarm(self, name: str, layers: int | None = None, chunk_pages: int = 64,
+                source: torch.Tensor | None = None) -> PrewarmSlot:
+        """prewarm(model, layers): take a slot (cluster.py:245-274), map all
+        of its pages chunk by chunk while the copy engine loads the
+        embedding + first ``layers`` decoder layers (memswitch.py:59-98
+        pipeline, run for real). ``layers=None`` uses the reference's
+        stall-free prefix k (required_prewarm_layers)."""
+        e = self.models[name]
+        if layers is None:
+            layers = required_prewarm_layers(e.spec, self.cluster.bandwidth)
+        layers = max(0, min(layers, e.cfg.layers))
+        pages = e.spec.partition_pages(self.page_size)
+        slot = self.cluster.begin_prewarm(self.gpu, e.spec, pages, max(layers, 1))
+        src = source if source is not None else e.host
+        prefix = e.layout.prefix_bytes(layers) if layers < e.cfg.layers else e.layout.total
+        t0 = time.perf_counter()
+        mapped = 0
+        with torch.cuda.stream(self.copy):
+            while mapped < pages:
+                n = min(chunk_pages, pages - mapped)
+                # map chunk c on the host while the copy engine moves chunk c-1
+                N.call("ws_slot_map_chunk", self.gpu.pool, slot.slot_id, mapped, n)
+                lo, hi = mapped * self.page_size, min((mapped + n) * self.page_size, prefix)
+                if hi > lo and src is not None:
+                    d = view(slot.va + lo, ((hi - lo) // 2,), torch.bfloat16, self.device)
+                    d.copy_(src[lo // 2: hi // 2], non_blocking=True)
+                mapped += n
+        self.copy.synchronize()
+        slot.load_start = None
+        slot.load_finish = None
+        slot.layers_loaded = layers
+        slot.weight_bytes_loaded = float(prefix)
+        slot.prewarm_ms = (time.perf_counter() - t0) * 1e3
+        return slot
+
+    def drop_suffix(self, name: str, layers: int) -> None:
+        """Forget residency of layers >= ``layers`` (bytes stay, ledger says
+        they are gone), so the next activation streams them again."""
+        s = self.slot(name)
+        e = self.models[name]
+        s.layers_loaded = layers
+        s.weight_bytes_loaded = float(e.layout.prefix_bytes(layers))
+
+    # ------------------------------------------------------------ switch
+    def switch_memory(self, name: str):
+        """Weight->KV memory switch (promote_to_dedicated, cluster.py:291-342):
+        evict other slots (async VMM unmap), every free page becomes KV via the
+        switch kernel, no driver call on this path. Returns (inst, evicted,
+        host_ms, kernel_ms)."""
+        e = self.models[name]
+        self.compute.wait_stream(self.copy)  # in-flight prewarm copies must not race KV reuse
+        t0 = time.perf_counter()
+        inst, evicted = self.cluster.promote_to_dedicated((0,), e.spec, self.slot(name).required_prewarm_layers
+                                                          if self.slot(name) else 1)
+        host_ms = (time.perf_counter() - t0) * 1e3
+        kms, ent = C.c_double(), C.c_int64()
+        N.call("ws_pool_last_switch", self.gpu.pool, C.byref(kms), C.byref(ent))
+        self.instance = inst
+        self.active_model = name
+        return inst, evicted, host_ms, kms.value
+
+    def reclaim(self, inflight: int, kv_used_bytes: float) -> int:
+        """KV->weights switch on a draining worker (cluster.py:351-365)."""
+        if self.gpu.role == Role.DEDICATED:
+            self.cluster.enter_grace(self.instance)
+        return self.cluster.reclaim_on_completion(self.gpu, inflight, self.instance.max_batch, kv_used_bytes)
+
+    def release(self) -> None:
+        """End of grace (cluster.py:367-387): KV pages back to free, slots kept."""
+        for s in list(self.open_seqs):
+            self.close_seq(s)
+        if self.instance is None:
+            return
+        if self.instance.state != InstanceState.GRACE:
+            if self.instance.state == InstanceState.STARTING:
+                self.instance.state = InstanceState.ACTIVE
+            self.cluster.enter_grace(self.instance)
+        self.cluster.release_instance(self.instance)
+        self.instance = None
+        self.active_model = None
+
+    # ------------------------------------------------------------ sequences
+    def open_seq(self, n_tokens: int) -> int:
+        s = C.c_int32()
+        N.call("ws_seq_open", self.gpu.pool, C.byref(s))
+        self.open_seqs.add(s.value)
+        self.reserve(s.value, n_tokens)
+        return s.value
+
+    def reserve(self, seq: int, n_tokens: int) -> None:
+        tpb, _ = self.models[self.active_model].cfg.kv_geometry(self.page_size)
+        N.call("ws_seq_reserve", self.gpu.pool, seq, -(-n_tokens // tpb), self.compute.cuda_stream)
+
+    def close_seq(self, seq: int) -> None:
+        N.call("ws_seq_close", self.gpu.pool, seq)
+        self.open_seqs.discard(seq)
+
+    # ------------------------------------------------------------ compute
+    def prefill(self, seq: int, tokens_dev: torch.Tensor, pos0: int = 0, stream_from: int | None = None):
+        """Prefill on the paged pool; returns (logits view [vocab], next-token device scalar)."""
+        e = self.models[self.active_model]
+        rows = tokens_dev.numel()
+        st = self.streamer if stream_from is not None else None
+        N.call("ws_model_prefill", e.handle, self.gpu.pool, C.c_void_p(self.slot(e.cfg.name).va), seq,
+               C.c_void_p(tokens_dev.data_ptr()), rows, pos0, st, stream_from or 0,
+               C.c_void_p(self._ws.data_ptr()), C.c_void_p(self.logits.data_ptr()),
+               C.c_void_p(self.next_tok.data_ptr()), C.c_void_p(self.compute.cuda_stream))
+        return self.logits[: e.cfg.vocab], self.next_tok[:1]
+
+    def decode(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor, max_ctx: int):
+        e = self.models[self.active_model]
+        n = seqs_dev.numel()
+        N.call("ws_model_decode", e.handle, self.gpu.pool, C.c_void_p(self.slot(e.cfg.name).va),
+               C.c_void_p(seqs_dev.data_ptr()), C.c_void_p(pos_dev.data_ptr()),
+               C.c_void_p(tokens_dev.data_ptr()), n, max_ctx, C.c_void_p(self._ws.data_ptr()),
+               C.c_void_p(self.logits.data_ptr()), C.c_void_p(self.next_tok.data_ptr()),
+               C.c_void_p(self.compute.cuda_stream))
+        return self.logits[: n * e.cfg.vocab].view(n, e.cfg.vocab), self.next_tok[:n]
+
+    # ------------------------------------------------------------ activation
+    def activate_instance(self, name: str, prompt_host: torch.Tensor, source: torch.Tensor | None = None,
+                          keep_seq: bool = False) -> ActivationResult:
+        """Cold (or warm) start: switch memory, stream the non-resident layers
+        on the copy engine, prefill the prompt with per-layer waits, return
+        the first token on the host. prompt_host: pinned int32 tokens."""
+        e = self.models[name]
+        L = e.cfg.layers
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        ev0.record(self.compute)
+        inst, evicted, sw_ms, sw_kernel_ms = self.switch_memory(name)
+        slot = self.slot(name)
+        k = slot.layers_loaded
+        stream_from = None
+        streamed = 0
+        if k < L:
+            src = source if source is not None else e.host
+            ranges = e.layout.stream_ranges(k)
+            flat = (C.c_int64 * (3 * len(ranges)))(*[v for r in ranges for v in r])
+            self.copy.wait_stream(self.compute)  # copy after the switch (pages owned)
+            N.call("ws_streamer_start", self.streamer, C.c_void_p(slot.va), C.c_void_p(src.data_ptr()),
+                   flat, len(ranges), C.c_void_p(self.copy.cuda_stream))
+            stream_from = k
+            streamed = sum(r[2] for r in ranges)
+        rows = prompt_host.numel()
+        seq = self.open_seq(rows + 1)
+        with torch.cuda.stream(self.compute):
+            toks = prompt_host.to(self.dev, non_blocking=True)
+        _, nt = self.prefill(seq, toks, 0, stream_from)
+        with torch.cuda.stream(self.compute):
+            out = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            out.copy_(nt, non_blocking=True)
+        ev1.record(self.compute)
+        ev1.synchronize()
+        ttft = (time.perf_counter() - t0) * 1e3
+        stream_ms = 0.0
+        if stream_from is not None:
+            times = (C.c_float * (L - k + 1))()
+            N.call("ws_streamer_times", self.streamer, times, L - k + 1)
+            stream_ms = times[L - k]
+        slot.layers_loaded = L
+        slot.weight_bytes_loaded = float(e.layout.total)
+        inst.state = InstanceState.ACTIVE
+        if not keep_seq:
+            self.close_seq(seq)
+        return ActivationResult(name, int(out.item()), ttft, ev0.elapsed_time(ev1), sw_ms, sw_kernel_ms,
+                                L - k, streamed, stream_ms, evicted, seq if keep_seq else -1)
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.dev)
+        for e in self.models.values():
+            if e.handle:
+                N.fns["ws_model_destroy"](e.handle)
+                e.handle = None
+        if self.streamer:
+            N.fns["ws_streamer_destroy"](self.streamer)
+            self.streamer = None

@@ -1,0 +1,194 @@
+"""Numerics of the sm_100a model path against the CPU fp32 oracle.
+
+Tolerances (north_star): logits within 2e-2 relative (||gpu - ref|| / ||ref||,
+bf16 weights and activations against fp32 math on the same bf16 weights);
+greedy first token identical on >= 99% of prompts.
+"""
+
+import math
+
+import pytest
+import torch
+
+from oracle import llama_fp32 as O
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 2e-2
+
+
+def _rel(a, b):
+    a, b = a.double().cpu(), b.double().cpu()
+    return ((a - b).norm() / b.norm()).item()
+
+
+@pytest.fixture(scope="module")
+def lib(cuda_device):
+    from paper_2512_09472_b200 import _native as N
+    from paper_2512_09472_b200 import models  # noqa: F401  (registers model signatures)
+
+    torch.cuda.set_device(cuda_device)
+    return N
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 256), (200, 384, 512), (2048, 512, 4096), (37, 1536, 256)])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_gemm_against_fp32(lib, M, N, K, impl):
+    import ctypes as C
+
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 0,
+             C.c_void_p(out.data_ptr()), None, impl, None)
+    assert _rel(out.float(), ref) < 1e-2
+    lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 1,
+             C.c_void_p(out.data_ptr()), C.c_void_p(bias.data_ptr()), impl, None)
+    assert _rel(out.float(), ref + bias.float()) < 1e-2
+    acc = torch.randn(M, N, device="cuda", generator=g)
+    want = acc + ref
+    lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 2,
+             C.c_void_p(acc.data_ptr()), None, impl, None)
+    torch.cuda.synchronize()
+    assert _rel(acc, want) < 1e-5
+
+
+@pytest.mark.parametrize("M", [1, 3, 8, 16])
+def test_gemv_against_fp32(lib, M):
+    import ctypes as C
+
+    N, K = 1000, 768
+    g = torch.Generator(device="cuda").manual_seed(M)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 3,
+             C.c_void_p(out.data_ptr()), None, 2, None)
+    torch.cuda.synchronize()
+    assert _rel(out, A.float() @ B.float().T) < 1e-5
+
+
+def _worker(cfg, seed=11, pool_pages=64):
+    from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat
+    from paper_2512_09472_b200.worker import UniversalWorker
+
+    w = UniversalWorker(0, pool_pages=pool_pages, max_tokens=1024)
+    flat = synth_flat(cfg, seed=seed, device="cuda")
+    host = pinned_host_copy(flat)
+    w.register(cfg, host)
+    return w, host
+
+
+@pytest.fixture(scope="module")
+def tiny(lib):
+    from paper_2512_09472_b200 import models as M
+
+    cfg = M.TINY
+    w, host = _worker(cfg)
+    weights = O.unpack(cfg, cfg.layout(), host.clone())
+    yield cfg, w, weights
+    w.release()
+    w.close()
+
+
+def _prompt(cfg, seed, n=512):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, cfg.vocab, (n,), generator=g, dtype=torch.int32)
+
+
+def test_tiny_cold_then_warm_prefill_matches_oracle(tiny):
+    cfg, w, weights = tiny
+    w.prewarm(cfg.name, layers=1)  # embedding + layer 0 resident (BASELINE config 1)
+    assert w.slot(cfg.name).layers_loaded == 1
+    prompt = _prompt(cfg, 0).pin_memory()
+    cold = w.activate_instance(cfg.name, prompt)
+    assert cold.streamed_layers == 1 and cold.streamed_bytes > 0
+    logits_cold = w.logits[: cfg.vocab].clone()
+    ref, _ = O.forward(cfg, weights, prompt.long())
+    assert _rel(logits_cold, ref[-1]) < LOGIT_RTOL
+    assert cold.token == int(ref[-1].argmax())
+    w.release()
+    warm = w.activate_instance(cfg.name, prompt)  # every layer resident now
+    assert warm.streamed_layers == 0
+    assert torch.equal(w.logits[: cfg.vocab], logits_cold)  # same kernels, same bytes: bit-identical
+    assert warm.token == cold.token
+    w.release()
+
+
+def test_tiny_greedy_agreement_256_prompts(tiny):
+    cfg, w, weights = tiny
+    if w.slot(cfg.name) is None:
+        w.prewarm(cfg.name, layers=cfg.layers)
+    inst, *_ = w.switch_memory(cfg.name)
+    agree, rels, margins = 0, [], []
+    n = 256
+    for s in range(n):
+        prompt = _prompt(cfg, 1000 + s)
+        seq = w.open_seq(prompt.numel())
+        _, nt = w.prefill(seq, prompt.cuda())
+        got = w.logits[: cfg.vocab].float().cpu()
+        w.close_seq(seq)
+        ref, _ = O.forward(cfg, weights, prompt.long())
+        r = ref[-1]
+        rels.append(_rel(got, r))
+        top2 = r.topk(2).values
+        margins.append((top2[0] - top2[1]).item())
+        agree += int(got.argmax()) == int(r.argmax())
+    w.release()
+    print(f"\ngreedy agreement {agree}/{n}; logits rel err max {max(rels):.2e} mean {sum(rels)/n:.2e}; "
+          f"ref top1-top2 margin min {min(margins):.2e} median {sorted(margins)[n//2]:.2e}")
+    assert max(rels) < LOGIT_RTOL
+    assert agree >= math.ceil(0.99 * n)
+
+
+def test_tiny_decode_batch_matches_oracle(tiny):
+    cfg, w, weights = tiny
+    if w.slot(cfg.name) is None:
+        w.prewarm(cfg.name, layers=cfg.layers)
+    w.switch_memory(cfg.name)
+    lens = [7, 130, 33]
+    prompts = [_prompt(cfg, 50 + i, n) for i, n in enumerate(lens)]
+    seqs, pasts, toks = [], [], []
+    for p in prompts:
+        s = w.open_seq(p.numel() + 8)
+        w.prefill(s, p.cuda())
+        seqs.append(s)
+        ref, past = O.forward(cfg, weights, p.long())
+        pasts.append(past)
+        toks.append(int(ref[-1].argmax()))
+    pos = list(lens)
+    for step in range(6):
+        logits, nt = w.decode(torch.tensor(seqs, dtype=torch.int32, device="cuda"),
+                              torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                              torch.tensor(toks, dtype=torch.int32, device="cuda"), max(pos) + 1)
+        got = logits.float().cpu()
+        for i in range(3):
+            ref, pasts[i] = O.forward(cfg, weights, [toks[i]], pos0=pos[i], past=pasts[i])
+            assert _rel(got[i], ref[0]) < LOGIT_RTOL, (step, i)
+            toks[i] = int(ref[0].argmax())
+            pos[i] += 1
+    for s in seqs:
+        w.close_seq(s)
+    w.release()
+
+
+def test_qwen_style_bias_and_phi_head_dim(lib):
+    """Shapes of the co-prewarmed family at tiny width: qkv bias (Qwen2.5),
+    head_dim 96 with MHA (Phi-3)."""
+    from paper_2512_09472_b200 import models as M
+
+    for cfg in (M.TINY.with_(name="tq", qkv_bias=True, rope_theta=1e6, rms_eps=1e-6),
+                M.TINY.with_(name="tp", heads=4, kv_heads=4, head_dim=96, hidden=384, rope_theta=1e4)):
+        w, host = _worker(cfg)
+        weights = O.unpack(cfg, cfg.layout(), host.clone())
+        w.prewarm(cfg.name, layers=cfg.layers)
+        prompt = _prompt(cfg, 9, 300).pin_memory()
+        res = w.activate_instance(cfg.name, prompt)
+        ref, _ = O.forward(cfg, weights, prompt.long())
+        assert _rel(w.logits[: cfg.vocab], ref[-1]) < LOGIT_RTOL, cfg.name
+        assert res.token == int(ref[-1].argmax())
+        w.release()
+        w.close()
