@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark of the universal-worker hot path (BASELINE.json configs[1]):
+
+  Llama-3-8B bf16 universal worker on one B200, first 4 of 32 layers
+  prewarmed, 2048-token prompt, cold start (layers 4..31 + lm_head streamed
+  from pinned host memory while the resident layers compute).
+
+One JSON line on rank 0:
+  value  warm prefill tokens/s, weights + prompt resident in HBM (CUDA events)
+  e2e    the same metric through the public API (UniversalWorker.
+         activate_instance) for a COLD start: the non-resident weights and the
+         prompt cross PCIe host->device inside the timed region, the first
+         token comes back to the host; e2e/value = warm TTFT / cold TTFT
+  ttft_ms / switch_us   cold vs warm TTFT p50/p99, memory-switch latency
+  roofline   the dominant kernel (prefill GEMM) vs MEASURED_PEAKS.json
+  cpu_baseline  the CPU fp32 oracle port on this host's cores (bounded sample)
+Multi-GPU: replicas only (this config does not shard) — every rank runs its
+own worker; value = all ranks' tokens / max-over-ranks time.
+`--impl reference` times the reference-side CPU path (oracle port) instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("prefill tokens/s (Llama-3-8B bf16, 2048-token prompt); cold-start TTFT p50/p99 vs warm; "
+          "memory-switch latency")
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = (len(xs) - 1) * q / 100.0
+    f = int(k)
+    c = min(f + 1, len(xs) - 1)
+    return xs[f] + (xs[c] - xs[f]) * (k - f)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_prefill_sample(cfg, tokens: int, min_seconds: float = 10.0, max_layers: int = 4):
+    """Oracle port (torch CPU fp32, all host threads): time decoder layers of
+    `cfg` at `tokens` tokens until min_seconds, extrapolate to the full model
+    (layers * t_layer + lm_head row). Returns (tokens/s, sample text, threads)."""
+    import torch
+
+    from oracle import llama_fp32 as O
+
+    torch.manual_seed(0)
+    d, H, KV, hd, f = cfg.hidden, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.ffn
+    w = {
+        "l0.attn_norm": torch.ones(d), "l0.ffn_norm": torch.ones(d),
+        "l0.wqkv": torch.randn(cfg.qkv_dim, d) * 0.02, "l0.wo": torch.randn(d, H * hd) * 0.02,
+        "l0.wgu": torch.randn(2 * f, d) * 0.02, "l0.wdown": torch.randn(d, f) * 0.02,
+    }
+    one = cfg.with_(layers=1)
+    x = torch.randn(tokens, d)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_layers and (time.perf_counter() - t_start < min_seconds or len(times) < 1):
+        t0 = time.perf_counter()
+        _layer_cpu(one, w, x, O)
+        times.append(time.perf_counter() - t0)
+    t_layer = statistics.median(times)
+    head = torch.randn(cfg.vocab, d) * 0.02
+    t0 = time.perf_counter()
+    _ = x[-1:] @ head.T
+    t_head = time.perf_counter() - t0
+    total = cfg.layers * t_layer + t_head
+    sample = (f"{len(times)} x one {cfg.name} decoder layer at {tokens} tokens (median {t_layer*1e3:.0f} ms) "
+              f"extrapolated x{cfg.layers} + lm_head row; torch CPU fp32 oracle port")
+    return tokens / total, sample, torch.get_num_threads(), time.perf_counter() - t_start
+
+
+def _layer_cpu(cfg, w, x, O):
+    import math
+
+    import torch
+
+    S = x.shape[0]
+    H, KV, hd = cfg.heads, cfg.kv_heads, cfg.head_dim
+    cos, sin = O.rope_table(hd, cfg.rope_theta, S)
+    h = O._rms(x, w["l0.attn_norm"], cfg.rms_eps)
+    qkv = h @ w["l0.wqkv"].T
+    q = O._rope(qkv[:, : H * hd].view(S, H, hd), cos, sin)
+    k = O._rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin)
+    v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+    g = H // KV
+    o = torch.nn.functional.scaled_dot_product_attention(
+        q.transpose(0, 1), k.repeat_interleave(g, 1).transpose(0, 1), v.repeat_interleave(g, 1).transpose(0, 1),
+        is_causal=True).transpose(0, 1).reshape(S, H * hd)
+    x = x + o @ w["l0.wo"].T
+    h = O._rms(x, w["l0.ffn_norm"], cfg.rms_eps)
+    gu = h @ w["l0.wgu"].T
+    x = x + (torch.nn.functional.silu(gu[:, : cfg.ffn]) * gu[:, cfg.ffn:]) @ w["l0.wdown"].T
+    return x
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU path (oracle port) on host cores."""
+    from paper_2512_09472_b200 import models as M
+
+    if rank != 0:
+        return
+    cfg = M.ALL[args.model]
+    vals = []
+    sample = ""
+    threads = 1
+    for i in range(args.warmup + args.steps):
+        v, sample, threads, _ = cpu_prefill_sample(cfg, args.prompt, min_seconds=0.0, max_layers=1)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.prompt / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} prefill of a {args.prompt}-token prompt on the host CPU "
+                               "(the reference has no GPU path; its prefill is the linear model "
+                               "engine.py:107-108 — timed here is the fp32 oracle port of the forward)",
+                   "model": cfg.name, "prompt_tokens": args.prompt},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09472_b200 import _native as N
+    from paper_2512_09472_b200 import models as M
+    from paper_2512_09472_b200.cluster import catchup_stall_ms, required_prewarm_layers
+    from paper_2512_09472_b200.devmem import view
+    from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat
+    from paper_2512_09472_b200.worker import UniversalWorker
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    cfg = M.ALL[args.model]
+    S, K, Wm = args.prompt, args.steps, args.warmup
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- setup: weights on the host (cold-start source), slot, prewarmed prefix
+    t_setup = time.perf_counter()
+    flat = synth_flat(cfg, seed=rank, device="cuda")
+    host = pinned_host_copy(flat)
+    del flat
+    torch.cuda.empty_cache()
+    w = UniversalWorker(dev, pool_pages=args.pool_pages, max_tokens=max(S, 256))
+    entry = w.register(cfg, host)
+    slot = w.prewarm(cfg.name, layers=args.prewarm_layers)
+    init_ms, map_pp, _ = (lambda a, b, c: (N.call("ws_pool_timing", w.gpu.pool, a, b, c), a, b, c))(
+        *(__import__("ctypes").c_double() for _ in range(3)))[1:]
+    prompt = torch.randint(0, cfg.vocab, (S,), generator=torch.Generator().manual_seed(7), dtype=torch.int32)
+    prompt_pinned = prompt.pin_memory()
+    setup_s = time.perf_counter() - t_setup
+
+    # ---- cold starts (e2e): layers k..L + lm_head stream over PCIe each step
+    cold = []
+    for i in range(Wm + K):
+        if i:
+            w.drop_suffix(cfg.name, args.prewarm_layers)
+        barrier()
+        r = w.activate_instance(cfg.name, prompt_pinned)
+        w.release()
+        if i >= Wm:
+            cold.append(r)
+    # ---- warm starts: every layer resident
+    warm = []
+    for i in range(Wm + K):
+        barrier()
+        r = w.activate_instance(cfg.name, prompt_pinned)
+        w.release()
+        if i >= Wm:
+            warm.append(r)
+
+    # ---- value: warm prefill throughput, prompt + weights resident in HBM
+    w.switch_memory(cfg.name)
+    toks = prompt.cuda()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(w.compute):
+        for _ in range(Wm):
+            s = w.open_seq(S)
+            w.prefill(s, toks)
+            w.close_seq(s)
+        torch.cuda.synchronize()
+        barrier()
+        launches0 = N.kernel_launches()
+        with Clocks(dev) as clk:
+            ev0.record(w.compute)
+            for _ in range(K):
+                s = w.open_seq(S)
+                w.prefill(s, toks)
+                w.close_seq(s)
+            ev1.record(w.compute)
+            torch.cuda.synchronize()
+        launches = N.kernel_launches() - launches0
+    barrier()
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = world * K * S / (elapsed_ms / 1e3)
+    prefill_ms = elapsed_ms / K
+
+    # ---- memory switch burst: promote (weight->KV), reclaim (KV->free), release
+    w.release()
+    sw_done, sw_host, sw_kernel, rc_done, rel_done = [], [], [], [], []
+    for i in range(args.switch_iters):
+        t0 = time.perf_counter()
+        inst, ev, host_ms, kms = w.switch_memory(cfg.name)
+        w.compute.synchronize()
+        t1 = time.perf_counter()
+        inst.state = inst.state.ACTIVE
+        w.cluster.enter_grace(inst)
+        t2 = time.perf_counter()
+        w.reclaim(0, 0.0)
+        w.compute.synchronize()
+        t3 = time.perf_counter()
+        w.release()
+        w.compute.synchronize()
+        t4 = time.perf_counter()
+        sw_done.append((t1 - t0) * 1e6)
+        sw_host.append(host_ms * 1e3)
+        sw_kernel.append(kms * 1e3)
+        rc_done.append((t3 - t2) * 1e6)
+        rel_done.append((t4 - t3) * 1e6)
+
+    # ---- dominant kernel: the gate/up GEMM of the prefill, timed alone
+    pk, kind = peaks()
+    lay = entry.layout.layers[0]
+    B = view(slot.va + lay["wgu"], (2 * cfg.ffn, cfg.hidden), torch.bfloat16, dev)
+    A = torch.randn(S, cfg.hidden, device="cuda").bfloat16()
+    Cm = torch.empty(S, 2 * cfg.ffn, device="cuda", dtype=torch.bfloat16)
+    import ctypes as C
+
+    def gemm_once(impl):
+        N.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), S, 2 * cfg.ffn, cfg.hidden, 0,
+               C.c_void_p(Cm.data_ptr()), None, impl, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+    gemm_flops = 2.0 * S * 2 * cfg.ffn * cfg.hidden
+    gemm_ms = {}
+    for impl in (0, 1):
+        for _ in range(3):
+            gemm_once(impl)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(20):
+            gemm_once(impl)
+        g1.record()
+        torch.cuda.synchronize()
+        gemm_ms[impl] = g0.elapsed_time(g1) / 20
+    achieved = gemm_flops / (gemm_ms[0] / 1e3) / 1e12
+
+    # ---- the reference's analytic model, evaluated with MEASURED inputs
+    stream_gbs = statistics.median(r.streamed_bytes / (r.stream_ms / 1e3) / 1e9 for r in cold)
+    bw_bytes_ms = stream_gbs * 1e9 / 1e3
+    spec = entry.spec
+    a_ms = (prefill_ms / S)  # measured per-token prefill cost
+    spec_m = type(spec)(spec.model_id, spec.weight_bytes, 1, layers=cfg.layers, prefill_a_ms=a_ms, prefill_b_ms=0.0)
+    k_req = required_prewarm_layers(spec_m, bw_bytes_ms, S)
+    stall_pred = catchup_stall_ms(spec_m, args.prewarm_layers, bw_bytes_ms, S)
+
+    traffic = None
+    tp = ROOT / "profiles" / "gemm_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+
+    cold_ttft = [r.ttft_ms for r in cold]
+    warm_ttft = [r.ttft_ms for r in warm]
+    cold_total_s = max_over_ranks(sum(cold_ttft) / 1e3)
+    e2e_value = world * K * S / cold_total_s
+    clk_sum = clk.summary()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        v, sample, threads, secs = cpu_prefill_sample(cfg, S, min_seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
+               "sample": sample + f"; {secs:.1f} s of CPU work", "cpu": _cpu_model()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": Wm,
+        "ms_per_step": prefill_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded random-init weights of the named shape, random token ids)",
+        "config": {"workload": f"{cfg.name} universal worker, first {args.prewarm_layers} of {cfg.layers} layers "
+                               f"prewarmed, {S}-token prompt (BASELINE configs[1])",
+                   "model": cfg.name, "prompt_tokens": S, "prewarmed_layers": args.prewarm_layers,
+                   "weight_source": "pinned host memory (PCIe H2D on the copy engine)",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "no flush needed: 16 GB of weights per step > 126 MB L2",
+                   "pool_pages": args.pool_pages},
+        "e2e": {"value": e2e_value, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(statistics.median(r.streamed_bytes for r in cold)) + S * 4,
+                "d2h_bytes_per_step": 4,
+                "path": "UniversalWorker.activate_instance (cold): switch_memory + layer streaming + prefill"},
+        "ttft_ms": {"cold_p50": pct(cold_ttft, 50), "cold_p99": pct(cold_ttft, 99),
+                    "warm_p50": pct(warm_ttft, 50), "warm_p99": pct(warm_ttft, 99),
+                    "cold_over_warm_p50": pct(cold_ttft, 50) / pct(warm_ttft, 50), "target_ratio": 1.2,
+                    "cold_device_p50": pct([r.device_ms for r in cold], 50),
+                    "stream_ms_p50": pct([r.stream_ms for r in cold], 50),
+                    "streamed_bytes": cold[0].streamed_bytes, "stream_gbs_p50": stream_gbs,
+                    "pcie_gen5_peak_gbs": 64.0},
+        "reference_model_at_measured_inputs": {
+            "required_prewarm_layers": k_req, "catchup_stall_ms_k4": stall_pred,
+            "predicted_cold_ttft_ms": pct(warm_ttft, 50) + stall_pred,
+            "note": "cluster.py:145-182 evaluated with the measured stream bandwidth and per-token prefill cost"},
+        "switch_us": {"promote_p50": pct(sw_done, 50), "promote_p99": pct(sw_done, 99),
+                      "promote_host_p50": pct(sw_host, 50), "switch_kernel_p50": pct(sw_kernel, 50),
+                      "reclaim_p50": pct(rc_done, 50), "reclaim_p99": pct(rc_done, 99),
+                      "release_p50": pct(rel_done, 50), "release_p99": pct(rel_done, 99),
+                      "n": len(sw_done), "target_us": 1000.0,
+                      "kv_pages_switched": w.gpu.total_pages - entry.spec.partition_pages(M.PAGE)},
+        "prefill": {"ms": prefill_ms, "tflops": cfg.prefill_flops(S) / (prefill_ms / 1e3) / 1e12,
+                    "frac_of_sustained": cfg.prefill_flops(S) / (prefill_ms / 1e3) / 1e12 /
+                    pk["bf16_tflops_sustained"], "algorithmic_tflop": cfg.prefill_flops(S) / 1e12},
+        "roofline": {"bound": "tensor", "kernel": "prefill gate/up GEMM 2048x28672x4096 (tensor-core path)",
+                     "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "peak_kind": kind + " burst",
+                     "launch_ms": gemm_ms[0], "legacy_mma_sync_ms": gemm_ms[1]},
+        "cpu_baseline": cpu,
+        "clocks": clk_sum,
+        "gpu_launches": launches,
+        "setup_s": setup_s,
+        "vmm": {"pool_init_ms": init_ms.value, "slot_map_us_per_page": map_pp.value * 1e3,
+                "prewarm_ms": getattr(slot, "prewarm_ms", None)},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    w.release()
+    w.close()
+
+
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return f"x{os.cpu_count()}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama3-8b")
+    ap.add_argument("--prompt", type=int, default=2048)
+    ap.add_argument("--prewarm-layers", type=int, default=4)
+    ap.add_argument("--pool-pages", type=int, default=12288)
+    ap.add_argument("--switch-iters", type=int, default=200)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

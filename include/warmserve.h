@@ -37,6 +37,8 @@ extern "C" {
 
 const char* ws_last_error(void);
 int ws_version(int* major, int* minor);
+/* Kernel launches issued by this library since load (evidence for gpu_launches). */
+int ws_kernel_launches(int64_t* out);
 
 /* ======================================================================
  * Planning math — bit-exact float64 restatements of the reference's

@@ -72,6 +72,7 @@ class PoolCounts(C.Structure):
 # name -> argtypes; every function returns int status.
 SIGNATURES: dict[str, list] = {
     "ws_version": [P(C.c_int), P(C.c_int)],
+    "ws_kernel_launches": [P(i64)],
     "ws_required_prewarm_layers": [i64, i32, i32, f64, f64, f64, i32, P(i32)],
     "ws_catchup_stall_ms": [i64, i32, i32, f64, f64, i32, f64, i32, P(f64)],
     "ws_reservation_target": [f64, i32, i32, f64, P(f64)],
@@ -135,6 +136,12 @@ def call(name: str, *args) -> None:
     rc = fns[name](*args)
     if rc != WS_OK:
         raise NativeError(rc, lib.ws_last_error().decode(errors="replace"))
+
+
+def kernel_launches() -> int:
+    v = C.c_int64()
+    call("ws_kernel_launches", C.byref(v))
+    return v.value
 
 
 def last_error() -> str:

@@ -35,4 +35,7 @@ const char* last_error();
 
 constexpr int kNumSMs = 148;
 
+// Count of kernel launches issued by this library (ws_kernel_launches()).
+void count_launch(int n = 1);
+
 }  // namespace ws

@@ -1,6 +1,7 @@
 #include "driver.h"
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -31,6 +32,9 @@ bool load(const char* name, F* fn) {
 }  // namespace
 
 void set_error(const std::string& msg) { g_err = msg; }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 const char* last_error() { return g_err.c_str(); }
 
 const Driver* driver() {
@@ -53,6 +57,11 @@ const Driver* driver() {
 }  // namespace ws
 
 extern "C" const char* ws_last_error(void) { return ws::last_error(); }
+extern "C" int ws_kernel_launches(int64_t* out) {
+  *out = ws::g_launches.load();
+  return WS_OK;
+}
+
 extern "C" int ws_version(int* major, int* minor) {
   *major = 0;
   *minor = 1;

@@ -346,6 +346,7 @@ void prefill_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int s
     attr = true;
   }
   dim3 grid((rows + kQTile - 1) / kQTile, heads);
+  count_launch();
   attn_prefill_kernel<HD><<<grid, kWarps * 32, smem, st>>>(qkv, out, kv, layer, seq, rows, pos0,
                                                            heads, scale * 1.4426950408889634f);
 }
@@ -356,6 +357,7 @@ void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const 
                  cudaStream_t st) {
   const int n_splits = (max_ctx + kSplit - 1) / kSplit;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
+  count_launch(2);
   attn_decode_kernel<HD><<<grid, kDecThreads, 0, st>>>(qkv, kv, layer, seqs, ctx, heads,
                                                        scale * 1.4426950408889634f, scratch, n_splits);
   attn_combine_kernel<HD><<<dim3(heads, n_seqs), HD, 0, st>>>(scratch, out, heads, n_splits);

@@ -179,11 +179,13 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
 }  // namespace
 
 void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n, int d, cudaStream_t st) {
+  count_launch();
   embed_kernel<<<n, 256, 0, st>>>(tokens, table, x, d);
 }
 
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, float eps,
                     cudaStream_t st) {
+  count_launch();
   if (d >= 2048)
     rmsnorm_kernel<512><<<rows, 512, 0, st>>>(x, w, out, d, eps);
   else
@@ -192,6 +194,7 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, f
 
 void launch_silu_mul(const bf16* gu, bf16* act, int rows, int ffn, cudaStream_t st) {
   dim3 grid((ffn / 8 + 255) / 256, rows);
+  count_launch();
   silu_mul_kernel<<<grid, 256, 0, st>>>(gu, act, ffn);
 }
 
@@ -199,10 +202,12 @@ void launch_rope_kv(bf16* qkv, const float2* rope, const KvGeom& kv, int layer, 
                     const int32_t* seq, const int32_t* pos, int seq0, int pos0, cudaStream_t st) {
   const int64_t warps = (int64_t)rows * (heads + 2 * kv.kv_heads);
   const int blocks = (int)((warps * 32 + 255) / 256);
+  count_launch();
   rope_kv_kernel<<<blocks, 256, 0, st>>>(qkv, rope, kv, layer, rows, heads, seq, pos, seq0, pos0);
 }
 
 void launch_argmax(const float* logits, int M, int V, int32_t* out, float*, cudaStream_t st) {
+  count_launch();
   argmax_kernel<<<M, 1024, 0, st>>>(logits, V, out);
 }
 

@@ -198,6 +198,7 @@ void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi,
     attr = true;
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  count_launch();
   gemm_mma_kernel<<<grid, THREADS, smem, st>>>(A, B, M, N, K, (int)epi, C, bias);
 }
 
@@ -214,6 +215,7 @@ void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
   const int warps_needed = (N + 1) / 2;
   int blocks = (warps_needed + 7) / 8;
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  count_launch();
   if (M <= 1)
     gemv_kernel<1><<<blocks, 256, 0, st>>>(A, B, M, N, K, (int)epi, C, bias);
   else if (M <= 4)

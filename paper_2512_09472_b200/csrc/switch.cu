@@ -79,6 +79,7 @@ void launch_switch(const SwitchArgs& a, cudaStream_t stream) {
   int n_mig_ctas = a.n_mig * kMigCtasPerPage;
   int grid = n_rule_ctas + n_set_ctas + n_mig_ctas;
   if (grid == 0) grid = 1;
+  count_launch();
   switch_kernel<<<grid, kThreads, 0, stream>>>(a, n_rule_ctas, n_set_ctas);
 }
 

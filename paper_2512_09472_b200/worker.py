@@ -216,20 +216,30 @@ class UniversalWorker:
         e = self.models[self.active_model]
         rows = tokens_dev.numel()
         st = self.streamer if stream_from is not None else None
+        caller = torch.cuda.current_stream(self.dev)
+        if caller != self.compute:
+            self.compute.wait_stream(caller)  # inputs produced on the caller's stream
         N.call("ws_model_prefill", e.handle, self.gpu.pool, C.c_void_p(self.slot(e.cfg.name).va), seq,
                C.c_void_p(tokens_dev.data_ptr()), rows, pos0, st, stream_from or 0,
                C.c_void_p(self._ws.data_ptr()), C.c_void_p(self.logits.data_ptr()),
                C.c_void_p(self.next_tok.data_ptr()), C.c_void_p(self.compute.cuda_stream))
+        if caller != self.compute:
+            caller.wait_stream(self.compute)  # outputs visible to the caller's stream
         return self.logits[: e.cfg.vocab], self.next_tok[:1]
 
     def decode(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor, max_ctx: int):
         e = self.models[self.active_model]
         n = seqs_dev.numel()
+        caller = torch.cuda.current_stream(self.dev)
+        if caller != self.compute:
+            self.compute.wait_stream(caller)
         N.call("ws_model_decode", e.handle, self.gpu.pool, C.c_void_p(self.slot(e.cfg.name).va),
                C.c_void_p(seqs_dev.data_ptr()), C.c_void_p(pos_dev.data_ptr()),
                C.c_void_p(tokens_dev.data_ptr()), n, max_ctx, C.c_void_p(self._ws.data_ptr()),
                C.c_void_p(self.logits.data_ptr()), C.c_void_p(self.next_tok.data_ptr()),
                C.c_void_p(self.compute.cuda_stream))
+        if caller != self.compute:
+            caller.wait_stream(self.compute)
         return self.logits[: n * e.cfg.vocab].view(n, e.cfg.vocab), self.next_tok[:n]
 
     # ------------------------------------------------------------ activation
