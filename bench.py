@@ -252,9 +252,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- value: warm prefill throughput, prompt + weights resident in HBM
     w.switch_memory(cfg.name)
-    toks = prompt.cuda()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(w.compute):
+        toks = prompt_pinned.to("cuda", non_blocking=True)
         for _ in range(Wm):
             s = w.open_seq(S)
             w.prefill(s, toks)

@@ -206,8 +206,8 @@ void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
                  const bf16* bias, cudaStream_t st) {
   if (M < 16)
     launch_gemv(A, B, M, N, K, epi, C, bias, st);
-  else
-    launch_gemm_mma(A, B, M, N, K, epi, C, bias, st);
+  else if (!launch_gemm_tc(A, B, M, N, K, epi, C, bias, st))
+    launch_gemm_mma(A, B, M, N, K, epi, C, bias, st);  // shapes outside the tcgen05 tiling
 }
 
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,

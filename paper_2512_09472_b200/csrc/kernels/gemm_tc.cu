@@ -1,0 +1,306 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a — the prefill projections
+// (QKV, O, gate/up, down) and large-M lm_head rows.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T   (both operands K-major bf16, fp32 accumulate)
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer (one elected lane): A 128x64 + B 256x64 tiles,
+//               SWIZZLE_128B, 4-stage smem ring guarded by full/empty mbarriers
+//   warp 1      MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16
+//               M=128 N=256 K=16 x4 per stage, accumulator in TMEM,
+//               tcgen05.commit frees the smem stage / publishes the tile
+//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> bf16 (+bias)
+//               or fp32 (+= residual) -> global; runs on accumulator b while
+//               the MMA warp fills accumulator b^1 (double-buffered TMEM)
+// Tile order: m fastest, so the 16 CTAs sharing a 256-row weight block run
+// together and the weight tile is read from HBM once (L2 reuse).
+#include <cuda.h>
+
+#include "../common.h"
+#include "../driver.h"
+#include "device.cuh"
+#include "ops.cuh"
+
+namespace ws {
+namespace {
+
+using namespace dev;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, THREADS = 256;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 512;
+
+// Instruction descriptor (kind::f16): D=F32 (bit 4), A=BF16 (bits 7-9 = 1),
+// B=BF16 (bits 10-12 = 1), both K-major, N>>3 at bits 17-22, M>>4 at 24-28.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+// Shared-memory matrix descriptor for a K-major SWIZZLE_128B tile: rows of
+// 128 B, 8-row core groups 1024 B apart (SBO), LBO unused (=1), version 1,
+// layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, v)                                                                        \
+  asm volatile(                                                                                    \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"             \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),       \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),   \
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),             \
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),             \
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])              \
+      : "r"(taddr))
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   int M, int N, int K, int epi, void* __restrict__ Cout, const bf16* __restrict__ bias) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023) & ~1023u;  // SWIZZLE_128B atoms need 1024 B alignment
+  const uint32_t bars = base + STAGES * STAGE_BYTES;
+  // barrier layout: full[STAGES], empty[STAGES], tfull[2], tempty[2], then the TMEM slot
+  auto full = [&](int s) { return bars + 8 * s; };
+  auto empty = [&](int s) { return bars + 8 * (STAGES + s); };
+  auto tfull = [&](int b) { return bars + 8 * (2 * STAGES + b); };
+  auto tempty = [&](int b) { return bars + 8 * (2 * STAGES + 2 + b); };
+  const uint32_t tmem_slot = bars + 8 * (2 * STAGES + 4);
+  uint32_t* tmem_slot_ptr =
+      reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_blocks = (M + BM - 1) / BM, n_blocks = N / BN, k_blocks = K / BK;
+  const int tiles = m_blocks * n_blocks;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % m_blocks) * BM, n0 = (t / m_blocks) * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1);
+          const uint32_t sa = base + stage * STAGE_BYTES;
+          mbar_expect_tx(full(stage), STAGE_BYTES);
+          tma_load(sa, &map_a, full(stage), kb * BK, m0);
+          tma_load(sa + A_BYTES, &map_b, full(stage), kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(tempty(acc), acc_phase ^ 1);  // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(full(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * STAGE_BYTES;
+          const uint64_t da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle row
+            tc_mma(d, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0);
+          tc_commit(empty(stage));  // smem stage free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull(acc));  // accumulator complete
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM lanes 32*q .. 32*q+31 belong to warp q = warp % 4 =====
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % m_blocks) * BM, n0 = (t / m_blocks) * BN;
+      mbar_wait(tfull(acc), acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (!ok) continue;
+        const int col = n0 + c * 32;
+        if (epi == (int)Epi::kAddF32 || epi == (int)Epi::kStoreF32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(Cout) + (int64_t)row * N + col);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 o = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            if (epi == (int)Epi::kAddF32) {
+              const float4 r = dst[j];
+              o.x += r.x;
+              o.y += r.y;
+              o.z += r.z;
+              o.w += r.w;
+            }
+            dst[j] = o;
+          }
+        } else {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (epi == (int)Epi::kBiasBf16) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] += bf2f(bias[col + j]);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<bf16*>(Cout) + (int64_t)row * N + col);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                                pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
+                                pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
+  const Driver* d = driver();
+  if (!d) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gemm_tc_supported(int M, int N, int K) { return M >= 16 && N % BN == 0 && K % BK == 0; }
+
+bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C, const bf16* bias,
+                    cudaStream_t st) {
+  if (!gemm_tc_supported(M, N, K)) return false;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, BM) || !make_map(&mb, B, N, K, BN)) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  count_launch();
+  gemm_tc_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, M, N, K, (int)epi, C, bias);
+  return true;
+}
+
+}  // namespace ws

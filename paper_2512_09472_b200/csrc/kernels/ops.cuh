@@ -61,6 +61,11 @@ void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
 // Legacy mma.sync GEMM (baseline + parity reference for the tcgen05 kernel).
 void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                      const bf16* bias, cudaStream_t st);
+// tcgen05/TMEM/TMA GEMM (gemm_tc.cu): needs M >= 16, N % 256 == 0, K % 64 == 0;
+// returns false (nothing launched) otherwise.
+bool gemm_tc_supported(int M, int N, int K);
+bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
+                    const bf16* bias, cudaStream_t st);
 // Skinny GEMM for M <= 16 (decode / lm_head rows): weight-streaming, HBM bound.
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                  const bf16* bias, cudaStream_t st);

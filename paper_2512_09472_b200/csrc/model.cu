@@ -317,12 +317,16 @@ int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32
   const bf16* a = static_cast<const bf16*>(A);
   const bf16* b = static_cast<const bf16*>(B);
   const bf16* bi = static_cast<const bf16*>(bias);
-  if (impl == 1 && M >= 16)
+  if (impl == 1 && M >= 16) {
     launch_gemm_mma(a, b, M, N, K, (Epi)epi, C, bi, st);
-  else if (impl == 2)
+  } else if (impl == 2) {
     launch_gemv(a, b, M, N, K, (Epi)epi, C, bi, st);
-  else
+  } else if (impl == 3) {
+    if (!launch_gemm_tc(a, b, M, N, K, (Epi)epi, C, bi, st))
+      WS_FAIL(WS_ERR_INVALID, "shape %dx%dx%d outside the tcgen05 tiling", M, N, K);
+  } else {
     launch_gemm(a, b, M, N, K, (Epi)epi, C, bi, st);
+  }
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }

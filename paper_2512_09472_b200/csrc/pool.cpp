@@ -78,8 +78,15 @@ struct ws_pool {
   int32_t max_seqs = 0, max_blocks = 0;
   std::vector<int32_t> seq_len;
   std::vector<char> seq_live;
-  int32_t* bt_host = nullptr;  // pinned on device pools
+  int32_t* bt_host = nullptr;  // host mirror of the block tables
   int32_t* bt_dev = nullptr;
+  // Block-table uploads go through a ring of pinned staging slots, each
+  // guarded by an event, so a later host write can never race an earlier
+  // queued copy (the mirror itself is rewritten freely).
+  static constexpr int kBtSlots = 4;
+  char* bt_stage = nullptr;
+  cudaEvent_t bt_ev[kBtSlots] = {};
+  int bt_next = 0;
   // ---- device ----
   const ws::Driver* drv = nullptr;
   std::vector<CUmemGenericAllocationHandle> handles;
@@ -385,12 +392,13 @@ int ws_pool_destroy(ws_pool* p) {
     if (p->stage_dev) cudaFree(p->stage_dev);
     if (p->stage_host) cudaFreeHost(p->stage_host);
     if (p->bt_dev) cudaFree(p->bt_dev);
-    if (p->bt_host) cudaFreeHost(p->bt_host);
+    if (p->bt_stage) cudaFreeHost(p->bt_stage);
+    for (cudaEvent_t e : p->bt_ev)
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {p->stage_ev, p->sw_start, p->sw_stop})
       if (e) cudaEventDestroy(e);
-  } else if (p->bt_host) {
-    free(p->bt_host);
   }
+  free(p->bt_host);
   delete p;
   return WS_OK;
 }
@@ -591,18 +599,22 @@ int ws_pool_seq_config(ws_pool* p, int32_t max_seqs, int32_t max_blocks) {
   if (max_seqs < 1 || max_blocks < 1) WS_FAIL(WS_ERR_INVALID, "bad sequence table shape");
   if (p->n_alloc) WS_FAIL(WS_ERR_STATE, "sequences still hold KV blocks");
   size_t bytes = (size_t)max_seqs * max_blocks * 4;
+  free(p->bt_host);
+  p->bt_host = static_cast<int32_t*>(malloc(bytes));
   if (p->on_device()) {
     WS_CUDA(cudaSetDevice(p->dev));
+    WS_CUDA(cudaDeviceSynchronize());
     if (p->bt_dev) cudaFree(p->bt_dev);
-    if (p->bt_host) cudaFreeHost(p->bt_host);
+    if (p->bt_stage) cudaFreeHost(p->bt_stage);
     p->bt_dev = nullptr;
-    p->bt_host = nullptr;
-    WS_CUDA(cudaHostAlloc(&p->bt_host, bytes, cudaHostAllocDefault));
+    p->bt_stage = nullptr;
     WS_CUDA(cudaMalloc(&p->bt_dev, bytes));
     WS_CUDA(cudaMemset(p->bt_dev, 0xff, bytes));
-  } else {
-    free(p->bt_host);
-    p->bt_host = static_cast<int32_t*>(malloc(bytes));
+    WS_CUDA(cudaHostAlloc(&p->bt_stage, (size_t)ws_pool::kBtSlots * max_blocks * 4, cudaHostAllocDefault));
+    for (auto& e : p->bt_ev) {
+      if (!e) WS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      WS_CUDA(cudaEventRecord(e, 0));
+    }
   }
   memset(p->bt_host, 0xff, bytes);
   p->max_seqs = max_seqs;
@@ -646,9 +658,15 @@ int ws_seq_reserve(ws_pool* p, int32_t seq, int32_t n_blocks, void* stream) {
   p->seq_len[seq] = n_blocks;
   if (p->on_device()) {
     WS_CUDA(cudaSetDevice(p->dev));
-    WS_CUDA(cudaMemcpyAsync(p->bt_dev + (int64_t)seq * p->max_blocks + have, row + have,
-                            (size_t)(n_blocks - have) * 4, cudaMemcpyHostToDevice,
-                            reinterpret_cast<cudaStream_t>(stream)));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int slot = p->bt_next;
+    p->bt_next = (p->bt_next + 1) % ws_pool::kBtSlots;
+    WS_CUDA(cudaEventSynchronize(p->bt_ev[slot]));  // the copy that last used this slot ran
+    int32_t* stage = reinterpret_cast<int32_t*>(p->bt_stage) + (int64_t)slot * p->max_blocks;
+    memcpy(stage, row + have, (size_t)(n_blocks - have) * 4);
+    WS_CUDA(cudaMemcpyAsync(p->bt_dev + (int64_t)seq * p->max_blocks + have, stage,
+                            (size_t)(n_blocks - have) * 4, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaEventRecord(p->bt_ev[slot], st));
   }
   return WS_OK;
 }

@@ -56,6 +56,34 @@ def test_gemm_against_fp32(lib, M, N, K, impl):
     assert _rel(acc, want) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (16, 256, 128), (100, 768, 256), (256, 512, 1024),
+                                   (2048, 6144, 4096), (2048, 4096, 14336), (1000, 28672, 4096)])
+def test_gemm_tcgen05_against_fp32(lib, M, N, K):
+    """impl 3 forces the tcgen05/TMEM/TMA kernel (no mma.sync fallback)."""
+    import ctypes as C
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    for epi in (0, 1, 2, 3):
+        if epi == 2:
+            out = torch.randn(M, N, device="cuda", generator=g)
+            want = out + ref
+        elif epi == 3:
+            out = torch.empty(M, N, device="cuda")
+            want = ref
+        else:
+            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            want = ref + (bias.float() if epi == 1 else 0)
+        lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, epi,
+                 C.c_void_p(out.data_ptr()), C.c_void_p(bias.data_ptr()), 3, None)
+        torch.cuda.synchronize()
+        tol = 1e-2 if epi in (0, 1) else 1e-4  # fp32 outputs: accumulation-order noise only
+        assert _rel(out.float(), want) < tol, (epi, _rel(out.float(), want))
+
+
 @pytest.mark.parametrize("M", [1, 3, 8, 16])
 def test_gemv_against_fp32(lib, M):
     import ctypes as C
