@@ -35,6 +35,14 @@ def unpack(cfg, layout, flat_bf16: torch.Tensor) -> dict:
     return out
 
 
+def split_gate_up(wgu: torch.Tensor, ffn: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Wgu stores gate and up rows interleaved in 128-row blocks
+    ([gate 0:128][up 0:128][gate 128:256]...), so a 256-wide GEMM tile holds
+    matching gate/up columns (SwiGLU fused in the epilogue)."""
+    blocks = wgu.view(ffn // 128, 2, 128, -1)
+    return blocks[:, 0].reshape(ffn, -1), blocks[:, 1].reshape(ffn, -1)
+
+
 def _rms(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
     return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
 
@@ -82,8 +90,7 @@ def forward(cfg, w: dict, tokens, pos0: int = 0, past: list | None = None):
         o = torch.einsum("hst,thd->shd", p, vv).reshape(S, H * hd)
         x = x + o @ w[f"l{l}.wo"].T
         h = _rms(x, w[f"l{l}.ffn_norm"], cfg.rms_eps)
-        gu = h @ w[f"l{l}.wgu"].T
-        gate, up = gu[:, : cfg.ffn], gu[:, cfg.ffn:]
-        x = x + (torch.nn.functional.silu(gate) * up) @ w[f"l{l}.wdown"].T
+        wg, wu = split_gate_up(w[f"l{l}.wgu"], cfg.ffn)
+        x = x + (torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ w[f"l{l}.wdown"].T
     h = _rms(x, w["final_norm"], cfg.rms_eps)
     return h @ w["lm_head"].T, new_past

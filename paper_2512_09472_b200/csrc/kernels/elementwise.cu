@@ -63,14 +63,19 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const float* __restri
   }
 }
 
-// act[r, j] = silu(g) * u with g = gu[r, j], u = gu[r, ffn + j].
+// act[r, j] = silu(g) * u. Gate/up rows of Wgu are interleaved in 128-row
+// blocks (layout of ws_model_layout), so g = gu[r, 256*(j/128) + j%128] and
+// u = gu[r, 256*(j/128) + 128 + j%128]. Used for the skinny (decode) path; the
+// tcgen05 GEMM applies SwiGLU in its epilogue instead.
 __global__ void __launch_bounds__(256) silu_mul_kernel(const bf16* __restrict__ gu,
                                                        bf16* __restrict__ act, int ffn) {
   const int r = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 8-element group
   if (i >= ffn / 8) return;
-  const uint4 g = __ldg(reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn) + i);
-  const uint4 u = __ldg(reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn + ffn) + i);
+  const int j = i * 8;
+  const int64_t g_off = (int64_t)r * 2 * ffn + (j >> 7) * 256 + (j & 127);
+  const uint4 g = __ldg(reinterpret_cast<const uint4*>(gu + g_off));
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(gu + g_off + 128));
   const uint32_t* gp = &g.x;
   const uint32_t* up = &u.x;
   uint4 o;

@@ -108,9 +108,137 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])              \
       : "r"(taddr))
 
+// 32 consecutive accumulator columns of one row -> bf16, 4 x 16 B stores
+__device__ __forceinline__ void store_bf16x32(bf16* dst, const float* f) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    d[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                      pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+}
+
+template <int MODE>
+__device__ __forceinline__ void epilogue_tile(const TcEpilogue& ep, uint32_t tacc, int row, int n0, int N,
+                                              int head_dim) {
+  if constexpr (MODE == (int)Epi::kSwiGLU) {
+    // tile columns [0,128) = gate block, [128,256) = matching up block
+    bf16* out = static_cast<bf16*>(ep.C) + (int64_t)row * (N / 2) + n0 / 2;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t g[32], u[32];
+      TMEM_LD32(tacc + c * 32, g);
+      TMEM_LD32(tacc + 128 + c * 32, u);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (row < 0) continue;
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = __uint_as_float(g[j]);
+        f[j] = x / (1.f + __expf(-x)) * __uint_as_float(u[j]);
+      }
+      store_bf16x32(out + c * 32, f);
+    }
+  } else if constexpr (MODE == (int)Epi::kRopeKV) {
+    // tile = BN/head_dim whole heads; rotate_half pairs (i, i + hd/2) sit in
+    // chunks (c, c + hd/64) of the same row, so one thread rotates its row.
+    const KvGeom& kv = ep.kv;
+    const int pos = row < 0 ? 0 : (ep.pos_arr ? ep.pos_arr[row] : ep.pos0 + row);
+    const int seq = row < 0 ? 0 : (ep.seq_arr ? ep.seq_arr[row] : ep.seq0);
+    const int half_chunks = head_dim / 64, per_head = head_dim / 32;
+    const float2* cs = ep.rope + (int64_t)pos * (head_dim / 2);
+    bf16* page = nullptr;
+    if (row >= 0) {
+      const int32_t pg = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
+      page = reinterpret_cast<bf16*>(kv.window + (int64_t)pg * kv.page_size) + (int64_t)(pos % kv.tpb) * head_dim;
+    }
+#pragma unroll 1
+    for (int hl = 0; hl < BN / head_dim; ++hl) {
+      const int hs = (n0 + hl * head_dim) / head_dim;  // head slot in [0, H + 2KV)
+      const bool is_v = hs >= ep.heads + kv.kv_heads;
+      const bool is_k = !is_v && hs >= ep.heads;
+#pragma unroll 1
+      for (int c = 0; c < half_chunks; ++c) {
+        uint32_t a[32], b[32];
+        const int ca = hl * per_head + c, cb = ca + half_chunks;
+        TMEM_LD32(tacc + ca * 32, a);
+        TMEM_LD32(tacc + cb * 32, b);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (row < 0) continue;
+        float fa[32], fb[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          fa[j] = __uint_as_float(a[j]);
+          fb[j] = __uint_as_float(b[j]);
+        }
+        if (ep.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            fa[j] += bf2f(ep.bias[n0 + ca * 32 + j]);
+            fb[j] += bf2f(ep.bias[n0 + cb * 32 + j]);
+          }
+        }
+        if (!is_v) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float2 t = cs[c * 32 + j];
+            const float x = fa[j], y = fb[j];
+            fa[j] = x * t.x - y * t.y;
+            fb[j] = y * t.x + x * t.y;
+          }
+        }
+        if (!is_k && !is_v) {
+          bf16* q = static_cast<bf16*>(ep.C) + (int64_t)row * N + n0;
+          store_bf16x32(q + ca * 32, fa);
+          store_bf16x32(q + cb * 32, fb);
+        } else {
+          const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
+          bf16* dst = page + kv.plane(ep.layer, is_v ? 1 : 0, kvh);
+          store_bf16x32(dst + c * 32, fa);
+          store_bf16x32(dst + c * 32 + head_dim / 2, fb);
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      TMEM_LD32(tacc + c * 32, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (row < 0) continue;
+      const int col = n0 + c * 32;
+      if constexpr (MODE == (int)Epi::kAddF32 || MODE == (int)Epi::kStoreF32) {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.C) + (int64_t)row * N + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 o = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          if constexpr (MODE == (int)Epi::kAddF32) {
+            const float4 r = dst[j];
+            o.x += r.x;
+            o.y += r.y;
+            o.z += r.z;
+            o.w += r.w;
+          }
+          dst[j] = o;
+        }
+      } else {
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        if constexpr (MODE == (int)Epi::kBiasBf16) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += bf2f(ep.bias[col + j]);
+        }
+        store_bf16x32(static_cast<bf16*>(ep.C) + (int64_t)row * N + col, f);
+      }
+    }
+  }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   int M, int N, int K, int epi, void* __restrict__ Cout, const bf16* __restrict__ bias) {
+                   int M, int N, int K, const __grid_constant__ TcEpilogue ep) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;  // SWIZZLE_128B atoms need 1024 B alignment
@@ -215,45 +343,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tfull(acc), acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      const bool ok = row < M;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (!ok) continue;
-        const int col = n0 + c * 32;
-        if (epi == (int)Epi::kAddF32 || epi == (int)Epi::kStoreF32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(Cout) + (int64_t)row * N + col);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 o = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-            if (epi == (int)Epi::kAddF32) {
-              const float4 r = dst[j];
-              o.x += r.x;
-              o.y += r.y;
-              o.z += r.z;
-              o.w += r.w;
-            }
-            dst[j] = o;
-          }
-        } else {
-          float f[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          if (epi == (int)Epi::kBiasBf16) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] += bf2f(bias[col + j]);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<bf16*>(Cout) + (int64_t)row * N + col);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                                pack_bf16x2(f[8 * j + 4], f[8 * j + 5]),
-                                pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
-        }
-      }
+      epilogue_tile<MODE>(ep, tmem + ((uint32_t)(q * 32) << 16) + acc * BN, row < M ? row : -1, n0, N,
+                          ep.kv.head_dim);
       tc_fence_before();
       mbar_arrive(tempty(acc));
       if (++acc == 2) {
@@ -286,21 +377,49 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) 
 
 bool gemm_tc_supported(int M, int N, int K) { return M >= 16 && N % BN == 0 && K % BK == 0; }
 
-bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C, const bf16* bias,
-                    cudaStream_t st) {
-  if (!gemm_tc_supported(M, N, K)) return false;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, A, M, K, BM) || !make_map(&mb, B, N, K, BN)) return false;
+bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim) {
+  if (e.mode == Epi::kRopeKV) return (head_dim == 64 || head_dim == 128) && N % BN == 0;
+  return true;
+}
+
+template <int MODE>
+void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
+                 cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   count_launch();
-  gemm_tc_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, M, N, K, (int)epi, C, bias);
+  gemm_tc_kernel<MODE><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, M, N, K, e);
+}
+
+bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
+                        cudaStream_t st) {
+  if (!gemm_tc_supported(M, N, K) || !gemm_tc_epilogue_supported(e, N, e.kv.head_dim)) return false;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, BM) || !make_map(&mb, B, N, K, BN)) return false;
+  switch (e.mode) {
+    case Epi::kStoreBf16: launch_mode<0>(ma, mb, M, N, K, e, st); break;
+    case Epi::kBiasBf16: launch_mode<1>(ma, mb, M, N, K, e, st); break;
+    case Epi::kAddF32: launch_mode<2>(ma, mb, M, N, K, e, st); break;
+    case Epi::kStoreF32: launch_mode<3>(ma, mb, M, N, K, e, st); break;
+    case Epi::kSwiGLU: launch_mode<4>(ma, mb, M, N, K, e, st); break;
+    case Epi::kRopeKV: launch_mode<5>(ma, mb, M, N, K, e, st); break;
+  }
   return true;
+}
+
+bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C, const bf16* bias,
+                    cudaStream_t st) {
+  if (epi == Epi::kSwiGLU || epi == Epi::kRopeKV) return false;
+  TcEpilogue e;
+  e.mode = epi;
+  e.C = C;
+  e.bias = bias;
+  return launch_gemm_tc_epi(A, B, M, N, K, e, st);
 }
 
 }  // namespace ws

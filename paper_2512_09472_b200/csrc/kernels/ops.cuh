@@ -54,7 +54,26 @@ void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,
 int decode_scratch_floats(int n_seqs, int heads, int head_dim, int max_ctx);
 
 // C[M,N] = A[M,K] * B[N,K]^T with epilogue:
-enum class Epi { kStoreBf16 = 0, kBiasBf16 = 1, kAddF32 = 2, kStoreF32 = 3 };
+//   kSwiGLU  (tcgen05 only): B = interleaved gate/up rows (128-row blocks);
+//            C = bf16 [M, N/2] = silu(gate) * up
+//   kRopeKV  (tcgen05 only): B = Wqkv; optional bias; q/k heads rotated (RoPE),
+//            q written to C ([M, N] bf16), k/v appended to the paged cache
+enum class Epi { kStoreBf16 = 0, kBiasBf16 = 1, kAddF32 = 2, kStoreF32 = 3, kSwiGLU = 4, kRopeKV = 5 };
+
+struct TcEpilogue {
+  Epi mode = Epi::kStoreBf16;
+  void* C = nullptr;
+  const bf16* bias = nullptr;
+  // kRopeKV
+  const float2* rope = nullptr;
+  KvGeom kv{};
+  int layer = 0, heads = 0, seq0 = 0, pos0 = 0;
+  const int32_t* seq_arr = nullptr;
+  const int32_t* pos_arr = nullptr;
+};
+bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim);
+bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
+                        cudaStream_t st);
 // Dispatch: M >= 16 -> tensor-core GEMM, else the skinny GEMV.
 void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                  const bf16* bias, cudaStream_t st);

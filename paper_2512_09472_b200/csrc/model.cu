@@ -36,7 +36,7 @@ int qkv_dim(const ws_model_config& c) { return (c.heads + 2 * c.kv_heads) * c.he
 bool valid_cfg(const ws_model_config& c) {
   return c.layers > 0 && c.hidden > 0 && c.ffn > 0 && c.heads > 0 && c.kv_heads > 0 &&
          c.heads % c.kv_heads == 0 && (c.head_dim == 64 || c.head_dim == 96 || c.head_dim == 128) &&
-         c.vocab > 0 && c.hidden % 32 == 0 && c.ffn % 32 == 0 && c.max_positions > 0 &&
+         c.vocab > 0 && c.hidden % 32 == 0 && c.ffn % 128 == 0 && c.max_positions > 0 &&
          c.heads / c.kv_heads <= 8;
 }
 
@@ -116,6 +116,48 @@ void gemm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N,
     ws::launch_gemm_mma(A, B, M, N, K, e, C, bias, st);
   else
     ws::launch_gemm(A, B, M, N, K, e, C, bias, st);
+}
+
+// QKV projection + RoPE + paged KV append. One tcgen05 launch with the fused
+// epilogue when the shape allows it, else GEMM then the rope_kv kernel.
+void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws::bf16* b, int rows,
+              const ws::KvGeom& kv, int layer, int seq0, int pos0, const int32_t* seqs, const int32_t* pos,
+              ws::bf16* qkv, cudaStream_t st) {
+  using namespace ws;
+  const ws_model_config& c = m->cfg;
+  const int q = (c.heads + 2 * c.kv_heads) * c.head_dim;
+  if (m->gemm_impl == 0 && rows >= 16) {
+    TcEpilogue e;
+    e.mode = Epi::kRopeKV;
+    e.C = qkv;
+    e.bias = b;
+    e.rope = m->rope;
+    e.kv = kv;
+    e.layer = layer;
+    e.heads = c.heads;
+    e.seq0 = seq0;
+    e.pos0 = pos0;
+    e.seq_arr = seqs;
+    e.pos_arr = pos;
+    if (launch_gemm_tc_epi(h, w, rows, q, c.hidden, e, st)) return;
+  }
+  gemm(m, h, w, rows, q, c.hidden, b ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv, b, st);
+  launch_rope_kv(qkv, m->rope, kv, layer, rows, c.heads, seqs, pos, seq0, pos0, st);
+}
+
+// gate/up projection + SwiGLU (fused epilogue on the tcgen05 path).
+void gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int rows, ws::bf16* gu,
+                    ws::bf16* act, cudaStream_t st) {
+  using namespace ws;
+  const ws_model_config& c = m->cfg;
+  if (m->gemm_impl == 0 && rows >= 16) {
+    TcEpilogue e;
+    e.mode = Epi::kSwiGLU;
+    e.C = act;
+    if (launch_gemm_tc_epi(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;
+  }
+  gemm(m, h, w, rows, 2 * c.ffn, c.hidden, Epi::kStoreBf16, gu, nullptr, st);
+  launch_silu_mul(gu, act, rows, c.ffn, st);
 }
 
 int kv_geom(ws_model* m, ws_pool* pool, ws::KvGeom* g) {
@@ -244,14 +286,12 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
       if (int e = ws_streamer_wait(streamer, l - first_streamed, stream)) return e;
     const auto& Ly = L.layers[l];
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
-    gemm(m, h, W<bf16>(wts, Ly.wqkv), rows, q, d, c.qkv_bias ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv,
-         c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, st);
-    launch_rope_kv(qkv, m->rope, kv, l, rows, c.heads, nullptr, nullptr, seq, pos0, st);
+    qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, rows, kv, l, seq,
+             pos0, nullptr, nullptr, qkv, st);
     launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
     gemm(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, Epi::kAddF32, x, nullptr, st);
     launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, rows, d, c.rms_eps, st);
-    gemm(m, h, W<bf16>(wts, Ly.wgu), rows, 2 * c.ffn, d, Epi::kStoreBf16, gu, nullptr, st);
-    launch_silu_mul(gu, act, rows, c.ffn, st);
+    gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), rows, gu, act, st);
     gemm(m, act, W<bf16>(wts, Ly.wdown), rows, d, c.ffn, Epi::kAddF32, x, nullptr, st);
   }
   if (streamer && c.layers >= first_streamed)
@@ -292,14 +332,12 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   for (int l = 0; l < c.layers; ++l) {
     const auto& Ly = L.layers[l];
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, n, d, c.rms_eps, st);
-    gemm(m, h, W<bf16>(wts, Ly.wqkv), n, q, d, c.qkv_bias ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv,
-         c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, st);
-    launch_rope_kv(qkv, m->rope, kv, l, n, c.heads, seqs, pos, 0, 0, st);
+    qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
+             pos, qkv, st);
     launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
     gemm(m, attn, W<bf16>(wts, Ly.wo), n, d, o, Epi::kAddF32, x, nullptr, st);
     launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
-    gemm(m, h, W<bf16>(wts, Ly.wgu), n, 2 * c.ffn, d, Epi::kStoreBf16, gu, nullptr, st);
-    launch_silu_mul(gu, act, n, c.ffn, st);
+    gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);
     gemm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, Epi::kAddF32, x, nullptr, st);
   }
   launch_rmsnorm(x, W<bf16>(wts, L.final_norm), hl, n, d, c.rms_eps, st);

@@ -45,8 +45,9 @@ def _hf_llama(cfg, w):
         sd[p + "self_attn.o_proj.weight"] = w[f"l{l}.wo"]
         sd[p + "input_layernorm.weight"] = w[f"l{l}.attn_norm"]
         sd[p + "post_attention_layernorm.weight"] = w[f"l{l}.ffn_norm"]
-        sd[p + "mlp.gate_proj.weight"] = w[f"l{l}.wgu"][: cfg.ffn]
-        sd[p + "mlp.up_proj.weight"] = w[f"l{l}.wgu"][cfg.ffn:]
+        gate, up = O.split_gate_up(w[f"l{l}.wgu"], cfg.ffn)
+        sd[p + "mlp.gate_proj.weight"] = gate
+        sd[p + "mlp.up_proj.weight"] = up
         sd[p + "mlp.down_proj.weight"] = w[f"l{l}.wdown"]
     missing, unexpected = model.load_state_dict(sd, strict=False)
     assert not unexpected, unexpected
