@@ -215,7 +215,8 @@ typedef struct ws_model ws_model;
 int ws_model_create(const ws_model_config* cfg, int32_t device, ws_model** out);
 int ws_model_destroy(ws_model* m);
 int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* bytes_out);
-/* 0 = tensor-core GEMM (default), 1 = legacy mma.sync baseline (tests / A-B). */
+/* Kernel selection bits (A/B tests): 0 = tcgen05 GEMMs + tcgen05 attention (default);
+ * bit 0 = legacy mma.sync GEMMs, bit 1 = legacy mma.sync attention (3 = all legacy). */
 int ws_model_set_gemm(ws_model* m, int32_t impl);
 
 /* Prefill `rows` new tokens of sequence `seq` (positions pos0..pos0+rows-1;

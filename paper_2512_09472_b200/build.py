@@ -26,6 +26,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
           f"-I{INCLUDE}", f"-I{CSRC}"]
 CUDA_ONLY = ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
+if os.environ.get("WS_DEBUG_WAIT"):  # watchdog build of the mbarrier waits (debugging only)
+    CUDA_ONLY.append("-DWS_DEBUG_WAIT")
 
 
 def _nvcc() -> str:

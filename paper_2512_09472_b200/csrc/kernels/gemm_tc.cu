@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer =====
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    __syncwarp();  // reconverge before the CTA-wide (aligned) barrier below
   } else if (warp >= 4) {
     // ===== epilogue: TMEM lanes 32*q .. 32*q+31 belong to warp q = warp % 4 =====
     const int q = warp & 3;

@@ -46,6 +46,11 @@ void launch_rope_kv(bf16* qkv, const float2* rope_table, const KvGeom& kv, int l
 void launch_attn_prefill(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq,
                          int rows, int pos0, int heads, float scale, cudaStream_t st);
 
+// tcgen05/TMEM flash-attention version (attn_tc.cu), head_dim 64 or 128;
+// returns false (nothing launched) for other head dims.
+bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows,
+                            int pos0, int heads, float scale, cudaStream_t st);
+
 // One query token per sequence: seqs[i] at position pos[i] (context pos+1,
 // its own K/V already appended). scratch: decode_scratch_floats() floats.
 void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,

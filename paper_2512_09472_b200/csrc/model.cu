@@ -112,7 +112,7 @@ namespace {
 
 void gemm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N, int K, ws::Epi e,
           void* C, const ws::bf16* bias, cudaStream_t st) {
-  if (m->gemm_impl == 1 && M >= 16)
+  if ((m->gemm_impl & 1) && M >= 16)
     ws::launch_gemm_mma(A, B, M, N, K, e, C, bias, st);
   else
     ws::launch_gemm(A, B, M, N, K, e, C, bias, st);
@@ -126,7 +126,7 @@ void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
   using namespace ws;
   const ws_model_config& c = m->cfg;
   const int q = (c.heads + 2 * c.kv_heads) * c.head_dim;
-  if (m->gemm_impl == 0 && rows >= 16) {
+  if (!(m->gemm_impl & 1) && rows >= 16) {
     TcEpilogue e;
     e.mode = Epi::kRopeKV;
     e.C = qkv;
@@ -150,7 +150,7 @@ void gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int
                     ws::bf16* act, cudaStream_t st) {
   using namespace ws;
   const ws_model_config& c = m->cfg;
-  if (m->gemm_impl == 0 && rows >= 16) {
+  if (!(m->gemm_impl & 1) && rows >= 16) {
     TcEpilogue e;
     e.mode = Epi::kSwiGLU;
     e.C = act;
@@ -250,7 +250,7 @@ int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* byt
 }
 
 int ws_model_set_gemm(ws_model* m, int32_t impl) {
-  if (!m || impl < 0 || impl > 1) WS_FAIL(WS_ERR_INVALID, "gemm impl must be 0 or 1");
+  if (!m || impl < 0 || impl > 3) WS_FAIL(WS_ERR_INVALID, "impl must be in 0..3");
   m->gemm_impl = impl;
   return WS_OK;
 }
@@ -288,7 +288,8 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, rows, kv, l, seq,
              pos0, nullptr, nullptr, qkv, st);
-    launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
+    if ((m->gemm_impl & 2) || !launch_attn_prefill_tc(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st))
+      launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
     gemm(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, Epi::kAddF32, x, nullptr, st);
     launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, rows, d, c.rms_eps, st);
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), rows, gu, act, st);
