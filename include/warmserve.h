@@ -135,6 +135,13 @@ int ws_pool_sync_unmaps(ws_pool* pool);
  * map_now=1 maps all of them before returning (device pools); map_now=0 lets
  * the caller drive ws_slot_map_chunk() from the pipelined loader. */
 int ws_slot_create(ws_pool* pool, int64_t slot_id, int64_t pages, int32_t map_now, void** va_out);
+/* Same, with a per-model key (nonzero): the slot VA is cached across
+ * evictions, so a later slot of the same model only remaps the pages whose
+ * physical identity changed (evicted keyed slots keep their mappings). */
+int ws_slot_create_keyed(ws_pool* pool, int64_t slot_id, int64_t pages, int32_t map_now, uint64_t key,
+                         void** va_out);
+/* Slot pages mapped by the driver vs served from the VA cache, since create. */
+int ws_pool_map_stats(ws_pool* pool, int64_t* remapped_pages, int64_t* reused_pages);
 /* Map pages [first, first+count) of the slot into its VA (memswitch.py:78-88
  * per-chunk map step). */
 int ws_slot_map_chunk(ws_pool* pool, int64_t slot_id, int64_t first, int64_t count);

@@ -88,6 +88,8 @@ SIGNATURES: dict[str, list] = {
     "ws_pool_timing": [vp, P(f64), P(f64), P(f64)],
     "ws_pool_sync_unmaps": [vp],
     "ws_slot_create": [vp, i64, i64, i32, P(vp)],
+    "ws_slot_create_keyed": [vp, i64, i64, i32, C.c_uint64, P(vp)],
+    "ws_pool_map_stats": [vp, P(i64), P(i64)],
     "ws_slot_map_chunk": [vp, i64, i64, i64],
     "ws_slot_evict": [vp, i64, vp],
     "ws_slot_info": [vp, i64, P(i64), P(i64), P(vp)],

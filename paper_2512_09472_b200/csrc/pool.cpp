@@ -39,6 +39,18 @@ struct Slot {
   std::vector<int32_t> pages;  // slot page j -> physical page id
   int64_t mapped = 0;          // pages [0, mapped) mapped into the slot VA
   int va = -1;                 // index into ws_pool::vas
+  uint64_t key = 0;            // model key of a cached VA (0: unkeyed slot)
+};
+
+// Per-model VA cache: an evicted keyed slot keeps its VA mappings (nothing
+// reads them while the model is not active), so re-prewarming the same model
+// only remaps the slot pages whose physical page changed. Driver map/access
+// calls cost ~0.2-1.5 ms per 2 MiB handle on this B200, so this turns a
+// re-prewarm of an 8B slot from seconds into (usually) zero driver calls.
+struct CachedVa {
+  int va = -1;
+  std::vector<int32_t> phys;  // physical page mapped at slot page j, -1 if none
+  bool in_use = false;
 };
 
 struct VaRange {
@@ -99,6 +111,8 @@ struct ws_pool {
   bool sw_recorded = false;
   int64_t sw_entries = 0;
   std::vector<VaRange> vas;
+  std::unordered_map<uint64_t, CachedVa> va_cache;
+  int64_t remapped_pages = 0, reused_pages = 0;
   // ---- background unmap worker ----
   std::mutex mu;
   std::condition_variable cv, cv_done;
@@ -223,14 +237,33 @@ int map_range(ws_pool* p, Slot& s, int64_t first, int64_t count) {
   }
   double t0 = now_ms();
   CUdeviceptr base = p->va_base(s.va);
-  for (int64_t j = first; j < first + count; ++j)
-    DRV(p->drv->cuMemMap(base + j * p->page, (size_t)p->page, 0, p->handles[s.pages[j]], 0));
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = p->dev;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  DRV(p->drv->cuMemSetAccess(base + first * p->page, (size_t)(count * p->page), &acc, 1));
-  p->map_ms_per_page = (now_ms() - t0) / (double)count;
+  std::vector<int32_t>* phys = nullptr;
+  if (s.key) {
+    phys = &p->va_cache[s.key].phys;
+    if ((int64_t)phys->size() < first + count) phys->resize(first + count, -1);
+  }
+  // map only pages whose cached physical page differs; coalesce SetAccess runs
+  int64_t run = -1, changed = 0;
+  for (int64_t j = first; j <= first + count; ++j) {
+    const bool need = j < first + count && (!phys || (*phys)[j] != s.pages[j]);
+    if (need) {
+      if (phys && (*phys)[j] >= 0) DRV(p->drv->cuMemUnmap(base + j * p->page, (size_t)p->page));
+      DRV(p->drv->cuMemMap(base + j * p->page, (size_t)p->page, 0, p->handles[s.pages[j]], 0));
+      if (phys) (*phys)[j] = s.pages[j];
+      if (run < 0) run = j;
+      ++changed;
+    } else if (run >= 0) {
+      DRV(p->drv->cuMemSetAccess(base + run * p->page, (size_t)((j - run) * p->page), &acc, 1));
+      run = -1;
+    }
+  }
+  if (changed) p->map_ms_per_page = (now_ms() - t0) / (double)changed;
+  p->remapped_pages += changed;
+  p->reused_pages += count - changed;
   s.mapped += count;
   return WS_OK;
 }
@@ -382,8 +415,12 @@ int ws_pool_destroy(ws_pool* p) {
     cudaSetDevice(p->dev);
     cudaDeviceSynchronize();
     for (auto& kv : p->slots)
-      for (int64_t j = 0; j < kv.second.mapped; ++j)
-        p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
+      if (!kv.second.key)
+        for (int64_t j = 0; j < kv.second.mapped; ++j)
+          p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
+    for (auto& kv : p->va_cache)
+      for (size_t j = 0; j < kv.second.phys.size(); ++j)
+        if (kv.second.phys[j] >= 0) p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
     for (auto& v : p->vas) p->drv->cuMemAddressFree(v.base, (size_t)(p->n * p->page));
     for (size_t i = 0; i < p->handles.size(); ++i) p->drv->cuMemUnmap(p->window + i * p->page, p->page);
     for (auto h : p->handles) p->drv->cuMemRelease(h);
@@ -459,6 +496,11 @@ int ws_pool_sync_unmaps(ws_pool* p) {
 }
 
 int ws_slot_create(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map_now, void** va_out) {
+  return ws_slot_create_keyed(p, slot_id, pages, map_now, 0, va_out);
+}
+
+int ws_slot_create_keyed(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map_now, uint64_t key,
+                         void** va_out) {
   if (int e = check_pool(p)) return e;
   if (slot_id < 0 || slot_id > INT32_MAX) WS_FAIL(WS_ERR_INVALID, "slot id out of range");
   if (p->slots.count(slot_id)) WS_FAIL(WS_ERR_DUPLICATE, "already holds slot %lld", (long long)slot_id);
@@ -472,7 +514,16 @@ int ws_slot_create(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map_now, 
     if (p->owner[q] == kOwnerFree) s.pages.push_back((int32_t)q);
   if (p->on_device()) {
     WS_CUDA(cudaSetDevice(p->dev));
-    if (int e = acquire_va(p, &s.va)) return e;
+    auto hit = key ? p->va_cache.find(key) : p->va_cache.end();
+    if (hit != p->va_cache.end() && !hit->second.in_use) {
+      s.va = hit->second.va;  // mappings of the previous residency stay valid
+    } else {
+      if (hit != p->va_cache.end()) WS_FAIL(WS_ERR_DUPLICATE, "model key already has a live slot");
+      if (int e = acquire_va(p, &s.va)) return e;
+      if (key) p->va_cache[key].va = s.va;
+    }
+    if (key) p->va_cache[key].in_use = true;
+    s.key = key;
   }
   for (int32_t q : s.pages) p->owner[q] = (int32_t)slot_id;
   p->n_free -= pages;
@@ -505,6 +556,10 @@ int ws_slot_evict(ws_pool* p, int64_t slot_id, void* fence_stream) {
   if (!p->on_device()) return WS_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(fence_stream);
   if (int e = device_switch(p, one_rule((int32_t)slot_id, kOwnerFree), {}, 0, {}, st)) return e;
+  if (s.key) {  // keep the mappings for the next residency of this model
+    p->va_cache[s.key].in_use = false;
+    return WS_OK;
+  }
   UnmapJob job{s.va, p->va_base(s.va), s.mapped, nullptr};
   WS_CUDA(cudaEventCreateWithFlags(&job.fence, cudaEventDisableTiming));
   WS_CUDA(cudaEventRecord(job.fence, st));
@@ -731,3 +786,10 @@ int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_
   return WS_OK;
 }
 }  // namespace ws
+
+extern "C" int ws_pool_map_stats(ws_pool* p, int64_t* remapped, int64_t* reused) {
+  if (int e = check_pool(p)) return e;
+  *remapped = p->remapped_pages;
+  *reused = p->reused_pages;
+  return WS_OK;
+}
