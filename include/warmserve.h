@@ -97,7 +97,9 @@ int ws_background_kv_mapping(int64_t pages, double map_ms_per_page, double consu
  * background worker (engine.py:615-632 async-unmap contract).
  *
  * Page identity rules (documented, deterministic; the reference pins only
- * counts): a new slot takes the lowest-id free pages; promotion turns every
+ * counts): a new slot takes the lowest-id free pages (a keyed slot on a device
+ * pool first reclaims, at the same slot index, the still-free pages its cached
+ * VA maps, so a re-prewarm needs no driver calls for them); promotion turns every
  * free page into KV; a KV shrink returns the highest-id KV pages, migrating
  * any live KV block that sits on one of them to the lowest-id unallocated
  * KV page that stays.

@@ -509,9 +509,28 @@ int ws_slot_create_keyed(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map
     WS_FAIL(WS_ERR_INSUFFICIENT, "insufficient pages (need %lld, free %lld)", (long long)pages,
             (long long)p->n_free);
   Slot s;
-  s.pages.reserve(pages);
-  for (int64_t q = 0; q < p->n && (int64_t)s.pages.size() < pages; ++q)
-    if (p->owner[q] == kOwnerFree) s.pages.push_back((int32_t)q);
+  s.pages.assign(pages, -1);
+  // Identity rule: a keyed slot on a device pool first takes back, at the same
+  // slot index, every page its cached VA still maps that is free now (no
+  // driver call needed for those); every other index gets the lowest free
+  // page. Unkeyed / ledger-only slots: lowest free pages in order.
+  auto cached = (key && p->on_device()) ? p->va_cache.find(key) : p->va_cache.end();
+  if (cached != p->va_cache.end() && !cached->second.in_use) {
+    const auto& ph = cached->second.phys;
+    for (int64_t j = 0; j < pages && j < (int64_t)ph.size(); ++j)
+      if (ph[j] >= 0 && p->owner[ph[j]] == kOwnerFree) {
+        s.pages[j] = ph[j];
+        p->owner[ph[j]] = (int32_t)slot_id;  // claimed (final owner below)
+      }
+  }
+  {
+    int64_t q = 0;
+    for (int64_t j = 0; j < pages; ++j) {
+      if (s.pages[j] >= 0) continue;
+      while (p->owner[q] != kOwnerFree) ++q;
+      s.pages[j] = (int32_t)q++;
+    }
+  }
   if (p->on_device()) {
     WS_CUDA(cudaSetDevice(p->dev));
     auto hit = key ? p->va_cache.find(key) : p->va_cache.end();

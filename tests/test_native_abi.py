@@ -6,6 +6,8 @@ from paper_2512_09472_b200 import _native as N
 
 
 def test_every_declared_symbol_is_exported_and_bound():
+    from paper_2512_09472_b200 import models  # noqa: F401  (binds the model entry points)
+
     declared = N.declared_symbols()
     assert len(declared) >= 30
     for name in declared:

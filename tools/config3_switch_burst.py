@@ -95,7 +95,20 @@ def main():
     rng = random.Random(a.seed)
     lat = {"promote": [], "reclaim": [], "release": [], "prefill": [], "proactive_prewarm": []}
     kernel_us = []
+    import ctypes as C
+
+    from paper_2512_09472_b200 import _native as NN
+
+    def progress(tag):
+        rm, ru = C.c_int64(), C.c_int64()
+        NN.call("ws_pool_map_stats", w.gpu.pool, C.byref(rm), C.byref(ru))
+        print(f"[{time.perf_counter() - t0:8.1f}s] {tag}: remapped {rm.value} reused {ru.value} pages",
+              file=sys.stderr, flush=True)
+
+    progress(f"init {init_s:.1f}s, initial prewarm {[round(x) for x in prewarm_ms]} ms")
     for i in range(a.switches):
+        if i % 10 == 0:
+            progress(f"switch {i}")
         resident = sorted(w.gpu.slots)
         m = rng.choice(resident)
         # ---- activate: weight -> KV switch
