@@ -207,7 +207,18 @@ typedef struct ws_model_config {
   float rope_theta, rms_eps;
   int32_t qkv_bias;       /* Qwen2.5-style q/k/v biases */
   int32_t max_positions;  /* RoPE table length */
+  int32_t lm_head_rows;   /* vocab-parallel lm_head shard rows (0 = vocab) */
 } ws_model_config;
+
+/* ---- tensor parallelism (config 4): NCCL communicator, created once at
+ * prewarm time. With a communicator set on a model, the
+ * row-parallel O and down projections write fp32 partials that are
+ * all-reduced (sum) before the residual add, and the vocab-parallel lm_head
+ * shards are all-gathered into full logits. ---- */
+typedef struct ws_comm ws_comm;
+int ws_nccl_unique_id(uint8_t* out, int32_t n);  /* n >= 128 */
+int ws_comm_create(const uint8_t* unique_id, int32_t rank, int32_t nranks, int32_t device, ws_comm** out);
+int ws_comm_destroy(ws_comm* comm);
 
 /* Weight layout of one (TP-partition of a) model inside its slot: byte
  * offsets, every tensor 256-byte aligned. offsets_out receives
@@ -244,6 +255,10 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* weights, int32_t se
 int ws_model_decode(ws_model* m, ws_pool* pool, const void* weights, const int32_t* seqs_dev,
                     const int32_t* pos_dev, const int32_t* tokens_dev, int32_t n, int32_t max_ctx,
                     void* workspace, float* logits_dev, int32_t* next_tokens_dev, void* stream);
+
+/* Attach a TP communicator (NULL detaches). The model config must be the
+ * rank's shard (heads/TP, kv_heads/TP, ffn/TP, lm_head_rows = vocab/TP). */
+int ws_model_set_comm(ws_model* m, ws_comm* comm);
 
 /* Standalone GEMM entry for tests/bench: C = A[M,K] * B[N,K]^T, epilogue
  * 0 bf16, 1 bf16+bias, 2 fp32 accumulate, 3 fp32 store; impl as above. */

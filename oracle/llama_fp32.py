@@ -55,6 +55,40 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
     return torch.cat([a * c - b * s, b * c + a * s], dim=-1)
 
 
+def forward_tp(cfg_shard, w: dict, tokens, allreduce, allgather):
+    """Tensor-parallel restatement for one rank: local heads / ffn slice /
+    vocab slice; ``allreduce(t)`` sums a tensor over ranks in place,
+    ``allgather(t)`` returns the rank tensors concatenated on the last dim.
+    Mathematically equal to ``forward`` of the full model (Megatron split)."""
+    tokens = torch.as_tensor(tokens, dtype=torch.long)
+    S = tokens.numel()
+    H, KV, hd = cfg_shard.heads, cfg_shard.kv_heads, cfg_shard.head_dim
+    cos, sin = rope_table(hd, cfg_shard.rope_theta, S)
+    x = w["embed"][tokens]
+    for l in range(cfg_shard.layers):
+        h = _rms(x, w[f"l{l}.attn_norm"], cfg_shard.rms_eps)
+        qkv = h @ w[f"l{l}.wqkv"].T
+        if f"l{l}.bqkv" in w:
+            qkv = qkv + w[f"l{l}.bqkv"]
+        q = _rope(qkv[:, : H * hd].view(S, H, hd), cos, sin)
+        k = _rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin)
+        v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+        g = H // KV
+        sc = torch.einsum("shd,thd->hst", q, k.repeat_interleave(g, 1)) / math.sqrt(hd)
+        sc = sc.masked_fill(torch.ones(S, S, dtype=torch.bool).triu(1)[None], float("-inf"))
+        o = torch.einsum("hst,thd->shd", torch.softmax(sc, -1), v.repeat_interleave(g, 1)).reshape(S, H * hd)
+        part = o @ w[f"l{l}.wo"].T
+        allreduce(part)
+        x = x + part
+        h = _rms(x, w[f"l{l}.ffn_norm"], cfg_shard.rms_eps)
+        wg, wu = split_gate_up(w[f"l{l}.wgu"], cfg_shard.ffn)
+        part = (torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ w[f"l{l}.wdown"].T
+        allreduce(part)
+        x = x + part
+    h = _rms(x, w["final_norm"], cfg_shard.rms_eps)
+    return allgather(h @ w["lm_head"].T)
+
+
 def forward(cfg, w: dict, tokens, pos0: int = 0, past: list | None = None):
     """Logits [S, vocab] for tokens at positions pos0.. with optional past
     K/V (list per layer of (k [P, kvh, hd], v)). Returns (logits, new_past)."""

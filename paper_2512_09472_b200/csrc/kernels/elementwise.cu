@@ -181,7 +181,42 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
   }
 }
 
+__global__ void __launch_bounds__(256) add_f32_kernel(float4* __restrict__ x, const float4* __restrict__ p,
+                                                      int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = x[i];
+    const float4 b = p[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    x[i] = a;
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_vocab_kernel(const float* __restrict__ g, float* __restrict__ out,
+                                                           int tp, int rows, int vs) {
+  const int r = blockIdx.y, shard = blockIdx.z;
+  const float* src = g + ((int64_t)shard * rows + r) * vs;
+  float* dst = out + (int64_t)r * tp * vs + (int64_t)shard * vs;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < vs; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace
+
+void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st) {
+  count_launch();
+  const int64_t n4 = count / 4;  // hidden sizes are multiples of 32
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  add_f32_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(x), reinterpret_cast<const float4*>(p), n4);
+}
+
+void launch_gather_vocab(const float* g, float* out, int tp, int rows, int vs, cudaStream_t st) {
+  count_launch();
+  dim3 grid((vs + 1023) / 1024, rows, tp);
+  gather_vocab_kernel<<<grid, 256, 0, st>>>(g, out, tp, rows, vs);
+}
 
 void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n, int d, cudaStream_t st) {
   count_launch();

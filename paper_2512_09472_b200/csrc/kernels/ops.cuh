@@ -93,6 +93,10 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, 
 // Skinny GEMM for M <= 16 (decode / lm_head rows): weight-streaming, HBM bound.
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                  const bf16* bias, cudaStream_t st);
+// TP boundary helpers: x += p (fp32, count elements); reorder all-gathered
+// vocab shards [tp][rows][vs] into logits [rows][tp*vs].
+void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st);
+void launch_gather_vocab(const float* gathered, float* logits, int tp, int rows, int vs, cudaStream_t st);
 // Logits (fp32) for M rows and their argmax.
 void launch_argmax(const float* logits, int M, int V, int32_t* out, float* scratch, cudaStream_t st);
 

@@ -12,6 +12,7 @@
 
 #include "common.h"
 #include "kernels/ops.cuh"
+#include "tp.h"
 
 namespace ws {
 int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_tables,
@@ -64,14 +65,16 @@ Layout make_layout(const ws_model_config& c) {
     L.layers.push_back(x);
   }
   L.final_norm = take(d * 2);
-  L.lm_head = take((int64_t)c.vocab * d * 2);
+  L.lm_head = take((int64_t)(c.lm_head_rows > 0 ? c.lm_head_rows : c.vocab) * d * 2);
   L.total = off;
   return L;
 }
 
 struct Workspace {
-  int64_t x, h, qkv, attn, gu, act, hl, seqs, scratch, total;
+  int64_t x, h, qkv, attn, gu, act, hl, seqs, scratch, partial, shard_logits, gathered, total;
 };
+
+int head_rows(const ws_model_config& c) { return c.lm_head_rows > 0 ? c.lm_head_rows : c.vocab; }
 
 int decode_cap(int max_tokens) { return max_tokens < 256 ? max_tokens : 256; }
 
@@ -94,6 +97,11 @@ Workspace make_ws(const ws_model_config& c, int T) {
   w.seqs = take(4 * 4);
   w.scratch = take((int64_t)ws::decode_scratch_floats(decode_cap(T), c.heads, c.head_dim,
                                                       c.max_positions) * 4);
+  // TP only: fp32 row-parallel partials and the local lm_head shard logits
+  const bool tp = head_rows(c) != c.vocab;
+  w.partial = take(tp ? (int64_t)T * d * 4 : 0);
+  w.shard_logits = take(tp ? (int64_t)decode_cap(T) * head_rows(c) * 4 : 0);
+  w.gathered = take(tp ? (int64_t)decode_cap(T) * c.vocab * 4 : 0);
   w.total = off;
   return w;
 }
@@ -106,6 +114,7 @@ struct ws_model {
   int device = 0;
   float2* rope = nullptr;  // [max_positions, head_dim/2] (cos, sin)
   int gemm_impl = 0;
+  ws_comm* comm = nullptr;  // TP group (config 4); null = single GPU
 };
 
 namespace {
@@ -158,6 +167,39 @@ void gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int
   }
   gemm(m, h, w, rows, 2 * c.ffn, c.hidden, Epi::kStoreBf16, gu, nullptr, st);
   launch_silu_mul(gu, act, rows, c.ffn, st);
+}
+
+// Row-parallel projection + residual add: x += A.B^T, summed over the TP group
+// (NCCL allreduce of the fp32 partial on the TP boundary).
+int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N, int K, float* x,
+                 float* partial, cudaStream_t st) {
+  using namespace ws;
+  if (!m->comm) {
+    gemm(m, A, B, M, N, K, Epi::kAddF32, x, nullptr, st);
+    return WS_OK;
+  }
+  gemm(m, A, B, M, N, K, Epi::kStoreF32, partial, nullptr, st);
+  if (int e = comm_allreduce_f32(m->comm, partial, (int64_t)M * N, st)) return e;
+  launch_add_f32(x, partial, (int64_t)M * N, st);
+  return WS_OK;
+}
+
+// lm_head for `rows` normalized rows -> fp32 logits [rows, vocab] + argmax.
+// TP: each rank holds vocab/TP rows; shards are all-gathered and reordered.
+int lm_head(const ws_model* m, const ws::bf16* hl, const ws::bf16* W, int rows, float* logits,
+            float* shard, float* gathered, int32_t* next, cudaStream_t st) {
+  using namespace ws;
+  const ws_model_config& c = m->cfg;
+  const int Vs = head_rows(c);
+  if (!m->comm) {
+    gemm(m, hl, W, rows, c.vocab, c.hidden, Epi::kStoreF32, logits, nullptr, st);
+  } else {
+    gemm(m, hl, W, rows, Vs, c.hidden, Epi::kStoreF32, shard, nullptr, st);
+    if (int e = comm_allgather_f32(m->comm, shard, gathered, (int64_t)rows * Vs, st)) return e;
+    launch_gather_vocab(gathered, logits, comm_size(m->comm), rows, Vs, st);
+  }
+  launch_argmax(logits, rows, c.vocab, next, nullptr, st);
+  return WS_OK;
 }
 
 int kv_geom(ws_model* m, ws_pool* pool, ws::KvGeom* g) {
@@ -249,6 +291,14 @@ int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* byt
   return WS_OK;
 }
 
+int ws_model_set_comm(ws_model* m, ws_comm* comm) {
+  if (!m) WS_FAIL(WS_ERR_INVALID, "null model");
+  if (comm && head_rows(m->cfg) * ws::comm_size(comm) != m->cfg.vocab)
+    WS_FAIL(WS_ERR_INVALID, "lm_head_rows x TP size must equal vocab");
+  m->comm = comm;
+  return WS_OK;
+}
+
 int ws_model_set_gemm(ws_model* m, int32_t impl) {
   if (!m || impl < 0 || impl > 3) WS_FAIL(WS_ERR_INVALID, "impl must be in 0..3");
   m->gemm_impl = impl;
@@ -276,6 +326,9 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
   bf16* gu = reinterpret_cast<bf16*>(wsb + w.gu);
   bf16* act = reinterpret_cast<bf16*>(wsb + w.act);
   bf16* hl = reinterpret_cast<bf16*>(wsb + w.hl);
+  float* partial = reinterpret_cast<float*>(wsb + w.partial);
+  float* shard = reinterpret_cast<float*>(wsb + w.shard_logits);
+  float* gathered = reinterpret_cast<float*>(wsb + w.gathered);
   const int d = c.hidden, q = qkv_dim(c), o = c.heads * c.head_dim;
   const float scale = 1.0f / std::sqrt((float)c.head_dim);
   const Layout& L = m->layout;
@@ -290,16 +343,15 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
              pos0, nullptr, nullptr, qkv, st);
     if ((m->gemm_impl & 2) || !launch_attn_prefill_tc(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st))
       launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
-    gemm(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, Epi::kAddF32, x, nullptr, st);
+    if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, x, partial, st)) return e;
     launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, rows, d, c.rms_eps, st);
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), rows, gu, act, st);
-    gemm(m, act, W<bf16>(wts, Ly.wdown), rows, d, c.ffn, Epi::kAddF32, x, nullptr, st);
+    if (int e = row_parallel(m, act, W<bf16>(wts, Ly.wdown), rows, d, c.ffn, x, partial, st)) return e;
   }
   if (streamer && c.layers >= first_streamed)
     if (int e = ws_streamer_wait(streamer, c.layers - first_streamed, stream)) return e;
   launch_rmsnorm(x + (int64_t)(rows - 1) * d, W<bf16>(wts, L.final_norm), hl, 1, d, c.rms_eps, st);
-  launch_gemv(hl, W<bf16>(wts, L.lm_head), 1, c.vocab, d, Epi::kStoreF32, logits, nullptr, st);
-  launch_argmax(logits, 1, c.vocab, next_token, nullptr, st);
+  if (int e = lm_head(m, hl, W<bf16>(wts, L.lm_head), 1, logits, shard, gathered, next_token, st)) return e;
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
@@ -325,6 +377,9 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   bf16* act = reinterpret_cast<bf16*>(wsb + w.act);
   bf16* hl = reinterpret_cast<bf16*>(wsb + w.hl);
   float* scratch = reinterpret_cast<float*>(wsb + w.scratch);
+  float* partial = reinterpret_cast<float*>(wsb + w.partial);
+  float* shard = reinterpret_cast<float*>(wsb + w.shard_logits);
+  float* gathered = reinterpret_cast<float*>(wsb + w.gathered);
   const int d = c.hidden, q = qkv_dim(c), o = c.heads * c.head_dim;
   const float scale = 1.0f / std::sqrt((float)c.head_dim);
   const Layout& L = m->layout;
@@ -336,14 +391,13 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
              pos, qkv, st);
     launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
-    gemm(m, attn, W<bf16>(wts, Ly.wo), n, d, o, Epi::kAddF32, x, nullptr, st);
+    if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x, partial, st)) return e;
     launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);
-    gemm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, Epi::kAddF32, x, nullptr, st);
+    if (int e = row_parallel(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial, st)) return e;
   }
   launch_rmsnorm(x, W<bf16>(wts, L.final_norm), hl, n, d, c.rms_eps, st);
-  gemm(m, hl, W<bf16>(wts, L.lm_head), n, c.vocab, d, Epi::kStoreF32, logits, nullptr, st);
-  launch_argmax(logits, n, c.vocab, next_tokens, nullptr, st);
+  if (int e = lm_head(m, hl, W<bf16>(wts, L.lm_head), n, logits, shard, gathered, next_tokens, st)) return e;
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }

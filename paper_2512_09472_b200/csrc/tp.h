@@ -1,0 +1,13 @@
+// Internal TP collective helpers (the C-ABI lives in include/warmserve.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/warmserve.h"
+
+namespace ws {
+int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st);
+int comm_allgather_f32(ws_comm* c, const float* send, float* recv, int64_t count, cudaStream_t st);
+int comm_rank(const ws_comm* c);
+int comm_size(const ws_comm* c);
+}  // namespace ws

@@ -22,7 +22,7 @@ class ModelConfigC(C.Structure):
         ("layers", C.c_int32), ("hidden", C.c_int32), ("ffn", C.c_int32), ("heads", C.c_int32),
         ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("vocab", C.c_int32),
         ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("qkv_bias", C.c_int32),
-        ("max_positions", C.c_int32),
+        ("max_positions", C.c_int32), ("lm_head_rows", C.c_int32),
     ]
 
 
@@ -39,6 +39,10 @@ N.register({
                         C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "ws_gemm": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                 C.c_void_p, C.c_int32, C.c_void_p],
+    "ws_nccl_unique_id": [C.POINTER(C.c_uint8), C.c_int32],
+    "ws_comm_create": [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)],
+    "ws_comm_destroy": [C.c_void_p],
+    "ws_model_set_comm": [C.c_void_p, C.c_void_p],
 })
 
 
@@ -56,10 +60,12 @@ class ModelConfig:
     rms_eps: float = 1e-5
     qkv_bias: bool = False
     max_positions: int = 8192
+    lm_head_rows: int = 0  # vocab-parallel lm_head shard (TP rank); 0 = full vocab
 
     def c(self) -> ModelConfigC:
         return ModelConfigC(self.layers, self.hidden, self.ffn, self.heads, self.kv_heads, self.head_dim,
-                            self.vocab, self.rope_theta, self.rms_eps, int(self.qkv_bias), self.max_positions)
+                            self.vocab, self.rope_theta, self.rms_eps, int(self.qkv_bias), self.max_positions,
+                            self.lm_head_rows)
 
     @property
     def qkv_dim(self) -> int:
@@ -114,7 +120,7 @@ class Layout:
             out.append((f"l{i}.wgu", L["wgu"], (2 * c.ffn, d)))
             out.append((f"l{i}.wdown", L["wdown"], (d, c.ffn)))
         out.append(("final_norm", self.final_norm, (d,)))
-        out.append(("lm_head", self.lm_head, (c.vocab, d)))
+        out.append(("lm_head", self.lm_head, (c.lm_head_rows or c.vocab, d)))
         return out
 
     def prefix_bytes(self, k: int) -> int:

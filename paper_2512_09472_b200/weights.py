@@ -17,25 +17,29 @@ def fill_flat(cfg: ModelConfig, out: torch.Tensor, seed: int = 0) -> torch.Tenso
     """Fill a flat bf16 tensor of layout.total/2 elements (any device)."""
     layout = cfg.layout()
     assert out.dtype == torch.bfloat16 and out.numel() * 2 >= layout.total
-    dev = out.device
-    gen = torch.Generator(device=dev)
-    chunk = 1 << 26
     for idx, (name, off, shape) in enumerate(layout.tensors()):
         n = 1
         for s in shape:
             n *= s
-        dst = out[off // 2: off // 2 + n]
-        gen.manual_seed(seed * 1_000_003 + idx)
-        is_norm = name.endswith("norm")
-        for i in range(0, n, chunk):
-            m = min(chunk, n - i)
-            v = torch.randn(m, generator=gen, device=dev, dtype=torch.float32)
-            if is_norm:
-                v.mul_(0.1).add_(1.0)
-            else:
-                v.mul_(0.02)
-            dst[i:i + m].copy_(v)
+        _fill_tensor(out[off // 2: off // 2 + n], name, idx, seed)
     return out
+
+
+def _fill_tensor(dst: torch.Tensor, name: str, idx: int, seed: int) -> None:
+    """Fill one flat bf16 tensor (index ``idx`` in layout order) from its own seed."""
+    gen = torch.Generator(device=dst.device)
+    gen.manual_seed(seed * 1_000_003 + idx)
+    is_norm = name.endswith("norm")
+    chunk = 1 << 26
+    n = dst.numel()
+    for i in range(0, n, chunk):
+        m = min(chunk, n - i)
+        v = torch.randn(m, generator=gen, device=dst.device, dtype=torch.float32)
+        if is_norm:
+            v.mul_(0.1).add_(1.0)
+        else:
+            v.mul_(0.02)
+        dst[i:i + m].copy_(v)
 
 
 def synth_flat(cfg: ModelConfig, seed: int = 0, device: str | torch.device = "cuda") -> torch.Tensor:

@@ -82,9 +82,17 @@ class UniversalWorker:
         self.open_seqs: set[int] = set()
 
     # ------------------------------------------------------------ models
-    def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32) -> ModelEntry:
+    def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32,
+                 tp=None) -> ModelEntry:
+        """Register a model (or, with ``tp`` = a ``tp.TpGroup``, this rank's
+        shard: ``cfg`` is then ``tp.shard_config(full, size)`` and the forward
+        all-reduces on the TP boundary over NCCL). The per-GPU ledger holds the
+        rank's shard as its slot; the cluster-level TP group (one instance over
+        ``parallelism`` GPUs of one server) is the reference Cluster's job."""
         h = C.c_void_p()
         N.call("ws_model_create", C.byref(cfg.c()), self.device, C.byref(h))
+        if tp is not None:
+            N.call("ws_model_set_comm", h, tp.handle)
         spec = model_spec(cfg, max_batch=max_batch)
         e = ModelEntry(cfg, spec, cfg.layout(), host_weights, h)
         self.models[cfg.name] = e

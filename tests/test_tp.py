@@ -1,0 +1,124 @@
+"""Tensor parallelism (config 4): shard math on CPU with a world_size-2 gloo
+group, shard sizing against the reference's partition rule, and (GPU) the
+native NCCL TP path at TP=1 against the single-GPU path."""
+
+import os
+import socket
+
+import pytest
+import torch
+
+from oracle import llama_fp32 as O
+from paper_2512_09472_b200 import models as M
+from paper_2512_09472_b200 import tp as TP
+from paper_2512_09472_b200.weights import synth_flat
+
+TINY_TP = M.TINY.with_(name="tiny-tp", heads=4, kv_heads=2, ffn=1024)  # ffn/2 = 512 = 4 x 128
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_70b_shards_match_reference_partition(tp):
+    """A rank's physical shard equals the reference's partition_bytes for a
+    spec with weight_bytes = TP x shard (cluster.py:79-80), and the shards of
+    the sharded tensors tile the full model."""
+    from paper_2512_09472_b200.cluster import ModelSpec
+
+    cfg = M.LLAMA3_70B
+    s = TP.shard_config(cfg, tp)
+    assert (s.heads, s.kv_heads, s.ffn, s.lm_head_rows) == (64 // tp, 8 // tp, 28672 // tp, 128256 // tp)
+    shard = s.layout().total
+    spec = ModelSpec(cfg.name, tp * shard, tp, layers=cfg.layers)
+    assert spec.partition_bytes == shard
+    d, V, L = cfg.hidden, cfg.vocab, cfg.layers
+    replicated = V * d * 2 + (2 * L + 1) * d * 2  # embedding + norms on every rank
+    per_layer = (cfg.qkv_dim * d + d * cfg.heads * cfg.head_dim + 3 * cfg.ffn * d) * 2
+    assert shard == replicated + (L * per_layer + V * d * 2) // tp  # sharded layers + lm_head
+
+
+def test_shard_flat_equals_synth_shard():
+    full = synth_flat(TINY_TP, seed=4, device="cpu")
+    for r in range(2):
+        a = TP.shard_flat(TINY_TP, full, 2, r)
+        b = TP.synth_shard(TINY_TP, 2, r, seed=4, device="cpu")
+        assert torch.equal(a, b)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _tp_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = TINY_TP
+        full = synth_flat(cfg, seed=9, device="cpu")
+        scfg = TP.shard_config(cfg, world)
+        w = O.unpack(scfg, scfg.layout(), TP.shard_flat(cfg, full, world, rank))
+        toks = torch.randint(0, cfg.vocab, (48,), generator=torch.Generator().manual_seed(3))
+
+        def allreduce(t):
+            dist.all_reduce(t)
+
+        def allgather(t):
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t.contiguous())
+            return torch.cat(parts, -1)
+
+        got = O.forward_tp(scfg, w, toks, allreduce, allgather)
+        if rank == 0:
+            ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), full), toks)
+            q.put(((got - ref).abs().max() / ref.abs().max()).item())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp2_gloo_shards_reproduce_full_model():
+    """world_size-2 gloo group: each rank runs its Megatron shard, allreduce
+    after O/down, allgather of the vocab-parallel lm_head == full model."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    err = q.get(timeout=10)
+    assert err < 1e-4, err
+
+
+@pytest.mark.gpu
+def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
+    """The NCCL TP path (fp32 partials + allreduce + residual add, lm_head
+    allgather + reorder) on a 1-rank communicator == the fused single-GPU path."""
+    from paper_2512_09472_b200.weights import pinned_host_copy
+    from paper_2512_09472_b200.worker import UniversalWorker
+
+    cfg = TINY_TP
+    host = pinned_host_copy(synth_flat(cfg, seed=2, device="cuda"))
+    prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(1), dtype=torch.int32)
+    outs = []
+    for use_tp in (False, True):
+        w = UniversalWorker(cuda_device, pool_pages=64, max_tokens=512)
+        grp = TP.TpGroup(0, 1, cuda_device, TP.TpGroup.unique_id()) if use_tp else None
+        w.register(cfg, host, tp=grp)
+        w.prewarm(cfg.name, layers=cfg.layers)
+        r = w.activate_instance(cfg.name, prompt.pin_memory())
+        outs.append((r.token, w.logits[: cfg.vocab].clone()))
+        w.release()
+        w.close()
+        if grp:
+            grp.close()
+    assert outs[0][0] == outs[1][0]
+    rel = ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item()
+    assert rel < 1e-3, rel
