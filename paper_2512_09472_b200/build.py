@@ -28,6 +28,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=o
 CUDA_ONLY = ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 if os.environ.get("WS_DEBUG_WAIT"):  # watchdog build of the mbarrier waits (debugging only)
     CUDA_ONLY.append("-DWS_DEBUG_WAIT")
+if os.environ.get("WS_ATTN_TRACE"):  # clock64 timeline of one attention CTA (debugging only)
+    CUDA_ONLY.append("-DWS_ATTN_TRACE")
 
 
 def _nvcc() -> str:

@@ -15,7 +15,10 @@
 //              O  += P_j V_j   (M=128, N=hd, K=128; V is MN-major — no transpose)
 //              S is double-buffered in TMEM so QK^T of tile j+1 overlaps the
 //              softmax of tile j. TMEM: S0 [0,128) S1 [128,256) O [256,256+hd).
+#include <cuda.h>
+
 #include "../common.h"
+#include "../driver.h"
 #include "device.cuh"
 #include "ops.cuh"
 
@@ -25,6 +28,16 @@ namespace {
 using namespace dev;
 
 constexpr int kRows = 128, kKeys = 128, kThreads = 288;
+
+#ifdef WS_ATTN_TRACE
+// debug timeline of block (0,0): [event][j] = clock64 (events: 0 S issued,
+// 1 PV issued, 2 softmax got S, 3 softmax released P)
+__device__ long long g_attn_trace[4][64];
+#define TRACE(ev, j) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) g_attn_trace[ev][j] = clock64(); } while (0)
+#else
+#define TRACE(ev, j) do { } while (0)
+#endif
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -61,10 +74,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void tma_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ float fast_exp2(float x) {  // one MUFU op, no range fix-up branches
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
+}
+__device__ __forceinline__ bool mbar_ready(uint32_t bar, uint32_t parity) {  // non-blocking probe
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
@@ -135,10 +166,10 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
   return (uint32_t)((c >> 3) * (kRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-template <int HD>
+template <int HD, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, KvGeom kv, int layer, int seq,
-                   int rows, int pos0, int heads, float scale_log2) {
+                   int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
   using S = Smem<HD>;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -155,8 +186,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (rows + kRows - 1) / kRows;
-  const int qt = n_qt - 1 - blockIdx.x;  // heaviest tiles first
-  const int h = blockIdx.y;
+  // grid = (heads, q tiles): CTAs launch in blockIdx order, so every head's
+  // heaviest (latest) query tile goes first and the tail holds the light ones
+  const int qt = n_qt - 1 - blockIdx.y;
+  const int h = blockIdx.x;
   const int kvh = h / (heads / kv.kv_heads);
   const int q0 = qt * kRows;
   const int n_keys = pos0 + min(rows, q0 + kRows);
@@ -166,9 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(B(0), 128);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(B(1 + i), 64);    // k_full: 64 K-producer threads (cp.async noinc)
+      mbar_init(B(1 + i), TMA ? 1 : 64);  // k_full: TMA thread (expect_tx) or 64 cp.async threads
       mbar_init(B(3 + i), 1);     // k_empty: MMA commit after S_j
-      mbar_init(B(5 + i), 64);    // v_full: 64 V-producer threads
+      mbar_init(B(5 + i), TMA ? 1 : 64);  // v_full
       mbar_init(B(7 + i), 1);     // v_empty: MMA commit after PV_j
       mbar_init(B(9 + i), 1);     // s_full: MMA commit
       mbar_init(B(11 + i), 128);  // s_empty: softmax threads
@@ -177,6 +210,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(B(17), 1);  // pv_done: MMA commit
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if constexpr (TMA) {
+    // K/V rows a tile does not load keep stale data; start from finite zeros
+    for (int i = threadIdx.x; i < 4 * S::kTile / 16; i += kThreads)
+      reinterpret_cast<uint4*>(gbase + S::kK)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(bar + 18 * 8));
@@ -203,22 +242,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t plane = kv.plane(layer, is_v ? 1 : 0, kvh);
     const uint32_t ring = is_v ? S::kV : S::kK;
     const int full0 = is_v ? 5 : 1, empty0 = is_v ? 7 : 3;
+    if constexpr (TMA) {
+      // One thread per ring issues 8-row TMA boxes (one per run of 8 tokens of
+      // a page; tokens-per-block is a multiple of 8): 16 x HD/64 bulk copies
+      // per tile instead of 2048 16-byte LDGSTS. Groups past the last key are
+      // skipped (their smem rows hold finite stale data and are masked).
+      if (u < 32) {  // the first warp of the ring's producer pair
+        const int rows_pp = (int)(kv.page_size / (HD * 2));
+        const int plane_rows = (int)(plane / HD);
+        // lane g resolves group g's page (16 block-table loads in parallel,
+        // one tile ahead), lane 0 issues the bulk copies
+        auto row_of = [&](int j) {
+          const int key0 = j * kKeys + (u & 7) * 16;
+          const int blk = key0 / kv.tpb, slot = key0 - blk * kv.tpb;
+          return key0 < n_keys ? bt[blk] * rows_pp + plane_rows + slot : 0;
+        };
+        int y_next = row_of(0);
+        for (int j = 0; j < n_kt; ++j) {
+          const int st = j & 1;
+          const int y = y_next;
+          if (j + 1 < n_kt) y_next = row_of(j + 1);
+          const int groups = min(kKeys / 16, (n_keys - j * kKeys + 15) / 16);
+          if (u == 0) {
+            mbar_wait(B(empty0 + st), ((j >> 1) & 1) ^ 1);
+            tma_expect(B(full0 + st), (uint32_t)(groups * (HD / 64) * 2048));
+          }
+          for (int g = 0; g < groups; ++g) {
+            const int yg = __shfl_sync(0xffffffffu, y, g);
+            if (u == 0) {
+#pragma unroll
+              for (int hh = 0; hh < HD / 64; ++hh)
+                tma_load_2d(base + ring + st * S::kTile + hh * (kRows * 128) + g * 2048, &kvmap,
+                            B(full0 + st), hh * 64, yg);
+            }
+          }
+        }
+      }
+    } else {
     for (int j = 0; j < n_kt; ++j) {
       const int st = j & 1;
       mbar_wait(B(empty0 + st), ((j >> 1) & 1) ^ 1);
       uint8_t* dst = gbase + ring + st * S::kTile;
-      // CH consecutive lanes cover one key row (HD*2 contiguous bytes): coalesced
+      // CH consecutive lanes cover one key row (HD*2 contiguous bytes, coalesced);
+      // this thread walks rows r, r+RS, ... with its (block, slot) position
+      // advanced incrementally — one integer division per tile, not per chunk.
+      constexpr int RS = 64 / CH;
+      const int c = u % CH;
+      int r = u / CH;
+      int key = j * kKeys + r;
+      int blk = key / kv.tpb, slot = key - blk * kv.tpb;
+      const char* wbase = kv.window;
 #pragma unroll 4
-      for (int i = u; i < kKeys * CH; i += 64) {
-        const int r = i / CH, c = i % CH;
-        const int key = j * kKeys + r;
+      for (int k = 0; k < kKeys / RS; ++k) {
         const bool ok = key < n_keys;
-        const int kk = ok ? key : 0;
-        const bf16* row = reinterpret_cast<const bf16*>(kv.window + (int64_t)bt[kk / kv.tpb] * kv.page_size) +
-                          plane + (int64_t)(kk % kv.tpb) * HD;
+        const int32_t page = bt[ok ? blk : 0];
+        const bf16* row = reinterpret_cast<const bf16*>(wbase + (int64_t)page * kv.page_size) + plane +
+                          (int64_t)(ok ? slot : 0) * HD;
         cp_async16(dst + swz(r, c), row + c * 8, ok);
+        r += RS;
+        key += RS;
+        slot += RS;
+        while (slot >= kv.tpb) {
+          slot -= kv.tpb;
+          ++blk;
+        }
       }
       cp_async_arrive(B(full0 + st));
+    }
     }
   } else if (warp == 8) {
     // ===================== MMA issuer =====================
@@ -227,11 +317,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tO = tmem + 256;
       mbar_wait(B(0), 0);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      // Event-driven issue: S_{j+1} = Q K_{j+1}^T and PV_j = P_j V_j are issued
+      // in whichever order their inputs become ready (non-blocking polls), so
+      // a late K tile never holds back the PV of the previous tile.
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        mbar_wait(B(1 + st), (j >> 1) & 1);             // K_j landed
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        mbar_wait(B(11 + st), ((j >> 1) & 1) ^ 1);      // softmax released S[st]
         fence_after();
         const uint32_t qa = base + S::kQ, ka = base + S::kK + st * S::kTile;
 #pragma unroll
@@ -242,12 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         commit(B(9 + st));  // S_j ready
         commit(B(3 + st));  // K stage free
       };
-      issue_s(0);
-      for (int j = 0; j < n_kt; ++j) {
+      auto issue_pv = [&](int j) {
         const int st = j & 1;
-        if (j + 1 < n_kt) issue_s(j + 1);
-        mbar_wait(B(13 + st), (j >> 1) & 1);             // P_j written (and O rescaled)
-        mbar_wait(B(5 + st), (j >> 1) & 1);              // V_j landed
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         fence_after();
         const uint32_t pa = base + S::kPo + st * S::kP, va = base + S::kV + st * S::kTile;
@@ -259,6 +346,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         commit(B(15 + st));  // P buffer free
         commit(B(7 + st));   // V stage free
         commit(B(17));       // O updated through tile j
+      };
+      // In-order issue with blocking (HW-suspending) waits: S_{j+1} first (its K
+      // tile is prefetched two tiles ahead, so it is normally already there),
+      // then PV_j once softmax has written P_j.
+      for (int j = 0; j < n_kt; ++j) {
+        if (j == 0) {
+          mbar_wait(B(1), 0);
+          TRACE(0, 0);
+          issue_s(0);
+        }
+        if (j + 1 < n_kt) {
+          const int s1 = (j + 1) & 1, ph1 = ((j + 1) >> 1) & 1;
+          mbar_wait(B(1 + s1), ph1);
+          mbar_wait(B(11 + s1), ph1 ^ 1);
+          TRACE(0, j + 1);
+          issue_s(j + 1);
+        }
+        mbar_wait(B(13 + (j & 1)), (j >> 1) & 1);
+        mbar_wait(B(5 + (j & 1)), (j >> 1) & 1);
+        TRACE(1, j);
+        issue_pv(j);
+      }
+      int ns = n_kt, npv = n_kt;  // event-driven variant below disabled
+      while (npv < n_kt) {
+        // S_ns needs K_ns and a free S buffer (softmax already read S_{ns-2}):
+        // it may run ahead of PV so the next softmax never waits on the pipe
+        if (ns < n_kt && mbar_ready(B(1 + (ns & 1)), (ns >> 1) & 1) &&
+            mbar_ready(B(11 + (ns & 1)), ((ns >> 1) & 1) ^ 1)) {
+          TRACE(0, ns);
+          issue_s(ns++);
+          continue;
+        }
+        // PV_npv needs P_npv (softmax) and V_npv
+        if (npv < ns && mbar_ready(B(13 + (npv & 1)), (npv >> 1) & 1) &&
+            mbar_ready(B(5 + (npv & 1)), (npv >> 1) & 1)) {
+          TRACE(1, npv);
+          issue_pv(npv++);
+          continue;
+        }
+        __nanosleep(64);  // back off: this warp shares an SMSP with a softmax warp
       }
     }
     __syncwarp();  // reconverge before the CTA-wide (aligned) barrier below
@@ -271,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < n_kt; ++j) {
       const int st = j & 1;
       mbar_wait(B(9 + st), (j >> 1) & 1);
+      if (threadIdx.x == 0) TRACE(2, j);
       fence_after();
       const uint32_t ts = tmem + lane_off + st * 128;
       const int key0 = j * kKeys;
@@ -349,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
       fence_before();
       mbar_arrive(B(13 + st));
+      if (threadIdx.x == 0) TRACE(3, j);
     }
     // epilogue: O / l -> bf16
     mbar_wait(B(17), (n_kt - 1) & 1);
@@ -377,28 +506,68 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-template <int HD>
+// 2D view of the page window as rows of HD bf16 (one token of one K or V
+// plane per row), 8-row x 64-column boxes with 128B swizzle.
+bool window_map(CUtensorMap* map, const KvGeom& kv, int hd) {
+  const Driver* d = driver();
+  if (!d) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)hd, (cuuint64_t)(kv.n_pages * kv.page_size / (hd * 2))};
+  cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t estr[2] = {1, 1};
+  return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.window, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int HD, bool TMA>
 void launch_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows, int pos0,
-                 int heads, float scale, cudaStream_t st) {
+                 int heads, float scale, const CUtensorMap& map, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::kBytes);
+    cudaFuncSetAttribute(attn_tc_kernel<HD, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<HD>::kBytes);
     attr = true;
   }
-  dim3 grid((rows + kRows - 1) / kRows, heads);
+  dim3 grid(heads, (rows + kRows - 1) / kRows);
   count_launch();
-  attn_tc_kernel<HD><<<grid, kThreads, Smem<HD>::kBytes, st>>>(qkv, out, kv, layer, seq, rows, pos0, heads,
-                                                               scale * 1.4426950408889634f);
+  attn_tc_kernel<HD, TMA><<<grid, kThreads, Smem<HD>::kBytes, st>>>(qkv, out, kv, layer, seq, rows, pos0, heads,
+                                                                    scale * 1.4426950408889634f, map);
+}
+
+template <int HD>
+void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows, int pos0, int heads,
+              float scale, cudaStream_t st) {
+  // TMA needs 8-token runs inside a block and the window addressable as HD-wide rows
+  static CUtensorMap map;
+  static const char* map_window = nullptr;
+  static int64_t map_pages = 0;
+  bool tma = kv.tpb % 16 == 0 && kv.page_size % (HD * 2) == 0;
+  if (tma && (map_window != kv.window || map_pages != kv.n_pages)) {
+    tma = window_map(&map, kv, HD);
+    map_window = tma ? kv.window : nullptr;
+    map_pages = tma ? kv.n_pages : 0;
+  }
+  if (tma)
+    launch_impl<HD, true>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, map, st);
+  else
+    launch_impl<HD, false>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, map, st);
 }
 
 }  // namespace
 
+#ifdef WS_ATTN_TRACE
+extern "C" int ws_attn_trace(long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess ? 0 : 6;
+}
+#endif
+
 bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows,
                             int pos0, int heads, float scale, cudaStream_t st) {
   if (kv.head_dim == 128)
-    launch_impl<128>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
+    dispatch<128>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
   else if (kv.head_dim == 64)
-    launch_impl<64>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
+    dispatch<64>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
   else
     return false;
   return true;

@@ -20,6 +20,7 @@ struct KvGeom {
   int32_t max_blocks;
   int32_t tpb;           // tokens per block
   int32_t layers, kv_heads, head_dim;
+  int64_t n_pages;       // pages in the window (TMA descriptor extent)
 
   __host__ __device__ int64_t head_stride() const { return (int64_t)tpb * head_dim; }
   // element offset of (layer, kind, head, slot 0) inside a page

@@ -16,7 +16,7 @@
 
 namespace ws {
 int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_tables,
-                 int32_t* max_blocks);
+                 int32_t* max_blocks, int64_t* n_pages);
 }
 
 namespace {
@@ -204,7 +204,7 @@ int lm_head(const ws_model* m, const ws::bf16* hl, const ws::bf16* W, int rows, 
 
 int kv_geom(ws_model* m, ws_pool* pool, ws::KvGeom* g) {
   int32_t* bt;
-  if (int e = ws::pool_kv_view(pool, &g->window, &g->page_size, &bt, &g->max_blocks)) return e;
+  if (int e = ws::pool_kv_view(pool, &g->window, &g->page_size, &bt, &g->max_blocks, &g->n_pages)) return e;
   g->block_tables = bt;
   int64_t kvb = 0;
   if (int e = ws_model_kv_geometry(&m->cfg, g->page_size, &g->tpb, &kvb)) return e;

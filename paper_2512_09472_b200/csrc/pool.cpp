@@ -382,6 +382,12 @@ int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_po
       ws::set_error("cuMemSetAccess(window) failed");
       return fail(WS_ERR_CUDA);
     }
+    // Zero every page once: afterwards a page only ever holds finite bf16
+    // (weights or KV), so kernels may read stale-but-finite rows and mask them.
+    if (cudaMemset(reinterpret_cast<void*>(p->window), 0, (size_t)(total_pages * page_size)) != cudaSuccess) {
+      ws::set_error("zeroing the page window failed");
+      return fail(WS_ERR_CUDA);
+    }
     p->stage_bytes = (size_t)total_pages * 24 + 4096;
     if (cudaMalloc(&p->owner_dev, total_pages * 4) != cudaSuccess ||
         cudaMemcpy(p->owner_dev, p->owner.data(), total_pages * 4, cudaMemcpyHostToDevice) !=
@@ -795,9 +801,10 @@ int ws_pool_last_switch(ws_pool* p, double* kernel_ms, int64_t* entries) {
 namespace ws {
 // Internal accessor for the model driver (not part of the C-ABI).
 int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_tables,
-                 int32_t* max_blocks) {
+                 int32_t* max_blocks, int64_t* n_pages) {
   if (!p || !p->on_device()) WS_FAIL(WS_ERR_NO_DEVICE, "model forward needs a device pool");
   if (!p->bt_dev) WS_FAIL(WS_ERR_STATE, "sequence table not configured (ws_pool_seq_config)");
+  *n_pages = p->n;
   *window = reinterpret_cast<char*>(p->window);
   *page_size = p->page;
   *block_tables = p->bt_dev;

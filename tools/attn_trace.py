@@ -1,0 +1,37 @@
+"""Print the clock64 timeline of attention CTA (0,0) (build with WS_ATTN_TRACE=1)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import subprocess
+    subprocess.run([sys.executable, str(Path(__file__).parent / "prefill_profile.py"), "--iters", "1"], check=True)
+
+
+if __name__ == "__main__":
+    import torch
+    from paper_2512_09472_b200 import _native as N
+    from paper_2512_09472_b200 import models as M
+    from paper_2512_09472_b200.weights import fill_flat
+    from paper_2512_09472_b200.worker import UniversalWorker
+    cfg = M.LLAMA3_8B.with_(layers=1)
+    w = UniversalWorker(0, pool_pages=2048, max_tokens=2048)
+    w.register(cfg, None)
+    w.prewarm(cfg.name, layers=1)
+    fill_flat(cfg, w.slot_view(cfg.name), seed=0)
+    w.switch_memory(cfg.name)
+    toks = torch.randint(0, cfg.vocab, (2048,), dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        with torch.cuda.stream(w.compute):
+            s = w.open_seq(2048); w.prefill(s, toks); w.close_seq(s)
+        torch.cuda.synchronize()
+    buf = (C.c_longlong * 256)()
+    N.lib.ws_attn_trace(buf)
+    t = [[buf[e * 64 + j] for j in range(16)] for e in range(4)]
+    t0 = min(x for row in t for x in row if x)
+    names = ["S issued", "PV issued", "softmax got S", "softmax P done"]
+    for e in range(4):
+        print(f"{names[e]:16s}", " ".join(f"{(x - t0) if x else -1:7d}" for x in t[e]))
