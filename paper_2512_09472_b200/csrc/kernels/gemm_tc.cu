@@ -362,6 +362,177 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair version (tcgen05.mma.cta_group::2): a 2-CTA cluster computes a
+// 256x256 tile; each CTA stages its 128 rows of A and 128 of the 256 B rows
+// (half the smem operand traffic per SM of the 1-CTA 128x256 tile), the leader
+// CTA issues M=256 MMAs reading both CTAs' smem, and each CTA's TMEM holds its
+// 128 rows x 256 columns, drained by its own epilogue warps (same epilogues).
+constexpr int P_BM = 128, P_BN = 256, P_BNH = 128, P_STAGES = 6;
+constexpr int P_A_BYTES = P_BM * BK * 2, P_B_BYTES = P_BNH * BK * 2;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+                    int N, int K, const __grid_constant__ TcEpilogue ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023) & ~1023u;
+  const uint32_t bars = base + P_STAGES * P_STAGE_BYTES;
+  auto full = [&](int s) { return bars + 8 * s; };
+  auto empty = [&](int s) { return bars + 8 * (P_STAGES + s); };
+  auto tfull = [&](int b) { return bars + 8 * (2 * P_STAGES + b); };
+  auto tempty = [&](int b) { return bars + 8 * (2 * P_STAGES + 2 + b); };
+  const uint32_t tmem_slot = bars + 8 * (2 * P_STAGES + 4);
+  uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - raw));
+  const uint32_t peer_mask = 0xFEFFFFFFu;  // same offset in the leader (rank 0) CTA
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int m_blocks = (M + 255) / 256, n_blocks = N / P_BN, k_blocks = K / BK;
+  const int tiles = m_blocks * n_blocks;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 256);  // both CTAs' epilogue threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += n_pairs) {
+        const int m0 = (t % m_blocks) * 256 + rank * P_BM, n0 = (t / m_blocks) * P_BN + rank * P_BNH;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1);
+          const uint32_t sa = base + stage * P_STAGE_BYTES;
+          if (rank == 0) mbar_expect_tx(full(stage), 2 * P_STAGE_BYTES);  // both CTAs' bytes
+          const uint32_t bar = full(stage) & peer_mask;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+              "[%1, {%3, %4}], [%2];\n" ::"r"(sa),
+              "l"(&map_a), "r"(bar), "r"(kb * BK), "r"(m0)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+              "[%1, {%3, %4}], [%2];\n" ::"r"(sa + P_A_BYTES),
+              "l"(&map_b), "r"(bar), "r"(kb * BK), "r"(n0)
+              : "memory");
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < tiles; t += n_pairs) {
+        mbar_wait(tempty(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * P_BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(full(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * P_STAGE_BYTES;
+          const uint64_t da = smem_desc(sa), db = smem_desc(sa + P_A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2), "r"((uint32_t)((kb | k) != 0)));
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                  empty(stage)),
+              "h"((uint16_t)3)
+              : "memory");
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                tfull(acc)),
+            "h"((uint16_t)3)
+            : "memory");
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < tiles; t += n_pairs) {
+      const int m0 = (t % m_blocks) * 256 + rank * P_BM, n0 = (t / m_blocks) * P_BN;
+      mbar_wait(tfull(acc), acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      epilogue_tile<MODE>(ep, tmem + ((uint32_t)(q * 32) << 16) + acc * P_BN, row < M ? row : -1, n0, N,
+                          ep.kv.head_dim);
+      tc_fence_before();
+      // release this accumulator to the leader's MMA thread (remote arrive)
+      asm volatile(
+          "{\n.reg .b32 remAddr32;\nmapa.shared::cluster.u32 remAddr32, %0, 0;\n"
+          "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [remAddr32];\n}\n" ::"r"(tempty(acc))
+          : "memory");
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
 bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
   const Driver* d = driver();
   if (!d) return false;
@@ -398,10 +569,46 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
   gemm_tc_kernel<MODE><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, M, N, K, e);
 }
 
+template <int MODE>
+void launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
+                  cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc2_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+    attr = true;
+  }
+  const int tiles = ((M + 255) / 256) * (N / P_BN);
+  const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+  count_launch();
+  gemm_tc2_kernel<MODE><<<grid, THREADS, P_SMEM_BYTES, st>>>(ma, mb, M, N, K, e);
+}
+
+int g_pair_mode = -1;  // -1: unset (env WS_GEMM_PAIR, default on), 0 off, 1 on
+
+bool use_pair(int M) {
+  if (g_pair_mode < 0) {
+    const char* v = getenv("WS_GEMM_PAIR");
+    g_pair_mode = (v && v[0] == '0') ? 0 : 1;
+  }
+  return g_pair_mode == 1 && M >= 256;
+}
+
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
                         cudaStream_t st) {
   if (!gemm_tc_supported(M, N, K) || !gemm_tc_epilogue_supported(e, N, e.kv.head_dim)) return false;
   CUtensorMap ma, mb;
+  if (use_pair(M)) {
+    if (!make_map(&ma, A, M, K, P_BM) || !make_map(&mb, B, N, K, P_BNH)) return false;
+    switch (e.mode) {
+      case Epi::kStoreBf16: launch_mode2<0>(ma, mb, M, N, K, e, st); break;
+      case Epi::kBiasBf16: launch_mode2<1>(ma, mb, M, N, K, e, st); break;
+      case Epi::kAddF32: launch_mode2<2>(ma, mb, M, N, K, e, st); break;
+      case Epi::kStoreF32: launch_mode2<3>(ma, mb, M, N, K, e, st); break;
+      case Epi::kSwiGLU: launch_mode2<4>(ma, mb, M, N, K, e, st); break;
+      case Epi::kRopeKV: launch_mode2<5>(ma, mb, M, N, K, e, st); break;
+    }
+    return true;
+  }
   if (!make_map(&ma, A, M, K, BM) || !make_map(&mb, B, N, K, BN)) return false;
   switch (e.mode) {
     case Epi::kStoreBf16: launch_mode<0>(ma, mb, M, N, K, e, st); break;
