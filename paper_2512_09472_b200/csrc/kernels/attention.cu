@@ -9,6 +9,7 @@
 #include "../common.h"
 #include "device.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace ws {
 namespace {
@@ -31,6 +32,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_prefill_kernel(const bf16* _
                                                                    int layer, int seq, int rows,
                                                                    int pos0, int heads,
                                                                    float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   using S = PrefillSmem<HD>;
   constexpr int ST = S::kStride;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
@@ -211,6 +214,8 @@ __global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
     int n_splits) {
+  pdl_trigger();
+  pdl_wait();
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int G = heads / kv.kv_heads;
   const int len = pos[b] + 1;  // the new token's K/V is already appended
@@ -321,6 +326,8 @@ template <int HD>
 __global__ void __launch_bounds__(HD) attn_combine_kernel(const float* __restrict__ part,
                                                           bf16* __restrict__ out, int heads,
                                                           int n_splits) {
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
   const float* p = part + ((int64_t)b * heads + h) * n_splits * (HD + 2);
   float mx = -INFINITY;
@@ -347,7 +354,7 @@ void prefill_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int s
   }
   dim3 grid((rows + kQTile - 1) / kQTile, heads);
   count_launch();
-  attn_prefill_kernel<HD><<<grid, kWarps * 32, smem, st>>>(qkv, out, kv, layer, seq, rows, pos0,
+  launch_pdl(attn_prefill_kernel<HD>, dim3(grid), dim3(kWarps * 32), smem, st, qkv, out, kv, layer, seq, rows, pos0,
                                                            heads, scale * 1.4426950408889634f);
 }
 
@@ -358,9 +365,9 @@ void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const 
   const int n_splits = (max_ctx + kSplit - 1) / kSplit;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
   count_launch(2);
-  attn_decode_kernel<HD><<<grid, kDecThreads, 0, st>>>(qkv, kv, layer, seqs, ctx, heads,
+  launch_pdl(attn_decode_kernel<HD>, dim3(grid), dim3(kDecThreads), 0, st, qkv, kv, layer, seqs, ctx, heads,
                                                        scale * 1.4426950408889634f, scratch, n_splits);
-  attn_combine_kernel<HD><<<dim3(heads, n_seqs), HD, 0, st>>>(scratch, out, heads, n_splits);
+  launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
 }
 
 }  // namespace

@@ -21,6 +21,7 @@
 #include "../driver.h"
 #include "device.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace ws {
 namespace {
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
   using S = Smem<HD>;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // everything above is prologue; global data from here on
 
   if (warp >= 4 && warp < 8) {
     // ===================== producers: warps 4-5 gather K, warps 6-7 gather V =====================
@@ -530,7 +533,7 @@ void launch_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int se
   }
   dim3 grid(heads, (rows + kRows - 1) / kRows);
   count_launch();
-  attn_tc_kernel<HD, TMA><<<grid, kThreads, Smem<HD>::kBytes, st>>>(qkv, out, kv, layer, seq, rows, pos0, heads,
+  launch_pdl(attn_tc_kernel<HD, TMA>, dim3(grid), dim3(kThreads), Smem<HD>::kBytes, st, qkv, out, kv, layer, seq, rows, pos0, heads,
                                                                     scale * 1.4426950408889634f, map);
 }
 

@@ -4,6 +4,7 @@
 #include "../common.h"
 #include "device.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace ws {
 namespace {
@@ -14,6 +15,8 @@ using namespace dev;
 __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ tok,
                                                     const bf16* __restrict__ table,
                                                     float* __restrict__ x, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int64_t t = tok[r];
   const uint4* src = reinterpret_cast<const uint4*>(table + t * d);
@@ -32,6 +35,8 @@ template <int kThreads>
 __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const float* __restrict__ x,
                                                           const bf16* __restrict__ w,
                                                           bf16* __restrict__ out, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)r * d);
   float ss = 0.f;
@@ -69,6 +74,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const float* __restri
 // tcgen05 GEMM applies SwiGLU in its epilogue instead.
 __global__ void __launch_bounds__(256) silu_mul_kernel(const bf16* __restrict__ gu,
                                                        bf16* __restrict__ act, int ffn) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 8-element group
   if (i >= ffn / 8) return;
@@ -98,6 +105,8 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(bf16* __restrict__ qkv,
                                                       const int32_t* __restrict__ seq_arr,
                                                       const int32_t* __restrict__ pos_arr, int seq0,
                                                       int pos0) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int slots = heads + 2 * kv.kv_heads;
@@ -137,6 +146,8 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(bf16* __restrict__ qkv,
 // Row-wise argmax over fp32 logits (first index on ties, like torch.argmax).
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V,
                                                       int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float* row = logits + (int64_t)r * V;
   float best = -INFINITY;
@@ -183,6 +194,8 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
 
 __global__ void __launch_bounds__(256) add_f32_kernel(float4* __restrict__ x, const float4* __restrict__ p,
                                                       int64_t n4) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = x[i];
     const float4 b = p[i];
@@ -196,6 +209,8 @@ __global__ void __launch_bounds__(256) add_f32_kernel(float4* __restrict__ x, co
 
 __global__ void __launch_bounds__(256) gather_vocab_kernel(const float* __restrict__ g, float* __restrict__ out,
                                                            int tp, int rows, int vs) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y, shard = blockIdx.z;
   const float* src = g + ((int64_t)shard * rows + r) * vs;
   float* dst = out + (int64_t)r * tp * vs + (int64_t)shard * vs;
@@ -209,33 +224,33 @@ void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st) {
   const int64_t n4 = count / 4;  // hidden sizes are multiples of 32
   int blocks = (int)((n4 + 255) / 256);
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-  add_f32_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(x), reinterpret_cast<const float4*>(p), n4);
+  launch_pdl(add_f32_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<float4*>(x), reinterpret_cast<const float4*>(p), n4);
 }
 
 void launch_gather_vocab(const float* g, float* out, int tp, int rows, int vs, cudaStream_t st) {
   count_launch();
   dim3 grid((vs + 1023) / 1024, rows, tp);
-  gather_vocab_kernel<<<grid, 256, 0, st>>>(g, out, tp, rows, vs);
+  launch_pdl(gather_vocab_kernel, dim3(grid), dim3(256), 0, st, g, out, tp, rows, vs);
 }
 
 void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n, int d, cudaStream_t st) {
   count_launch();
-  embed_kernel<<<n, 256, 0, st>>>(tokens, table, x, d);
+  launch_pdl(embed_kernel, dim3(n), dim3(256), 0, st, tokens, table, x, d);
 }
 
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, float eps,
                     cudaStream_t st) {
   count_launch();
   if (d >= 2048)
-    rmsnorm_kernel<512><<<rows, 512, 0, st>>>(x, w, out, d, eps);
+    launch_pdl(rmsnorm_kernel<512>, dim3(rows), dim3(512), 0, st, x, w, out, d, eps);
   else
-    rmsnorm_kernel<128><<<rows, 128, 0, st>>>(x, w, out, d, eps);
+    launch_pdl(rmsnorm_kernel<128>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
 }
 
 void launch_silu_mul(const bf16* gu, bf16* act, int rows, int ffn, cudaStream_t st) {
   dim3 grid((ffn / 8 + 255) / 256, rows);
   count_launch();
-  silu_mul_kernel<<<grid, 256, 0, st>>>(gu, act, ffn);
+  launch_pdl(silu_mul_kernel, dim3(grid), dim3(256), 0, st, gu, act, ffn);
 }
 
 void launch_rope_kv(bf16* qkv, const float2* rope, const KvGeom& kv, int layer, int rows, int heads,
@@ -243,12 +258,12 @@ void launch_rope_kv(bf16* qkv, const float2* rope, const KvGeom& kv, int layer, 
   const int64_t warps = (int64_t)rows * (heads + 2 * kv.kv_heads);
   const int blocks = (int)((warps * 32 + 255) / 256);
   count_launch();
-  rope_kv_kernel<<<blocks, 256, 0, st>>>(qkv, rope, kv, layer, rows, heads, seq, pos, seq0, pos0);
+  launch_pdl(rope_kv_kernel, dim3(blocks), dim3(256), 0, st, qkv, rope, kv, layer, rows, heads, seq, pos, seq0, pos0);
 }
 
 void launch_argmax(const float* logits, int M, int V, int32_t* out, float*, cudaStream_t st) {
   count_launch();
-  argmax_kernel<<<M, 1024, 0, st>>>(logits, V, out);
+  launch_pdl(argmax_kernel, dim3(M), dim3(1024), 0, st, logits, V, out);
 }
 
 }  // namespace ws

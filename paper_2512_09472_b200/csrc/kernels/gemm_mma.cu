@@ -6,6 +6,7 @@
 #include "../common.h"
 #include "device.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace ws {
 namespace {
@@ -22,6 +23,8 @@ __global__ void __launch_bounds__(THREADS) gemm_mma_kernel(const bf16* __restric
                                                            const bf16* __restrict__ B, int M, int N,
                                                            int K, int epi, void* __restrict__ Cout,
                                                            const bf16* __restrict__ bias) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sA = reinterpret_cast<bf16*>(smem_raw);
   bf16* sB = sA + STAGES * TILE_ELEMS;
@@ -132,6 +135,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(const bf16* __restrict__ A,
                                                    const bf16* __restrict__ B, int M, int N, int K,
                                                    int epi, void* __restrict__ Cout,
                                                    const bf16* __restrict__ bias) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int n_warps = (gridDim.x * blockDim.x) >> 5;
@@ -199,7 +204,7 @@ void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi,
   }
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
   count_launch();
-  gemm_mma_kernel<<<grid, THREADS, smem, st>>>(A, B, M, N, K, (int)epi, C, bias);
+  launch_pdl(gemm_mma_kernel, dim3(grid), dim3(THREADS), smem, st, A, B, M, N, K, (int)epi, C, bias);
 }
 
 void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
@@ -217,13 +222,13 @@ void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
   count_launch();
   if (M <= 1)
-    gemv_kernel<1><<<blocks, 256, 0, st>>>(A, B, M, N, K, (int)epi, C, bias);
+    launch_pdl(gemv_kernel<1>, dim3(blocks), dim3(256), 0, st, A, B, M, N, K, (int)epi, C, bias);
   else if (M <= 4)
-    gemv_kernel<4><<<blocks, 256, 0, st>>>(A, B, M, N, K, (int)epi, C, bias);
+    launch_pdl(gemv_kernel<4>, dim3(blocks), dim3(256), 0, st, A, B, M, N, K, (int)epi, C, bias);
   else if (M <= 8)
-    gemv_kernel<8><<<blocks, 256, 0, st>>>(A, B, M, N, K, (int)epi, C, bias);
+    launch_pdl(gemv_kernel<8>, dim3(blocks), dim3(256), 0, st, A, B, M, N, K, (int)epi, C, bias);
   else
-    gemv_kernel<16><<<blocks, 256, 0, st>>>(A, B, M, N, K, (int)epi, C, bias);
+    launch_pdl(gemv_kernel<16>, dim3(blocks), dim3(256), 0, st, A, B, M, N, K, (int)epi, C, bias);
 }
 
 }  // namespace ws

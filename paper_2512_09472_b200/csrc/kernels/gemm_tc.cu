@@ -21,6 +21,7 @@
 #include "../driver.h"
 #include "device.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace ws {
 namespace {
@@ -239,6 +240,7 @@ template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    int M, int N, int K, const __grid_constant__ TcEpilogue ep) {
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;  // SWIZZLE_128B atoms need 1024 B alignment
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  pdl_wait();  // everything above is prologue; global data from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -388,6 +391,7 @@ template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                     int N, int K, const __grid_constant__ TcEpilogue ep) {
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
@@ -430,6 +434,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  pdl_wait();  // everything above is prologue; global data from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -566,7 +571,7 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   count_launch();
-  gemm_tc_kernel<MODE><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, M, N, K, e);
+  launch_pdl(gemm_tc_kernel<MODE>, dim3(grid), dim3(THREADS), SMEM_BYTES, st, ma, mb, M, N, K, e);
 }
 
 template <int MODE>
@@ -580,7 +585,7 @@ void launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
   const int tiles = ((M + 255) / 256) * (N / P_BN);
   const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
   count_launch();
-  gemm_tc2_kernel<MODE><<<grid, THREADS, P_SMEM_BYTES, st>>>(ma, mb, M, N, K, e);
+  launch_pdl(gemm_tc2_kernel<MODE>, dim3(grid), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e);
 }
 
 int g_pair_mode = -1;  // -1: unset (env WS_GEMM_PAIR, default on), 0 off, 1 on

@@ -40,14 +40,22 @@ def main():
     w.switch_memory(cfg.name)
     toks = torch.randint(0, cfg.vocab, (a.tokens,), dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
+    dev_ms = []
     for i in range(a.iters):
         t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(w.compute):
             s = w.open_seq(a.tokens)
+            e0.record(w.compute)
             w.prefill(s, toks)
+            e1.record(w.compute)
             w.close_seq(s)
         torch.cuda.synchronize()
-        print(f"prefill {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms", flush=True)
+        dev_ms.append(e0.elapsed_time(e1))
+        print(f"prefill {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms wall, {dev_ms[-1]:.3f} ms device", flush=True)
+    if len(dev_ms) > 2:
+        tail = sorted(dev_ms[2:])
+        print(f"device median {tail[len(tail) // 2]:.3f} ms min {tail[0]:.3f} ms over {len(tail)}", flush=True)
     w.release()
     w.close()
 
