@@ -261,7 +261,11 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* weights, const int32
 int ws_model_set_comm(ws_model* m, ws_comm* comm);
 
 /* Standalone GEMM entry for tests/bench: C = A[M,K] * B[N,K]^T, epilogue
- * 0 bf16, 1 bf16+bias, 2 fp32 accumulate, 3 fp32 store; impl as above. */
+ * 0 bf16, 1 bf16+bias, 2 fp32 accumulate, 3 fp32 store, 4 SwiGLU (B = Wgu with
+ * 128-row interleaved gate/up blocks, C = bf16 [M, N/2]; tcgen05 paths only).
+ * impl: 0 dispatch (skinny tcgen05 for M <= 128, tcgen05 tiles above), 1 legacy
+ * mma.sync, 2 legacy GEMV, 3 force the tiled tcgen05 kernel, 4 force the skinny
+ * split-K tcgen05 kernel. */
 int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
             void* C, const void* bias, int32_t impl, void* stream);
 

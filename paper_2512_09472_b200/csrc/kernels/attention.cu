@@ -4,8 +4,10 @@
 // q head), 4 warps x 16 query rows, K/V tiles of 64 keys gathered page by page
 // with cp.async (double-buffered), S = QK^T and O += PV on mma.sync, online
 // softmax in fp32 registers (exp2 with the log2e-folded scale).
-// Decode: split-K over the context, one CTA per (split, kv head, sequence)
-// serving all q heads of the GQA group, then a combine kernel.
+// Decode: split-K over the context, one CTA per (split, kv head, sequence),
+// the GQA group on the M side of mma.sync, then a combine kernel.
+#include <algorithm>
+
 #include "../common.h"
 #include "device.cuh"
 #include "ops.cuh"
@@ -204,143 +206,244 @@ __global__ void __launch_bounds__(kWarps * 32) attn_prefill_kernel(const bf16* _
 }
 
 // ---------------------------------------------------------------- decode
-constexpr int kSplit = 256;      // keys per split
-constexpr int kDecThreads = 128;
-constexpr int kMaxGroup = 8;     // q heads per kv head handled per CTA
+// HBM-bound: every K/V byte of the context is read once per step. Work unit =
+// (key split, kv head, sequence); the CTA's 4 warps take interleaved 16-key
+// tiles of the split, each with its own 3-stage cp.async ring, so one SM keeps
+// ~100 KB of K/V in flight. The GQA group (G <= 16 q heads sharing the kv
+// head) is the M=16 side of mma.sync: S = Q K^T (16 x 16 keys), O += P V,
+// online softmax in registers. The warps' states merge in smem into one
+// unnormalised partial (m, l, O) per split; a combine kernel merges the splits.
+constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = 3;
+constexpr int kDecTargetCtas = 8 * kNumSMs;  // 2 resident CTAs/SM x 4 waves
 
-// partial layout per (seq, q head, split): o[HD] (unnormalised), m, l
 template <int HD>
-__global__ void __launch_bounds__(kDecThreads) attn_decode_kernel(
+struct DecodeSmem {
+  static constexpr int kStride = HD + 8;  // padded rows: conflict-free ldmatrix
+  static constexpr int kTile = kDecKeys * kStride;
+  static constexpr int kWarp = kDecStages * 2 * kTile;  // K and V per stage
+  static constexpr int kBytes = kDecWarps * kWarp * 2;
+};
+
+// partial layout per (seq, q head, part): o[HD] (unnormalised), m, l
+template <int HD>
+__global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
-    int n_splits) {
+    int n_splits, int split_keys) {
   pdl_trigger();
   pdl_wait();
+  using S = DecodeSmem<HD>;
+  constexpr int ST = S::kStride, CH = HD / 8;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bf16* sw = reinterpret_cast<bf16*>(smem_raw) + warp * S::kWarp;
   const int G = heads / kv.kv_heads;
   const int len = pos[b] + 1;  // the new token's K/V is already appended
-  const int k_lo = split * kSplit, k_hi = min(len, k_lo + kSplit);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ float sq[kMaxGroup][HD];
-  __shared__ float sp[kMaxGroup][kSplit];
-  __shared__ float so[kDecThreads / 32][kMaxGroup][HD];
-  __shared__ float sm[kMaxGroup], sl[kMaxGroup];
-  const int ldq = (heads + 2 * kv.kv_heads) * HD;
-  for (int i = tid; i < G * HD; i += kDecThreads)
-    sq[i / HD][i % HD] = bf2f(qkv[(int64_t)b * ldq + (kvh * G + i / HD) * HD + i % HD]);
-  __syncthreads();
+  const int k_lo = split * split_keys, k_hi = min(len, k_lo + split_keys);
+  const int n_tiles = k_hi > k_lo ? (k_hi - k_lo + kDecKeys - 1) / kDecKeys : 0;
+  const int my_n = n_tiles > warp ? (n_tiles - warp + kDecWarps - 1) / kDecWarps : 0;
   const int32_t* bt = kv.block_tables + (int64_t)seqs[b] * kv.max_blocks;
   const int64_t k_plane = kv.plane(layer, 0, kvh), v_plane = kv.plane(layer, 1, kvh);
-  // scores: half-warp per key, 16 lanes x (HD/16) dims
-  constexpr int DPL = HD / 16;
-  const int half = lane >> 4, hl = lane & 15;
-  // warp-uniform trip count: both half-warps iterate together (full-mask shuffles)
-  for (int kb = k_lo + warp * 2; kb < k_hi; kb += kDecThreads / 16) {
-    const int key = kb + half;
-    const bool valid = key < k_hi;
-    float kf[DPL];
-    if (valid) {
-      const int32_t page = bt[key / kv.tpb];
-      const bf16* kr = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) +
-                       k_plane + (int64_t)(key % kv.tpb) * HD + hl * DPL;
+
+  auto load = [&](int stage, int t) {
+    bf16* tk = sw + stage * 2 * S::kTile;
+    bf16* tv = tk + S::kTile;
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) kf[d] = bf2f(kr[d]);
-    } else {
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) kf[d] = 0.f;
+    for (int i = lane; i < kDecKeys * CH; i += 32) {
+      const int r = i / CH, c = i % CH;
+      const int key = k_lo + t * kDecKeys + r;
+      const bool ok = key < k_hi;
+      const int kk = ok ? key : k_lo;
+      const int32_t page = bt[kk / kv.tpb];
+      const bf16* base = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) +
+                         (int64_t)(kk % kv.tpb) * HD + c * 8;
+      cp_async16(tk + r * ST + c * 8, base + k_plane, ok);
+      cp_async16(tv + r * ST + c * 8, base + v_plane, ok);
     }
-    for (int g = 0; g < G; ++g) {
-      float acc = 0.f;
+  };
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) acc += kf[d] * sq[g][hl * DPL + d];
-      acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (hl == 0 && valid) sp[g][key - k_lo] = acc * scale_log2;
-    }
+  for (int s = 0; s < kDecStages - 1; ++s) {
+    if (s < my_n) load(s, warp + s * kDecWarps);
+    cp_async_commit();
   }
-  __syncthreads();
-  // per-head max / exp / sum over this split (warp g handles head g, g+4..)
-  for (int g = warp; g < G; g += kDecThreads / 32) {
-    float mx = -INFINITY;
-    for (int k = lane; k < k_hi - k_lo; k += 32) mx = fmaxf(mx, sp[g][k]);
-    mx = warp_max(mx);
-    float s = 0.f;
-    for (int k = lane; k < k_hi - k_lo; k += 32) {
-      const float p = exp2f(sp[g][k] - mx);
-      sp[g][k] = p;
-      s += p;
-    }
-    s = warp_sum(s);
-    if (lane == 0) {
-      sm[g] = mx;
-      sl[g] = s;
-    }
+
+  // Q as the A operand: rows = the group's q heads (rows >= G are zero)
+  const int g0 = lane >> 2, g1 = g0 + 8;
+  const int ldq = (heads + 2 * kv.kv_heads) * HD;
+  const bf16* q0 = qkv + (int64_t)b * ldq + (int64_t)(kvh * G + g0) * HD;
+  const bf16* q1 = qkv + (int64_t)b * ldq + (int64_t)(kvh * G + g1) * HD;
+  uint32_t qf[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int c = kk * 16 + (lane & 3) * 2;
+    qf[kk][0] = g0 < G ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
+    qf[kk][1] = g1 < G ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
+    qf[kk][2] = g0 < G ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
+    qf[kk][3] = g1 < G ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
   }
-  __syncthreads();
-  // O = sum_k p_k V_k : warp w takes keys w, w+4, ...; lane owns HD/32 dims
-  constexpr int DV = HD / 32;
-  float acc[kMaxGroup][DV];
+
+  float o[HD / 8][4];
 #pragma unroll
-  for (int g = 0; g < kMaxGroup; ++g)
+  for (int j = 0; j < HD / 8; ++j)
 #pragma unroll
-    for (int d = 0; d < DV; ++d) acc[g][d] = 0.f;
-  for (int key = k_lo + warp; key < k_hi; key += kDecThreads / 32) {
-    const int32_t page = bt[key / kv.tpb];
-    const bf16* vr = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) + v_plane +
-                     (int64_t)(key % kv.tpb) * HD + lane * DV;
-    float vf[DV];
+    for (int e = 0; e < 4; ++e) o[j][e] = 0.f;
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+
+  for (int it = 0; it < my_n; ++it) {
+    const int nx = it + kDecStages - 1;
+    if (nx < my_n) load(nx % kDecStages, warp + nx * kDecWarps);
+    cp_async_commit();
+    cp_async_wait<kDecStages - 1>();
+    __syncwarp();
+    const bf16* tk = sw + (it % kDecStages) * 2 * S::kTile;
+    const bf16* tv = tk + S::kTile;
+    float s[2][4];
 #pragma unroll
-    for (int d = 0; d < DV; ++d) vf[d] = bf2f(vr[d]);
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
-    for (int g = 0; g < kMaxGroup; ++g) {
-      if (g < G) {
-        const float p = sp[g][key - k_lo];
+      for (int e = 0; e < 4; ++e) s[j][e] = 0.f;
 #pragma unroll
-        for (int d = 0; d < DV; ++d) acc[g][d] += p * vf[d];
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, tk + ((lane & 7) + ((lane >> 4) << 3)) * ST + kk * 16 + ((lane >> 3) & 1) * 8);
+      uint32_t bl[2] = {b0, b1}, bh[2] = {b2, b3};
+      mma_bf16_16816(s[0], qf[kk], bl);
+      mma_bf16_16816(s[1], qf[kk], bh);
+    }
+    const int key_base = k_lo + (warp + it * kDecWarps) * kDecKeys + (lane & 3) * 2;
+    float mx[2] = {m_run[0], m_run[1]};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = s[j][e] * scale_log2;
+        if (key_base + j * 8 + (e & 1) >= k_hi) v = -INFINITY;
+        s[j][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
       }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+    }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float base = mx[r] == -INFINITY ? 0.f : mx[r];
+      corr[r] = exp2f(m_run[r] - base);
+      m_run[r] = mx[r];
+      mx[r] = base;
+    }
+    uint32_t a[4];
+    float lsum[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float p0 = exp2f(s[j][0] - mx[0]), p1 = exp2f(s[j][1] - mx[0]);
+      const float p2 = exp2f(s[j][2] - mx[1]), p3 = exp2f(s[j][3] - mx[1]);
+      lsum[0] += p0 + p1;
+      lsum[1] += p2 + p3;
+      a[2 * j] = pack_bf16x2(p0, p1);
+      a[2 * j + 1] = pack_bf16x2(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) l_run[r] = l_run[r] * corr[r] + lsum[r];
+#pragma unroll
+    for (int j = 0; j < HD / 8; ++j) {
+      o[j][0] *= corr[0];
+      o[j][1] *= corr[0];
+      o[j][2] *= corr[1];
+      o[j][3] *= corr[1];
+    }
+#pragma unroll
+    for (int d = 0; d < HD / 16; ++d) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4_trans(b0, b1, b2, b3, tv + ((lane & 7) + ((lane >> 3) & 1) * 8) * ST + d * 16 + (lane >> 4) * 8);
+      uint32_t bl[2] = {b0, b1}, bh[2] = {b2, b3};
+      mma_bf16_16816(o[2 * d], a, bl);
+      mma_bf16_16816(o[2 * d + 1], a, bh);
+    }
+    __syncwarp();  // every lane is done with this stage before it is refilled
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
+    l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 2);
+  }
+  // merge the 4 warps' states in smem (the K/V rings are free now), one part per split
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem_raw);  // [warp][16 rows][HD + 2]
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    float* row = red + ((int64_t)warp * 16 + (r ? g1 : g0)) * (HD + 2);
+#pragma unroll
+    for (int j = 0; j < HD / 8; ++j)
+      *reinterpret_cast<float2*>(row + j * 8 + (lane & 3) * 2) = make_float2(o[j][2 * r], o[j][2 * r + 1]);
+    if ((lane & 3) == 0) {
+      row[HD] = my_n > 0 ? m_run[r] : -INFINITY;
+      row[HD + 1] = l_run[r];
     }
   }
-#pragma unroll
-  for (int g = 0; g < kMaxGroup; ++g)
-    if (g < G)
-#pragma unroll
-      for (int d = 0; d < DV; ++d) so[warp][g][lane * DV + d] = acc[g][d];
   __syncthreads();
-  for (int i = tid; i < G * HD; i += kDecThreads) {
-    const int g = i / HD, d = i % HD;
-    float v = 0.f;
+  for (int idx = threadIdx.x; idx < G * HD; idx += kDecWarps * 32) {
+    const int g = idx / HD, d = idx % HD;
+    float mw[kDecWarps], mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kDecThreads / 32; ++w) v += so[w][g][d];
+    for (int w = 0; w < kDecWarps; ++w) {
+      mw[w] = red[((int64_t)w * 16 + g) * (HD + 2) + HD];
+      mx = fmaxf(mx, mw[w]);
+    }
+    float acc = 0.f, l = 0.f;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) {
+      if (mw[w] == -INFINITY) continue;
+      const float f = exp2f(mw[w] - mx);
+      const float* row = red + ((int64_t)w * 16 + g) * (HD + 2);
+      acc += f * row[d];
+      l += f * row[HD + 1];
+    }
     float* dst = part + (((int64_t)b * heads + kvh * G + g) * n_splits + split) * (HD + 2);
-    dst[d] = v;
+    dst[d] = acc;
     if (d == 0) {
-      dst[HD] = k_hi > k_lo ? sm[g] : -INFINITY;
-      dst[HD + 1] = k_hi > k_lo ? sl[g] : 0.f;
+      dst[HD] = mx;
+      dst[HD + 1] = l;
     }
   }
 }
 
+// out[b, h] = sum_p w_p o_p / sum_p w_p l_p with w_p = 2^(m_p - max m). Warp 0
+// computes the weights of all parts, then every thread owns one dim.
+constexpr int kMaxSplits = 256;
 template <int HD>
 __global__ void __launch_bounds__(HD) attn_combine_kernel(const float* __restrict__ part,
                                                           bf16* __restrict__ out, int heads,
-                                                          int n_splits) {
+                                                          int n_parts) {
   pdl_trigger();
   pdl_wait();
   const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x;
-  const float* p = part + ((int64_t)b * heads + h) * n_splits * (HD + 2);
-  float mx = -INFINITY;
-  for (int s = 0; s < n_splits; ++s) mx = fmaxf(mx, p[s * (HD + 2) + HD]);
-  float num = 0.f, den = 0.f;
-  for (int s = 0; s < n_splits; ++s) {
-    const float m = p[s * (HD + 2) + HD];
-    if (m == -INFINITY) continue;
-    const float w = exp2f(m - mx);
-    num += w * p[s * (HD + 2) + d];
-    den += w * p[s * (HD + 2) + HD + 1];
+  const float* p = part + ((int64_t)b * heads + h) * n_parts * (HD + 2);
+  __shared__ float sw[kMaxSplits];
+  __shared__ float s_inv;
+  if (d < 32) {
+    float mx = -INFINITY;
+    for (int s = d; s < n_parts; s += 32) mx = fmaxf(mx, p[s * (HD + 2) + HD]);
+    mx = warp_max(mx);
+    float den = 0.f;
+    for (int s = d; s < n_parts; s += 32) {
+      const float m = p[s * (HD + 2) + HD];
+      const float w = m == -INFINITY ? 0.f : exp2f(m - mx);
+      sw[s] = w;
+      den += w * p[s * (HD + 2) + HD + 1];
+    }
+    den = warp_sum(den);
+    if (d == 0) s_inv = den > 0 ? 1.f / den : 0.f;
   }
-  out[(int64_t)b * heads * HD + h * HD + d] = f2bf(den > 0 ? num / den : 0.f);
+  __syncthreads();
+  float num = 0.f;
+#pragma unroll 8
+  for (int s = 0; s < n_parts; ++s) num += sw[s] * p[s * (HD + 2) + d];
+  out[(int64_t)b * heads * HD + h * HD + d] = f2bf(num * s_inv);
 }
 
 template <int HD>
@@ -362,11 +465,21 @@ template <int HD>
 void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
                  const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
                  cudaStream_t st) {
-  const int n_splits = (max_ctx + kSplit - 1) / kSplit;
+  using S = DecodeSmem<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+    attr = true;
+  }
+  // enough (split, kv head, seq) units to fill the SMs; >= 64 keys per split
+  const int units = n_seqs * kv.kv_heads;
+  int n_splits = std::max(1, std::min({(kDecTargetCtas + units - 1) / units, (max_ctx + 63) / 64, kMaxSplits}));
+  const int split_keys = ((max_ctx + n_splits - 1) / n_splits + kDecKeys - 1) / kDecKeys * kDecKeys;
+  n_splits = (max_ctx + split_keys - 1) / split_keys;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
   count_launch(2);
-  launch_pdl(attn_decode_kernel<HD>, dim3(grid), dim3(kDecThreads), 0, st, qkv, kv, layer, seqs, ctx, heads,
-                                                       scale * 1.4426950408889634f, scratch, n_splits);
+  launch_pdl(attn_decode_kernel<HD>, grid, dim3(kDecWarps * 32), S::kBytes, st, qkv, kv, layer, seqs, ctx, heads,
+             scale * 1.4426950408889634f, scratch, n_splits, split_keys);
   launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
 }
 
@@ -393,8 +506,9 @@ void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,
   }
 }
 
-int decode_scratch_floats(int n_seqs, int heads, int head_dim, int max_ctx) {
-  return n_seqs * heads * ((max_ctx + kSplit - 1) / kSplit) * (head_dim + 2);
+int decode_scratch_floats(int n_seqs, int heads, int kv_heads, int head_dim) {
+  // one part per split, n_splits <= ceil(target / (n_seqs * kv_heads))
+  return (head_dim + 2) * (kDecTargetCtas * (heads / kv_heads) + n_seqs * heads);
 }
 
 }  // namespace ws

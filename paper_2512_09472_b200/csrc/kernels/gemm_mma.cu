@@ -209,6 +209,13 @@ void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi,
 
 void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                  const bf16* bias, cudaStream_t st) {
+  if (M <= 128) {
+    TcEpilogue e;
+    e.mode = epi;
+    e.C = C;
+    e.bias = bias;
+    if (launch_gemm_skinny(A, B, M, N, K, e, st)) return;
+  }
   if (M < 16)
     launch_gemv(A, B, M, N, K, epi, C, bias, st);
   else if (!launch_gemm_tc(A, B, M, N, K, epi, C, bias, st))

@@ -1,0 +1,413 @@
+// Decode-shaped tcgen05 GEMM: C[M,N] = A[M,K] . W[N,K]^T for M <= 128.
+//
+// Decode rows are few, so the GEMM is a weight stream (HBM bound): the kernel
+// swaps the operands — 128 weight rows are the MMA's M side, the M activation
+// rows (padded to Mp, a multiple of 16) its N side — so one
+// tcgen05.mma.cta_group::1 M=128 N=Mp K=16 consumes a whole 128x16 weight
+// slice however small the batch is.
+//
+// Persistent stream-K: one CTA per SM; the (unit, k-block) iteration space —
+// unit = one 128-row weight block (a 256-row gate|up group for SwiGLU) — is
+// cut into equal contiguous ranges, so every SM streams the same number of
+// weight bytes through one uninterrupted TMA ring, with no wave quantization
+// whatever N and K are. A CTA's range is a list of segments (one per unit it
+// touches); only its first and last segment can cover part of a unit.
+//
+//   warp 0 lane 0  TMA producer: W block(s) 128x64 + A Mp x64 per stage (SW128)
+//   warp 1 lane 0  MMA issuer; double-buffered TMEM accumulators [128][NB*Mp]
+//   warp 2         TMEM allocation
+//   warps 4-7      epilogue: TMEM lane i = weight row i, columns = batch rows
+//
+// A segment covering a whole unit is stored directly. Partial segments write
+// fp32 partials to a per-(CTA, first|last) slot and skinny_fixup_kernel sums
+// each split unit's contributors in k order — deterministic — and applies the
+// epilogue: bf16, +bias, fp32 store, fp32 residual add, or SwiGLU over the
+// gate block (TMEM columns [0,Mp)) and the matching up block (columns
+// [Mp,2Mp)) of the interleaved Wgu.
+#include <cuda.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "../common.h"
+#include "../driver.h"
+#include "device.cuh"
+#include "ops.cuh"
+#include "pdl.cuh"
+#include "tcgen05.cuh"
+
+namespace ws {
+namespace {
+
+using namespace dev;
+
+constexpr int kRows = 128, kBK = 64, kThreads = 256;
+constexpr int kW_BYTES = kRows * kBK * 2;  // 16 KiB weight tile
+constexpr int kSmemBudget = 200 * 1024;    // TMA ring, one CTA per SM
+
+struct SkinnyArgs {
+  int M, N, K, Mp, stages, stage_bytes, total_iters;
+  float* partial;      // [grid][2][NB*128][Mp]
+};
+
+template <int MODE>
+__device__ __forceinline__ void store_out(const TcEpilogue& ep, const SkinnyArgs& a, int row, const float* v,
+                                          int c0) {
+  // v[j]: batch row c0 + j of output column `row`
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int b = c0 + j;
+    if (b >= a.M) break;
+    float x = v[j];
+    if constexpr (MODE == (int)Epi::kAddF32) {
+      // exactly one add per element (whole unit or reduced sum): deterministic,
+      // and a fire-and-forget reduction instead of a load-add-store chain
+      atomicAdd(static_cast<float*>(ep.C) + (int64_t)b * a.N + row, x);
+    } else if constexpr (MODE == (int)Epi::kStoreF32) {
+      static_cast<float*>(ep.C)[(int64_t)b * a.N + row] = x;
+    } else if constexpr (MODE == (int)Epi::kSwiGLU) {
+      static_cast<bf16*>(ep.C)[(int64_t)b * (a.N / 2) + row] = f2bf(x);
+    } else {
+      if constexpr (MODE == (int)Epi::kBiasBf16) x += bf2f(ep.bias[row]);
+      static_cast<bf16*>(ep.C)[(int64_t)b * a.N + row] = f2bf(x);
+    }
+  }
+}
+
+// CTA whose iteration range [it_begin(c), it_begin(c+1)) contains `it`
+__device__ __forceinline__ int cta_of(int64_t it, int G, int total) { return (int)(((it + 1) * G - 1) / total); }
+__device__ __forceinline__ int it_begin(int c, int G, int total) { return (int)((int64_t)c * total / G); }
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ SkinnyArgs args, const __grid_constant__ TcEpilogue ep) {
+  constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  pdl_trigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023) & ~1023u;
+  const int S = args.stages;
+  const uint32_t bars = base + S * args.stage_bytes;
+  auto full = [&](int s) { return bars + 8 * s; };
+  auto empty = [&](int s) { return bars + 8 * (S + s); };
+  auto tfull = [&](int b) { return bars + 8 * (2 * S + b); };
+  auto tempty = [&](int b) { return bars + 8 * (2 * S + 2 + b); };
+  const uint32_t tmem_slot = bars + 8 * (2 * S + 4);
+  volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Mp = args.Mp, G = gridDim.x, total = args.total_iters;
+  const int kbs = args.K / kBK;
+  const int it0 = it_begin(blockIdx.x, G, total), it1 = it_begin(blockIdx.x + 1, G, total);
+  const uint32_t acc_cols = NB * Mp;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < 2 * acc_cols) tmem_cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_a) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(full(s), 1);
+      tc::mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(tfull(b), 1);
+      tc::mbar_init(tempty(b), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  pdl_wait();  // prologue above; global data from here on
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = it0; it < it1; ++it) {
+        const int unit = it / kbs, kb = it % kbs;
+        tc::mbar_wait(empty(stage), phase ^ 1);
+        const uint32_t sa = base + stage * args.stage_bytes;
+        tc::mbar_expect_tx(full(stage), args.stage_bytes);
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          tc::tma_load_2d(sa + j * kW_BYTES, &map_w, full(stage), kb * kBK, (unit * NB + j) * kRows);
+        tc::tma_load_2d(sa + NB * kW_BYTES, &map_a, full(stage), kb * kBK, 0);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer: one accumulator per segment =====
+      const uint32_t idesc = tc::idesc_bf16(kRows, Mp);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int it = it0; it < it1;) {
+        const int seg_end = min(it1, (it / kbs + 1) * kbs);
+        tc::mbar_wait(tempty(acc), acc_phase ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem + acc * acc_cols;
+        for (int i = it; i < seg_end; ++i) {
+          tc::mbar_wait(full(stage), phase);
+          tc::fence_after();
+          const uint32_t sa = base + stage * args.stage_bytes;
+          const uint64_t db = tc::sdesc_sw128(sa + NB * kW_BYTES);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            const uint64_t da = tc::sdesc_sw128(sa + j * kW_BYTES);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle row
+              tc::mma_f16(d + j * Mp, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i > it) | k);
+          }
+          tc::commit(empty(stage));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::commit(tfull(acc));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        it = seg_end;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===== epilogue: thread i <-> TMEM lane i <-> weight row i of the unit's block(s) =====
+    const int i = threadIdx.x - 128;
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int64_t slot_floats = (int64_t)NB * kRows * Mp;
+    int acc = 0, seg = 0;
+    uint32_t acc_phase = 0;
+    for (int it = it0; it < it1; ++seg) {
+      const int unit = it / kbs;
+      const int seg_end = min(it1, (unit + 1) * kbs);
+      const bool whole = it % kbs == 0 && seg_end == (unit + 1) * kbs;
+      const int out_row = unit * kRows + i;  // output column (SwiGLU: act column)
+      tc::mbar_wait(tfull(acc), acc_phase);
+      tc::fence_after();
+      const uint32_t tacc = trow + acc * acc_cols;
+      float* mine = args.partial + ((int64_t)blockIdx.x * 2 + (seg == 0 ? 0 : 1)) * slot_floats;
+      for (int c = 0; c < Mp; c += 16) {
+        uint32_t v[NB][16];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) WS_TMEM_LD16(tacc + j * Mp + c, v[j]);
+        tc::wait_ld();
+        if (whole) {
+          float f[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            f[q] = __uint_as_float(v[0][q]);
+            if constexpr (NB == 2) f[q] = f[q] / (1.f + __expf(-f[q])) * __uint_as_float(v[NB - 1][q]);
+          }
+          store_out<MODE>(ep, args, out_row, f, c);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            float4* dst = reinterpret_cast<float4*>(mine + ((int64_t)j * kRows + i) * Mp + c);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              __stcg(dst + q, make_float4(__uint_as_float(v[j][4 * q]), __uint_as_float(v[j][4 * q + 1]),
+                                          __uint_as_float(v[j][4 * q + 2]), __uint_as_float(v[j][4 * q + 3])));
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(tempty(acc));  // accumulator drained: the MMA may reuse it
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+      it = seg_end;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// Split-K fix-up for the units no single CTA covered: out = epilogue(sum of
+// the contributors' partials in k order). Deterministic, and spread over the
+// whole GPU instead of one CTA per unit at the tail of the GEMM. Thread =
+// (unit, weight row i, 4 batch rows); rows fastest so the output stores of a
+// warp are coalesced. Launched with PDL right behind the GEMM.
+template <int MODE>
+__global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant__ SkinnyArgs args,
+                                                           const __grid_constant__ TcEpilogue ep, int G) {
+  constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  pdl_trigger();
+  pdl_wait();
+  const int Mp = args.Mp, kbs = args.K / kBK, total = args.total_iters;
+  const int quads = Mp / 4;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int unit = (int)(t / (kRows * quads));
+  if (unit >= total / kbs) return;
+  const int rem = (int)(t % (kRows * quads));
+  const int q4 = rem / kRows, i = rem % kRows;
+  const int c_first = cta_of((int64_t)unit * kbs, G, total);
+  const int c_last = cta_of((int64_t)(unit + 1) * kbs - 1, G, total);
+  if (c_first == c_last) return;  // whole unit: stored by the GEMM
+  const int64_t slot_floats = (int64_t)NB * kRows * Mp;
+  float4 sum[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) sum[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int cc = c_first; cc <= c_last; ++cc) {  // k order
+    const int slot = unit == it_begin(cc, G, total) / kbs ? 0 : 1;
+    const float* src = args.partial + ((int64_t)cc * 2 + slot) * slot_floats;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(src + ((int64_t)j * kRows + i) * Mp) + q4);
+      sum[j].x += p.x;
+      sum[j].y += p.y;
+      sum[j].z += p.z;
+      sum[j].w += p.w;
+    }
+  }
+  float v[4] = {sum[0].x, sum[0].y, sum[0].z, sum[0].w};
+  if constexpr (NB == 2) {
+    const float u[4] = {sum[1].x, sum[1].y, sum[1].z, sum[1].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
+  }
+  const int row = unit * kRows + i;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = q4 * 4 + k;
+    if (b >= args.M) break;
+    if constexpr (MODE == (int)Epi::kAddF32) {
+      static_cast<float*>(ep.C)[(int64_t)b * args.N + row] += v[k];
+    } else if constexpr (MODE == (int)Epi::kStoreF32) {
+      static_cast<float*>(ep.C)[(int64_t)b * args.N + row] = v[k];
+    } else if constexpr (MODE == (int)Epi::kSwiGLU) {
+      static_cast<bf16*>(ep.C)[(int64_t)b * (args.N / 2) + row] = f2bf(v[k]);
+    } else {
+      float x = v[k];
+      if constexpr (MODE == (int)Epi::kBiasBf16) x += bf2f(ep.bias[row]);
+      static_cast<bf16*>(ep.C)[(int64_t)b * args.N + row] = f2bf(x);
+    }
+  }
+}
+
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
+  const Driver* d = driver();
+  if (!d) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Partial slots, one set per (device, stream): launches on one
+// stream are ordered, so they can share it. Slots: 148 CTAs x 2 x 256 rows x
+// 128 columns fp32 = 38.8 MB.
+constexpr int64_t kPartialFloats = (int64_t)kNumSMs * 2 * 2 * kRows * 128;
+struct Scratch {
+  float* partial = nullptr;
+};
+std::mutex g_mu;
+std::map<std::pair<int, cudaStream_t>, Scratch> g_scratch;
+
+bool scratch_for(cudaStream_t st, Scratch* out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_scratch.find({dev, st});
+  if (it == g_scratch.end()) {
+    Scratch s;
+    if (cudaMalloc(&s.partial, kPartialFloats * sizeof(float)) != cudaSuccess) return false;
+    it = g_scratch.emplace(std::make_pair(dev, st), s).first;
+  }
+  *out = it->second;
+  return true;
+}
+
+int g_skinny_mode = -1;  // env WS_SKINNY=0 disables (A/B against the GEMV / 128-row tiles)
+
+template <int MODE>
+void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs& a, int grid, int smem,
+                 const TcEpilogue& e, cudaStream_t st) {
+  static int attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(gemm_skinny_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
+  }
+  count_launch();
+  launch_pdl(gemm_skinny_kernel<MODE>, dim3(grid), dim3(kThreads), (size_t)smem, st, mw, ma, a, e);
+  const int kbs = a.K / kBK, units = a.total_iters / kbs;
+  bool split = false;  // does any CTA boundary fall inside a unit?
+  for (int c = 1; c < grid && !split; ++c) split = ((int64_t)c * a.total_iters / grid) % kbs != 0;
+  if (split) {
+    const int64_t threads = (int64_t)units * kRows * (a.Mp / 4);
+    count_launch();
+    launch_pdl(skinny_fixup_kernel<MODE>, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, a, e, grid);
+  }
+}
+
+}  // namespace
+
+bool gemm_skinny_enabled() {
+  if (g_skinny_mode < 0) {
+    const char* v = getenv("WS_SKINNY");
+    g_skinny_mode = (v && v[0] == '0') ? 0 : 1;
+  }
+  return g_skinny_mode == 1;
+}
+
+bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st) {
+  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBK || K % kBK || e.mode == Epi::kRopeKV) return false;
+  const int NB = e.mode == Epi::kSwiGLU ? 2 : 1;
+  if (N % (kRows * NB)) return false;
+  const int units = N / (kRows * NB), kbs = K / kBK;
+  SkinnyArgs a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.Mp = (M + 15) / 16 * 16;
+  a.stage_bytes = NB * kW_BYTES + a.Mp * kBK * 2;
+  a.stages = std::max(2, std::min(12, kSmemBudget / a.stage_bytes));
+  a.total_iters = units * kbs;
+  const int smem = a.stages * a.stage_bytes + 1024 + 256;
+  // one CTA per SM, >= 2 k-blocks each
+  const int grid = std::max(1, std::min(kNumSMs, a.total_iters / 2));
+  Scratch s;
+  if (!scratch_for(st, &s)) return false;
+  a.partial = s.partial;
+  CUtensorMap mw, ma;
+  if (!make_map(&mw, W, N, K, kRows) || !make_map(&ma, A, M, K, a.Mp)) return false;
+  switch (e.mode) {
+    case Epi::kStoreBf16: launch_mode<0>(mw, ma, a, grid, smem, e, st); break;
+    case Epi::kBiasBf16: launch_mode<1>(mw, ma, a, grid, smem, e, st); break;
+    case Epi::kAddF32: launch_mode<2>(mw, ma, a, grid, smem, e, st); break;
+    case Epi::kStoreF32: launch_mode<3>(mw, ma, a, grid, smem, e, st); break;
+    case Epi::kSwiGLU: launch_mode<4>(mw, ma, a, grid, smem, e, st); break;
+    default: return false;
+  }
+  return true;
+}
+
+}  // namespace ws

@@ -57,7 +57,7 @@ bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int la
 void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,
                         const int32_t* seqs, const int32_t* pos, int n_seqs, int heads,
                         int max_ctx, float scale, float* scratch, cudaStream_t st);
-int decode_scratch_floats(int n_seqs, int heads, int head_dim, int max_ctx);
+int decode_scratch_floats(int n_seqs, int heads, int kv_heads, int head_dim);
 
 // C[M,N] = A[M,K] * B[N,K]^T with epilogue:
 //   kSwiGLU  (tcgen05 only): B = interleaved gate/up rows (128-row blocks);
@@ -91,7 +91,13 @@ void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi,
 bool gemm_tc_supported(int M, int N, int K);
 bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                     const bf16* bias, cudaStream_t st);
-// Skinny GEMM for M <= 16 (decode / lm_head rows): weight-streaming, HBM bound.
+// Decode-shaped tcgen05 GEMM (gemm_skinny.cu): M <= 128, N % 128 == 0
+// (% 256 for kSwiGLU), K % 64 == 0, any epilogue but kRopeKV; swap-AB split-K,
+// HBM bound. Returns false (nothing launched) outside that envelope or when
+// disabled with WS_SKINNY=0.
+bool gemm_skinny_enabled();
+bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st);
+// Legacy CUDA-core GEMV for M <= 16 (fallback when the skinny kernel does not apply).
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                  const bf16* bias, cudaStream_t st);
 // TP boundary helpers: x += p (fp32, count elements); reorder all-gathered

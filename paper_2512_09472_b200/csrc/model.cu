@@ -95,8 +95,8 @@ Workspace make_ws(const ws_model_config& c, int T) {
   w.act = take((int64_t)T * c.ffn * 2);
   w.hl = take((int64_t)T * d * 2);
   w.seqs = take(4 * 4);
-  w.scratch = take((int64_t)ws::decode_scratch_floats(decode_cap(T), c.heads, c.head_dim,
-                                                      c.max_positions) * 4);
+  w.scratch = take((int64_t)ws::decode_scratch_floats(decode_cap(T), c.heads, c.kv_heads,
+                                                      c.head_dim) * 4);
   // TP only: fp32 row-parallel partials and the local lm_head shard logits
   const bool tp = head_rows(c) != c.vocab;
   w.partial = take(tp ? (int64_t)T * d * 4 : 0);
@@ -123,6 +123,8 @@ void gemm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N,
           void* C, const ws::bf16* bias, cudaStream_t st) {
   if ((m->gemm_impl & 1) && M >= 16)
     ws::launch_gemm_mma(A, B, M, N, K, e, C, bias, st);
+  else if (m->gemm_impl & 1)
+    ws::launch_gemv(A, B, M, N, K, e, C, bias, st);  // legacy path end to end
   else
     ws::launch_gemm(A, B, M, N, K, e, C, bias, st);
 }
@@ -135,7 +137,8 @@ void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
   using namespace ws;
   const ws_model_config& c = m->cfg;
   const int q = (c.heads + 2 * c.kv_heads) * c.head_dim;
-  if (!(m->gemm_impl & 1) && rows >= 16) {
+  // decode rows: the split-K skinny GEMM + rope kernel beats 128-row tiles
+  if (!(m->gemm_impl & 1) && rows >= 16 && !(rows <= 128 && ws::gemm_skinny_enabled())) {
     TcEpilogue e;
     e.mode = Epi::kRopeKV;
     e.C = qkv;
@@ -159,11 +162,12 @@ void gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int
                     ws::bf16* act, cudaStream_t st) {
   using namespace ws;
   const ws_model_config& c = m->cfg;
-  if (!(m->gemm_impl & 1) && rows >= 16) {
+  if (!(m->gemm_impl & 1)) {
     TcEpilogue e;
     e.mode = Epi::kSwiGLU;
     e.C = act;
-    if (launch_gemm_tc_epi(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;
+    if (rows <= 128 && launch_gemm_skinny(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;  // decode
+    if (rows >= 16 && launch_gemm_tc_epi(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;
   }
   gemm(m, h, w, rows, 2 * c.ffn, c.hidden, Epi::kStoreBf16, gu, nullptr, st);
   launch_silu_mul(gu, act, rows, c.ffn, st);
@@ -405,18 +409,34 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
 int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epi, void* C,
             const void* bias, int32_t impl, void* stream) {
   using namespace ws;
-  if (M < 1 || N < 1 || K < 32 || K % 32 || epi < 0 || epi > 3) WS_FAIL(WS_ERR_INVALID, "bad GEMM shape");
+  if (M < 1 || N < 1 || K < 32 || K % 32 || epi < 0 || epi > 4) WS_FAIL(WS_ERR_INVALID, "bad GEMM shape");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bf16* a = static_cast<const bf16*>(A);
   const bf16* b = static_cast<const bf16*>(B);
   const bf16* bi = static_cast<const bf16*>(bias);
-  if (impl == 1 && M >= 16) {
+  if (epi == (int)Epi::kSwiGLU) {
+    TcEpilogue e;
+    e.mode = Epi::kSwiGLU;
+    e.C = C;
+    const bool ok = impl == 4   ? launch_gemm_skinny(a, b, M, N, K, e, st)
+                    : impl == 3 ? launch_gemm_tc_epi(a, b, M, N, K, e, st)
+                                : (M <= 128 && launch_gemm_skinny(a, b, M, N, K, e, st)) ||
+                                      launch_gemm_tc_epi(a, b, M, N, K, e, st);
+    if (!ok) WS_FAIL(WS_ERR_INVALID, "SwiGLU GEMM %dx%dx%d unsupported", M, N, K);
+  } else if (impl == 1 && M >= 16) {
     launch_gemm_mma(a, b, M, N, K, (Epi)epi, C, bi, st);
   } else if (impl == 2) {
     launch_gemv(a, b, M, N, K, (Epi)epi, C, bi, st);
   } else if (impl == 3) {
     if (!launch_gemm_tc(a, b, M, N, K, (Epi)epi, C, bi, st))
       WS_FAIL(WS_ERR_INVALID, "shape %dx%dx%d outside the tcgen05 tiling", M, N, K);
+  } else if (impl == 4) {
+    TcEpilogue e;
+    e.mode = (Epi)epi;
+    e.C = C;
+    e.bias = bi;
+    if (!launch_gemm_skinny(a, b, M, N, K, e, st))
+      WS_FAIL(WS_ERR_INVALID, "shape %dx%dx%d outside the skinny tcgen05 envelope", M, N, K);
   } else {
     launch_gemm(a, b, M, N, K, (Epi)epi, C, bi, st);
   }

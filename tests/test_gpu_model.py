@@ -262,3 +262,102 @@ def test_qwen_style_bias_and_phi_head_dim(lib):
         assert res.token == int(ref[-1].argmax())
         w.release()
         w.close()
+
+
+def _swiglu_ref(A, W):
+    """act[:, j] = silu(g) * u with Wgu's 128-row interleaved gate/up blocks."""
+    full = A.float() @ W.float().T
+    n = W.shape[0] // 2
+    j = torch.arange(n, device=A.device)
+    gate = full[:, (j // 128) * 256 + j % 128]
+    up = full[:, (j // 128) * 256 + 128 + j % 128]
+    return torch.nn.functional.silu(gate) * up
+
+
+@pytest.mark.parametrize("M", [1, 7, 16, 40, 128])
+@pytest.mark.parametrize("N,K", [(256, 512), (4096, 4096), (1024, 14336), (6144, 256)])
+def test_gemm_skinny_against_fp32(lib, M, N, K):
+    """impl 4 forces the decode-shaped swap-AB split-K tcgen05 kernel; every
+    epilogue, and the split-K reduction is deterministic (bit-identical reruns)."""
+    import ctypes as C
+
+    g = torch.Generator(device="cuda").manual_seed(M * 31 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+
+    def run(epi, out, b=None):
+        lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, epi,
+                 C.c_void_p(out.data_ptr()), C.c_void_p(b.data_ptr()) if b is not None else None, 4, None)
+        torch.cuda.synchronize()
+
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    run(0, out)
+    assert _rel(out.float(), ref) < 1e-2
+    run(1, out, bias)
+    assert _rel(out.float(), ref + bias.float()) < 1e-2
+    acc = torch.randn(M, N, device="cuda", generator=g)
+    want = acc + ref
+    run(2, acc)
+    assert _rel(acc, want) < 1e-5
+    f1 = torch.empty(M, N, device="cuda")
+    f2 = torch.empty(M, N, device="cuda")
+    run(3, f1)
+    run(3, f2)
+    assert _rel(f1, ref) < 1e-5
+    assert torch.equal(f1, f2)
+    if N % 256 == 0:
+        act = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        run(4, act)
+        assert _rel(act.float(), _swiglu_ref(A, B)) < 1e-2
+
+
+_DECODE_SHAPES = {
+    "llama-like": dict(heads=8, kv_heads=2, head_dim=128, hidden=1024),
+    "qwen-like": dict(heads=14, kv_heads=2, head_dim=128, hidden=1792, qkv_bias=True, rope_theta=1e6),
+    "phi-like": dict(heads=4, kv_heads=4, head_dim=96, hidden=384, rope_theta=1e4),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(_DECODE_SHAPES))
+@pytest.mark.parametrize("lens", [[700], [3 + 61 * i for i in range(12)], [20 + 3 * i for i in range(40)]])
+def test_decode_gqa_shapes_match_oracle(lib, shape, lens):
+    """Decode over the paged pool at head_dim 128/96 and GQA groups 4/7/1:
+    split-K attention (per-warp partials + combine) and the skinny tcgen05
+    GEMMs (1, 12 and 40 rows), 4 steps against the fp32 oracle with KV past."""
+    from paper_2512_09472_b200 import models as M
+
+    cfg = M.TINY.with_(name="d" + shape[:2], **_DECODE_SHAPES[shape])
+    w, host = _worker(cfg, pool_pages=256)
+    try:
+        weights = O.unpack(cfg, cfg.layout(), host.clone())
+        w.prewarm(cfg.name, layers=cfg.layers)
+        w.switch_memory(cfg.name)
+        seqs, pasts, toks = [], [], []
+        for i, n in enumerate(lens):
+            p = _prompt(cfg, 300 + i, n)
+            s = w.open_seq(n + 8)
+            w.prefill(s, p.cuda())
+            seqs.append(s)
+            ref, past = O.forward(cfg, weights, p.long())
+            pasts.append(past)
+            toks.append(int(ref[-1].argmax()))
+        pos = list(lens)
+        worst = 0.0
+        for step in range(4):
+            logits, _ = w.decode(torch.tensor(seqs, dtype=torch.int32, device="cuda"),
+                                 torch.tensor(pos, dtype=torch.int32, device="cuda"),
+                                 torch.tensor(toks, dtype=torch.int32, device="cuda"), max(pos) + 1)
+            got = logits.float().cpu()
+            for i in range(len(lens)):
+                ref, pasts[i] = O.forward(cfg, weights, [toks[i]], pos0=pos[i], past=pasts[i])
+                worst = max(worst, _rel(got[i], ref[0]))
+                toks[i] = int(ref[0].argmax())
+                pos[i] += 1
+        assert worst < LOGIT_RTOL, worst
+        for s in seqs:
+            w.close_seq(s)
+        w.release()
+    finally:
+        w.close()
