@@ -302,6 +302,47 @@ def run_ours(args, rank, world, local_rank):
         rc_done.append((t3 - t2) * 1e6)
         rel_done.append((t4 - t3) * 1e6)
 
+    # ---- decode: every sequence prefilled to decode_ctx, then B tokens per step
+    #      (HBM bound: all weights but the embedding table + each sequence's KV)
+    decode = []
+    if args.decode_batches:
+        w.switch_memory(cfg.name)
+        ctx = args.decode_ctx
+        bmax = max(args.decode_batches)
+        g = torch.Generator().manual_seed(11)
+        seqs = []
+        with torch.cuda.stream(w.compute):
+            for _ in range(bmax):
+                s = w.open_seq(ctx + Wm + K + 1)
+                w.prefill(s, torch.randint(0, cfg.vocab, (ctx,), generator=g, dtype=torch.int32).cuda())
+                seqs.append(s)
+        torch.cuda.synchronize()
+        weight_bytes = entry.layout.total - cfg.vocab * cfg.hidden * 2
+        kv_tok = cfg.kv_geometry()[1]
+        pk_hbm = peaks()[0]["hbm_gbs"]
+        for B in args.decode_batches:
+            sd = torch.tensor(seqs[:B], dtype=torch.int32, device="cuda")
+            tok = torch.randint(0, cfg.vocab, (B,), generator=g, dtype=torch.int32).cuda()
+            with torch.cuda.stream(w.compute):
+                for i in range(Wm + K):
+                    if i == Wm:
+                        barrier()
+                        d0 = torch.cuda.Event(enable_timing=True)
+                        d0.record(w.compute)
+                    pos = torch.full((B,), ctx + i, dtype=torch.int32, device="cuda")
+                    _, tok = w.decode(sd, pos, tok, ctx + i + 1)
+                d1 = torch.cuda.Event(enable_timing=True)
+                d1.record(w.compute)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(d0.elapsed_time(d1)) / K
+            nbytes = weight_bytes + B * (ctx + Wm + K / 2) * kv_tok
+            decode.append({"batch": B, "ctx": ctx, "ms_per_step": ms, "tokens_per_s": world * B / ms * 1e3,
+                           "algorithmic_gb": nbytes / 1e9, "achieved_gbs": nbytes / ms / 1e6,
+                           "frac_of_hbm": nbytes / ms / 1e6 / pk_hbm})
+        for s in seqs:
+            w.close_seq(s)
+        w.release()
+
     # ---- dominant kernel: the gate/up GEMM of the prefill, timed alone
     pk, kind = peaks()
     lay = entry.layout.layers[0]
@@ -389,6 +430,9 @@ def run_ours(args, rank, world, local_rank):
         "prefill": {"ms": prefill_ms, "tflops": cfg.prefill_flops(S) / (prefill_ms / 1e3) / 1e12,
                     "frac_of_sustained": cfg.prefill_flops(S) / (prefill_ms / 1e3) / 1e12 /
                     pk["bf16_tflops_sustained"], "algorithmic_tflop": cfg.prefill_flops(S) / 1e12},
+        "decode": {"per_batch": decode, "bound": "hbm", "peak_gbs": peaks()[0]["hbm_gbs"],
+                   "bytes": "all weights except the embedding table + every sequence's K/V, per step",
+                   "path": "UniversalWorker.decode: skinny stream-K tcgen05 GEMMs + paged GQA decode attention"},
         "roofline": {"bound": "tensor", "kernel": "prefill gate/up GEMM 2048x28672x4096 (tensor-core path)",
                      "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "peak_kind": kind + " burst",
@@ -429,6 +473,8 @@ def main():
     ap.add_argument("--switch-iters", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--decode-ctx", type=int, default=1024)
+    ap.add_argument("--decode-batches", type=lambda v: [int(x) for x in v.split(",") if x], default=[1, 16, 64])
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
