@@ -30,40 +30,45 @@ __global__ void __launch_bounds__(256) embed_kernel(const int32_t* __restrict__ 
   }
 }
 
-// out = bf16(x * rsqrt(mean(x^2) + eps) * w), fp32 math. One CTA per row.
-template <int kThreads>
-__global__ void __launch_bounds__(kThreads) rmsnorm_kernel(const float* __restrict__ x,
-                                                          const bf16* __restrict__ w,
-                                                          bf16* __restrict__ out, int d, float eps) {
+// out = bf16(x * rsqrt(mean(x^2) + eps) * w), fp32 math. One CTA per row;
+// the row stays in registers (kVec float4 per thread, d <= 4*kT*kVec), so x
+// is read from memory exactly once. Few rows (decode) use wide CTAs for
+// memory parallelism, many rows (prefill) narrow ones.
+template <int kT, int kVec>
+__global__ void __launch_bounds__(kT) rmsnorm_kernel(const float* __restrict__ x,
+                                                     const bf16* __restrict__ w,
+                                                     bf16* __restrict__ out, int d, float eps) {
   pdl_trigger();
   pdl_wait();
-  const int r = blockIdx.x;
+  const int r = blockIdx.x, n4 = d / 4;
   const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)r * d);
+  float4 v[kVec];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d / 4; i += kThreads) {
-    float4 v = xr[i];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
   }
-  __shared__ float red[kThreads / 32];
+  __shared__ float red[kT / 32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / (float)d + eps);
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < kT / 32; ++k) tot += red[k];
+  const float inv = rsqrtf(tot / (float)d + eps);
   const uint2* wr = reinterpret_cast<const uint2*>(w);
   uint2* orow = reinterpret_cast<uint2*>(out + (int64_t)r * d);
-  for (int i = threadIdx.x; i < d / 4; i += kThreads) {
-    float4 v = xr[i];
-    uint2 wv = __ldg(wr + i);
-    float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kT;
+    if (i >= n4) break;
+    const uint2 wv = __ldg(wr + i);
+    const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
     uint2 o;
-    o.x = pack_bf16x2(v.x * inv * w0.x, v.y * inv * w0.y);
-    o.y = pack_bf16x2(v.z * inv * w1.x, v.w * inv * w1.y);
+    o.x = pack_bf16x2(v[k].x * inv * w0.x, v[k].y * inv * w0.y);
+    o.y = pack_bf16x2(v[k].z * inv * w1.x, v[k].w * inv * w1.y);
     orow[i] = o;
   }
 }
@@ -241,10 +246,18 @@ void launch_embed(const int32_t* tokens, const bf16* table, float* x, int n, int
 void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, float eps,
                     cudaStream_t st) {
   count_launch();
-  if (d >= 2048)
-    launch_pdl(rmsnorm_kernel<512>, dim3(rows), dim3(512), 0, st, x, w, out, d, eps);
-  else
-    launch_pdl(rmsnorm_kernel<128>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
+  if (rows < 2 * kNumSMs) {  // decode rows
+    if (d <= 4096)
+      launch_pdl(rmsnorm_kernel<512, 2>, dim3(rows), dim3(512), 0, st, x, w, out, d, eps);
+    else
+      launch_pdl(rmsnorm_kernel<512, 4>, dim3(rows), dim3(512), 0, st, x, w, out, d, eps);
+  } else if (d <= 1024) {
+    launch_pdl(rmsnorm_kernel<128, 2>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
+  } else if (d <= 4096) {
+    launch_pdl(rmsnorm_kernel<128, 8>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
+  } else {
+    launch_pdl(rmsnorm_kernel<128, 16>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
+  }
 }
 
 void launch_silu_mul(const bf16* gu, bf16* act, int rows, int ffn, cudaStream_t st) {

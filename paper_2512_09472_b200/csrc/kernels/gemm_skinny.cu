@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = it0; it < it1; ++seg) {
       const int unit = it / kbs;
       const int seg_end = min(it1, (unit + 1) * kbs);
-      const bool whole = it % kbs == 0 && seg_end == (unit + 1) * kbs;
+      // RoPE + KV append needs both halves of a head: always via the fix-up
+      const bool whole = MODE != (int)Epi::kRopeKV && it % kbs == 0 && seg_end == (unit + 1) * kbs;
       const int out_row = unit * kRows + i;  // output column (SwiGLU: act column)
       tc::mbar_wait(tfull(acc), acc_phase);
       tc::fence_after();
@@ -252,18 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (unit, weight row i, 4 batch rows); rows fastest so the output stores of a
 // warp are coalesced. Launched with PDL right behind the GEMM.
 template <int MODE>
-__global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant__ SkinnyArgs args,
-                                                           const __grid_constant__ TcEpilogue ep, int G) {
+__device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEpilogue& ep, int G, int unit, int i,
+                                              int q4) {
   constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
-  pdl_trigger();
-  pdl_wait();
   const int Mp = args.Mp, kbs = args.K / kBK, total = args.total_iters;
-  const int quads = Mp / 4;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int unit = (int)(t / (kRows * quads));
-  if (unit >= total / kbs) return;
-  const int rem = (int)(t % (kRows * quads));
-  const int q4 = rem / kRows, i = rem % kRows;
   const int c_first = cta_of((int64_t)unit * kbs, G, total);
   const int c_last = cta_of((int64_t)(unit + 1) * kbs - 1, G, total);
   if (c_first == c_last) return;  // whole unit: stored by the GEMM
@@ -305,6 +298,82 @@ __global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant
       float x = v[k];
       if constexpr (MODE == (int)Epi::kBiasBf16) x += bf2f(ep.bias[row]);
       static_cast<bf16*>(ep.C)[(int64_t)b * args.N + row] = f2bf(x);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant__ SkinnyArgs args,
+                                                           const __grid_constant__ TcEpilogue ep, int G) {
+  pdl_trigger();
+  pdl_wait();
+  const int kbs = args.K / kBK, total = args.total_iters;
+  const int q4 = blockIdx.y;  // batch rows 4*q4 .. 4*q4+3
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int unit = x / kRows, i = x % kRows;
+  if (unit < total / kbs) fixup_columns<MODE>(args, ep, G, unit, i, q4);
+}
+
+
+// RoPE + paged KV append fix-up (decode QKV): thread = (unit, 4 batch rows,
+// pair j < 64) owns columns (d, d + hd/2) of one head, sums both over the
+// unit's contributors in k order, adds the bias, rotates q/k heads, writes q
+// to the qkv buffer and k/v into the sequence's KV page (layout of KvGeom).
+__global__ void __launch_bounds__(256) skinny_rope_fixup_kernel(const __grid_constant__ SkinnyArgs args,
+                                                                const __grid_constant__ TcEpilogue ep, int G) {
+  pdl_trigger();
+  pdl_wait();
+  const KvGeom& kv = ep.kv;
+  const int Mp = args.Mp, kbs = args.K / kBK, total = args.total_iters;
+  const int quads = Mp / 4, hd = kv.head_dim, half = hd / 2;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int unit = (int)(t / (64 * quads));
+  if (unit >= total / kbs) return;
+  const int rem = (int)(t % (64 * quads));
+  const int q4 = rem / 64, j = rem % 64;
+  const int dd = j % half;
+  const int col_a = unit * kRows + (j / half) * hd + dd, col_b = col_a + half;
+  const int c_first = cta_of((int64_t)unit * kbs, G, total);
+  const int c_last = cta_of((int64_t)(unit + 1) * kbs - 1, G, total);
+  const int64_t slot_floats = (int64_t)kRows * Mp;
+  float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
+#pragma unroll 4
+  for (int cc = c_first; cc <= c_last; ++cc) {
+    const int slot = unit == it_begin(cc, G, total) / kbs ? 0 : 1;
+    const float* src = args.partial + ((int64_t)cc * 2 + slot) * slot_floats;
+    const float4 pa = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_a - unit * kRows) * Mp) + q4);
+    const float4 pb = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_b - unit * kRows) * Mp) + q4);
+    sa.x += pa.x; sa.y += pa.y; sa.z += pa.z; sa.w += pa.w;
+    sb.x += pb.x; sb.y += pb.y; sb.z += pb.z; sb.w += pb.w;
+  }
+  const float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
+  const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
+  const int hs = col_a / hd;  // head slot in [0, H + 2KV)
+  const bool is_v = hs >= ep.heads + kv.kv_heads, is_k = !is_v && hs >= ep.heads;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = q4 * 4 + k;
+    if (b >= args.M) break;
+    const int pos = ep.pos_arr ? ep.pos_arr[b] : ep.pos0 + b;
+    float x = va[k] + bias_a, y = vb[k] + bias_b;
+    if (!is_v) {
+      const float2 c = ep.rope[(int64_t)pos * half + dd];
+      const float rx = x * c.x - y * c.y, ry = y * c.x + x * c.y;
+      x = rx;
+      y = ry;
+    }
+    if (!is_k && !is_v) {
+      bf16* q = static_cast<bf16*>(ep.C) + (int64_t)b * args.N;
+      q[col_a] = f2bf(x);
+      q[col_b] = f2bf(y);
+    } else {
+      const int seq = ep.seq_arr ? ep.seq_arr[b] : ep.seq0;
+      const int32_t page = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
+      const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
+      bf16* dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page * kv.page_size) +
+                  kv.plane(ep.layer, is_v ? 1 : 0, kvh) + (int64_t)(pos % kv.tpb) * hd;
+      dst[dd] = f2bf(x);
+      dst[dd + half] = f2bf(y);
     }
   }
 }
@@ -359,12 +428,18 @@ void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs&
   count_launch();
   launch_pdl(gemm_skinny_kernel<MODE>, dim3(grid), dim3(kThreads), (size_t)smem, st, mw, ma, a, e);
   const int kbs = a.K / kBK, units = a.total_iters / kbs;
+  if constexpr (MODE == (int)Epi::kRopeKV) {
+    const int64_t threads = (int64_t)units * 64 * (a.Mp / 4);
+    count_launch();
+    launch_pdl(skinny_rope_fixup_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, a, e, grid);
+    return;
+  }
   bool split = false;  // does any CTA boundary fall inside a unit?
   for (int c = 1; c < grid && !split; ++c) split = ((int64_t)c * a.total_iters / grid) % kbs != 0;
   if (split) {
-    const int64_t threads = (int64_t)units * kRows * (a.Mp / 4);
     count_launch();
-    launch_pdl(skinny_fixup_kernel<MODE>, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, a, e, grid);
+    launch_pdl(skinny_fixup_kernel<MODE>, dim3((unsigned)((units * kRows + 255) / 256), a.Mp / 4), dim3(256), 0, st,
+               a, e, grid);
   }
 }
 
@@ -379,7 +454,8 @@ bool gemm_skinny_enabled() {
 }
 
 bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st) {
-  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBK || K % kBK || e.mode == Epi::kRopeKV) return false;
+  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBK || K % kBK) return false;
+  if (e.mode == Epi::kRopeKV && e.kv.head_dim != 64 && e.kv.head_dim != 128) return false;  // heads tile 128 rows
   const int NB = e.mode == Epi::kSwiGLU ? 2 : 1;
   if (N % (kRows * NB)) return false;
   const int units = N / (kRows * NB), kbs = K / kBK;
@@ -394,6 +470,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   const int smem = a.stages * a.stage_bytes + 1024 + 256;
   // one CTA per SM, >= 2 k-blocks each
   const int grid = std::max(1, std::min(kNumSMs, a.total_iters / 2));
+  if (e.mode == Epi::kRopeKV && units > grid) return false;  // <= 2 segments (partial slots) per CTA
   Scratch s;
   if (!scratch_for(st, &s)) return false;
   a.partial = s.partial;
@@ -405,7 +482,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
     case Epi::kAddF32: launch_mode<2>(mw, ma, a, grid, smem, e, st); break;
     case Epi::kStoreF32: launch_mode<3>(mw, ma, a, grid, smem, e, st); break;
     case Epi::kSwiGLU: launch_mode<4>(mw, ma, a, grid, smem, e, st); break;
-    default: return false;
+    case Epi::kRopeKV: launch_mode<5>(mw, ma, a, grid, smem, e, st); break;
   }
   return true;
 }

@@ -8,6 +8,7 @@
 // event of its weights (ws_streamer_wait), so compute of resident layers
 // overlaps the copy of the rest (cluster.py:145-182).
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.h"
@@ -38,7 +39,7 @@ bool valid_cfg(const ws_model_config& c) {
   return c.layers > 0 && c.hidden > 0 && c.ffn > 0 && c.heads > 0 && c.kv_heads > 0 &&
          c.heads % c.kv_heads == 0 && (c.head_dim == 64 || c.head_dim == 96 || c.head_dim == 128) &&
          c.vocab > 0 && c.hidden % 32 == 0 && c.ffn % 128 == 0 && c.max_positions > 0 &&
-         c.heads / c.kv_heads <= 8;
+         c.heads / c.kv_heads <= 8 && c.hidden <= 8192;  // rmsnorm keeps a row in registers
 }
 
 Layout make_layout(const ws_model_config& c) {
@@ -137,8 +138,7 @@ void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
   using namespace ws;
   const ws_model_config& c = m->cfg;
   const int q = (c.heads + 2 * c.kv_heads) * c.head_dim;
-  // decode rows: the split-K skinny GEMM + rope kernel beats 128-row tiles
-  if (!(m->gemm_impl & 1) && rows >= 16 && !(rows <= 128 && ws::gemm_skinny_enabled())) {
+  if (!(m->gemm_impl & 1)) {
     TcEpilogue e;
     e.mode = Epi::kRopeKV;
     e.C = qkv;
@@ -151,7 +151,12 @@ void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
     e.pos0 = pos0;
     e.seq_arr = seqs;
     e.pos_arr = pos;
-    if (launch_gemm_tc_epi(h, w, rows, q, c.hidden, e, st)) return;
+    // a few decode rows: skinny split-K GEMM with RoPE/KV-append in its fix-up
+    // (one launch less; for more rows the plain fix-up + rope kernel is faster)
+    static const bool fuse = !(getenv("WS_FUSE_ROPE") && getenv("WS_FUSE_ROPE")[0] == '0');
+    if (fuse && rows <= 8 && launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return;
+    if (rows >= 16 && !(rows <= 128 && gemm_skinny_enabled()) && launch_gemm_tc_epi(h, w, rows, q, c.hidden, e, st))
+      return;
   }
   gemm(m, h, w, rows, q, c.hidden, b ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv, b, st);
   launch_rope_kv(qkv, m->rope, kv, layer, rows, c.heads, seqs, pos, seq0, pos0, st);
@@ -185,6 +190,14 @@ int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M,
   gemm(m, A, B, M, N, K, Epi::kStoreF32, partial, nullptr, st);
   if (int e = comm_allreduce_f32(m->comm, partial, (int64_t)M * N, st)) return e;
   launch_add_f32(x, partial, (int64_t)M * N, st);
+  return WS_OK;
+}
+
+// Row-parallel projection + residual add, then RMSNorm of the updated rows into `out`.
+int row_parallel_norm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N, int K, float* x,
+                      float* partial, const ws::bf16* norm_w, ws::bf16* out, cudaStream_t st) {
+  if (int e = row_parallel(m, A, B, M, N, K, x, partial, st)) return e;
+  ws::launch_rmsnorm(x, norm_w, out, M, N, m->cfg.rms_eps, st);
   return WS_OK;
 }
 
@@ -389,18 +402,22 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   const Layout& L = m->layout;
 
   launch_embed(tokens, W<bf16>(wts, L.embed), x, n, d, st);
+  launch_rmsnorm(x, W<bf16>(wts, L.layers[0].attn_norm), h, n, d, c.rms_eps, st);
   for (int l = 0; l < c.layers; ++l) {
     const auto& Ly = L.layers[l];
-    launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, n, d, c.rms_eps, st);
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
              pos, qkv, st);
     launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
-    if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x, partial, st)) return e;
-    launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
+    if (int e = row_parallel_norm(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x, partial, W<bf16>(wts, Ly.ffn_norm), h,
+                                  st))
+      return e;
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);
-    if (int e = row_parallel(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial, st)) return e;
+    // the residual after the FFN feeds the next layer's attn_norm (or the final norm)
+    const bool last = l + 1 == c.layers;
+    if (int e = row_parallel_norm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial,
+                                  W<bf16>(wts, last ? L.final_norm : L.layers[l + 1].attn_norm), last ? hl : h, st))
+      return e;
   }
-  launch_rmsnorm(x, W<bf16>(wts, L.final_norm), hl, n, d, c.rms_eps, st);
   if (int e = lm_head(m, hl, W<bf16>(wts, L.lm_head), n, logits, shard, gathered, next_tokens, st)) return e;
   WS_CUDA(cudaGetLastError());
   return WS_OK;
