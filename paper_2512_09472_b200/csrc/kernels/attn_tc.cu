@@ -1,15 +1,17 @@
 // tcgen05 flash-attention prefill over the paged KV pool (sm_100a).
 //
 // One CTA = 128 queries of one q head (GQA: its kv head = h / group), K/V
-// tiles of 128 keys gathered page by page. Warp roles (288 threads):
-//   warps 0-3  softmax + correction: thread r owns query row r (TMEM lane r).
-//              Reads S_j from TMEM in 32-column chunks (two passes: row max,
-//              then exp2/sum), writes P_j as bf16 into SMEM (K-major SW128),
-//              rescales the TMEM output accumulator only when the running max
-//              grows by more than 2^8 (exact: final O/l uses the same max).
-//   warps 4-7  producers: cp.async gather of Q (once) and K_j/V_j rows from
-//              the block table into SWIZZLE_128B smem tiles; completion via
-//              cp.async.mbarrier.arrive.noinc.
+// tiles of 128 keys gathered page by page. Warp roles (416 threads):
+//   warps 0-7  softmax + correction: warps w and w+4 share TMEM lanes
+//              32(w%4).. (query rows) and split the 128 key columns of S_j
+//              in halves, so two warps per SM sub-partition issue the
+//              exp2/max/sum stream. The row max is exchanged through smem
+//              each tile; P_j goes to SMEM as bf16 (K-major SW128); the TMEM
+//              output accumulator is rescaled only when the running max grows
+//              by more than 2^8 (exact: the final O/l uses the same max).
+//   warps 9-12 producers: Q (cp.async, once); K_j/V_j by TMA page-row boxes
+//              from the block table (or a cp.async gather when pages do not
+//              hold 16-token runs) into SWIZZLE_128B smem tiles.
 //   warp 8     TMEM allocator + single-thread MMA issuer:
 //              S_j = Q K_j^T   (M=128, N=128, K=hd; both operands K-major)
 //              O  += P_j V_j   (M=128, N=hd, K=128; V is MN-major — no transpose)
@@ -28,7 +30,7 @@ namespace {
 
 using namespace dev;
 
-constexpr int kRows = 128, kKeys = 128, kThreads = 288;
+constexpr int kRows = 128, kKeys = 128, kThreads = 416;
 
 #ifdef WS_ATTN_TRACE
 // debug timeline of block (0,0): [event][j] = clock64 (events: 0 S issued,
@@ -36,6 +38,13 @@ constexpr int kRows = 128, kKeys = 128, kThreads = 288;
 __device__ long long g_attn_trace[4][64];
 #define TRACE(ev, j) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) g_attn_trace[ev][j] = clock64(); } while (0)
+// per-CTA [start (after pdl_wait), end, smid] in globaltimer ns, grid order
+__device__ long long g_attn_cta[4096][3];
+__device__ __forceinline__ long long attn_gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #else
 #define TRACE(ev, j) do { } while (0)
 #endif
@@ -118,6 +127,16 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// A operand from TMEM (the P tile, 128 lanes x 8 packed columns per K=16 step)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
 // SWIZZLE_128B smem descriptor (version 1); LBO only matters for MN-major.
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo) {
   return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -149,17 +168,23 @@ __host__ __device__ constexpr uint32_t idesc(int n, bool b_mn_major) {
       "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]),          \
       "r"(v[30]), "r"(v[31]))
 
+constexpr int NS = 3;  // K and V ring stages (TMA page gathers take ~2 us; 3 tiles in flight hide them)
+
 template <int HD>
 struct Smem {
   static constexpr int kTile = kRows * HD * 2;     // Q, K or V tile: [HD/64 blocks][128 rows][128 B]
-  static constexpr int kP = kRows * kKeys * 2;     // P tile: [2 blocks][128 rows][128 B]
   static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kTile;            // 2 stages
-  static constexpr int kV = kK + 2 * kTile;        // 2 stages
-  static constexpr int kPo = kV + 2 * kTile;       // 2 buffers
-  static constexpr int kBar = kPo + 2 * kP;
+  static constexpr int kK = kQ + kTile;            // NS stages
+  static constexpr int kV = kK + NS * kTile;       // NS stages
+  static constexpr int kX = kV + NS * kTile;       // [2 halves][128 rows] fp32 row-max / row-sum exchange
+  static constexpr int kBar = kX + 2 * kRows * 4;
   static constexpr int kBytes = kBar + 256 + 1024;  // barriers + alignment slack
 };
+
+// barrier indices
+constexpr int kQFull = 0, kKFull = 1, kKEmpty = kKFull + NS, kVFull = kKEmpty + NS, kVEmpty = kVFull + NS,
+              kSFull = kVEmpty + NS, kSEmpty = kSFull + 2, kPFull = kSEmpty + 2, kPvDone = kPFull + 2,
+              kTmemSlot = kPvDone + 1;
 
 // byte offset of 16-byte chunk c (0 .. 2*HD/16-1 across the row) of row r in a
 // [blocks][128][128 B] SWIZZLE_128B tile
@@ -170,7 +195,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 template <int HD, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, KvGeom kv, int layer, int seq,
-                   int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
+                   int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap, int dbg) {
   using S = Smem<HD>;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   pdl_trigger();
@@ -179,12 +204,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t base = (raw + 1023) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);  // generic pointer to the aligned base
   const uint32_t bar = base + S::kBar;
-  // barriers: 0 q_full | 1,2 k_full | 3,4 k_empty | 5,6 v_full | 7,8 v_empty | 9,10 s_full |
-  //           11,12 s_empty | 13,14 p_full | 15,16 p_empty | 17 pv_done | TMEM base slot at +18*8
   // K_j is released right after S_j (QK^T) retires, V_j after PV_j, so the
-  // gather of K_{j+2} overlaps the softmax of tile j.
+  // gathers of K_{j+3} / V_{j+3} overlap the softmax of tile j.
   auto B = [&](int i) { return bar + 8 * i; };
-  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + S::kBar + 18 * 8);
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + S::kBar + kTmemSlot * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_qt = (rows + kRows - 1) / kRows;
@@ -199,28 +222,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ldq = (heads + 2 * kv.kv_heads) * HD;
 
   if (threadIdx.x == 0) {
-    mbar_init(B(0), 128);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(B(1 + i), TMA ? 1 : 64);  // k_full: TMA thread (expect_tx) or 64 cp.async threads
-      mbar_init(B(3 + i), 1);     // k_empty: MMA commit after S_j
-      mbar_init(B(5 + i), TMA ? 1 : 64);  // v_full
-      mbar_init(B(7 + i), 1);     // v_empty: MMA commit after PV_j
-      mbar_init(B(9 + i), 1);     // s_full: MMA commit
-      mbar_init(B(11 + i), 128);  // s_empty: softmax threads
-      mbar_init(B(13 + i), 128);  // p_full: softmax threads
-      mbar_init(B(15 + i), 1);    // p_empty: MMA commit
+    mbar_init(B(kQFull), 128);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(B(kKFull + i), TMA ? 1 : 64);  // TMA thread (expect_tx) or 64 cp.async threads
+      mbar_init(B(kKEmpty + i), 1);            // MMA commit after S_j
+      mbar_init(B(kVFull + i), TMA ? 1 : 64);
+      mbar_init(B(kVEmpty + i), 1);            // MMA commit after PV_j
     }
-    mbar_init(B(17), 1);  // pv_done: MMA commit
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(B(kSFull + i), 1);     // MMA commit
+      mbar_init(B(kSEmpty + i), 256);  // softmax threads read S
+      mbar_init(B(kPFull + i), 256);   // softmax threads wrote P (into the same TMEM columns)
+    }
+    mbar_init(B(kPvDone), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if constexpr (TMA) {
     // K/V rows a tile does not load keep stale data; start from finite zeros
-    for (int i = threadIdx.x; i < 4 * S::kTile / 16; i += kThreads)
+    for (int i = threadIdx.x; i < 2 * NS * S::kTile / 16; i += kThreads)
       reinterpret_cast<uint4*>(gbase + S::kK)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   if (warp == 8) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(bar + 18 * 8));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(B(kTmemSlot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   fence_before();
@@ -228,23 +252,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // everything above is prologue; global data from here on
+#ifdef WS_ATTN_TRACE
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0 && cta_id < 4096) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_attn_cta[cta_id][0] = attn_gtimer();
+    g_attn_cta[cta_id][2] = smid;
+  }
+#endif
 
-  if (warp >= 4 && warp < 8) {
-    // ===================== producers: warps 4-5 gather K, warps 6-7 gather V =====================
-    const int t = threadIdx.x - 128;
+  if (warp >= 9) {
+    // ===================== producers: warps 9-10 gather K, warps 11-12 gather V =====================
+    const int t = threadIdx.x - 288;
     for (int i = t; i < kRows * CH; i += 128) {
       const int r = i / CH, c = i % CH;
       const int gr = q0 + r;
       const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + h * HD + c * 8;
       cp_async16(gbase + S::kQ + swz(r, c), src, gr < rows);
     }
-    cp_async_arrive(B(0));
+    cp_async_arrive(B(kQFull));
     const bool is_v = t >= 64;
     const int u = t & 63;  // rows u and u + 64 of every tile
     const int32_t* bt = kv.block_tables + (int64_t)seq * kv.max_blocks;
     const int64_t plane = kv.plane(layer, is_v ? 1 : 0, kvh);
     const uint32_t ring = is_v ? S::kV : S::kK;
-    const int full0 = is_v ? 5 : 1, empty0 = is_v ? 7 : 3;
+    const int full0 = is_v ? kVFull : kKFull, empty0 = is_v ? kVEmpty : kKEmpty;
     if constexpr (TMA) {
       // One thread per ring issues 8-row TMA boxes (one per run of 8 tokens of
       // a page; tokens-per-block is a multiple of 8): 16 x HD/64 bulk copies
@@ -262,15 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         int y_next = row_of(0);
         for (int j = 0; j < n_kt; ++j) {
-          const int st = j & 1;
+          const int st = j % NS;
           const int y = y_next;
           if (j + 1 < n_kt) y_next = row_of(j + 1);
           const int groups = min(kKeys / 16, (n_keys - j * kKeys + 15) / 16);
           if (u == 0) {
-            mbar_wait(B(empty0 + st), ((j >> 1) & 1) ^ 1);
+            mbar_wait(B(empty0 + st), ((j / NS) & 1) ^ 1);
             tma_expect(B(full0 + st), (uint32_t)(groups * (HD / 64) * 2048));
           }
-          for (int g = 0; g < groups; ++g) {
+          const int gstep = (dbg & 1) ? 8 : 1;  // timing experiment: 128-row boxes (wrong data)
+          for (int g = 0; g < groups; g += gstep) {
             const int yg = __shfl_sync(0xffffffffu, y, g);
             if (u == 0) {
 #pragma unroll
@@ -283,8 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
     for (int j = 0; j < n_kt; ++j) {
-      const int st = j & 1;
-      mbar_wait(B(empty0 + st), ((j >> 1) & 1) ^ 1);
+      const int st = j % NS;
+      mbar_wait(B(empty0 + st), ((j / NS) & 1) ^ 1);
       uint8_t* dst = gbase + ring + st * S::kTile;
       // CH consecutive lanes cover one key row (HD*2 contiguous bytes, coalesced);
       // this thread walks rows r, r+RS, ... with its (block, slot) position
@@ -318,188 +352,455 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t id_s = idesc(kKeys, false), id_pv = idesc(HD, true);
       const uint32_t tO = tmem + 256;
-      mbar_wait(B(0), 0);
+      mbar_wait(B(kQFull), 0);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      // Event-driven issue: S_{j+1} = Q K_{j+1}^T and PV_j = P_j V_j are issued
-      // in whichever order their inputs become ready (non-blocking polls), so
-      // a late K tile never holds back the PV of the previous tile.
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T into TMEM columns [128 (j&1), +128)
+        const int ks = j % NS;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         fence_after();
-        const uint32_t qa = base + S::kQ, ka = base + S::kK + st * S::kTile;
+        const uint32_t qa = base + S::kQ, ka = base + S::kK + ks * S::kTile;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (kRows * 128) + (k & 3) * 32;
-          mma(tmem + st * 128, sdesc(qa + off, 16), sdesc(ka + off, 16), id_s, k > 0);
+          mma(tmem + (j & 1) * 128, sdesc(qa + off, 16), sdesc(ka + off, 16), id_s, k > 0);
         }
-        commit(B(9 + st));  // S_j ready
-        commit(B(3 + st));  // K stage free
+        commit(B(kSFull + (j & 1)));  // S_j ready (also: every earlier PV has retired)
+        commit(B(kKEmpty + ks));      // K stage free
       };
-      auto issue_pv = [&](int j) {
-        const int st = j & 1;
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      auto issue_pv = [&](int j) {  // O += P_j V_j, P_j bf16 in TMEM (aliasing S_j's columns)
+        const int vs = j % NS;
         fence_after();
-        const uint32_t pa = base + S::kPo + st * S::kP, va = base + S::kV + st * S::kTile;
+        const uint32_t pa = tmem + (j & 1) * 128, va = base + S::kV + vs * S::kTile;
 #pragma unroll
-        for (int k = 0; k < kKeys / 16; ++k) {
-          const uint32_t a_off = (k >> 2) * (kRows * 128) + (k & 3) * 32;
-          mma(tO, sdesc(pa + a_off, 16), sdesc(va + k * 16 * 128, kRows * 128), id_pv, (j | k) != 0);
-        }
-        commit(B(15 + st));  // P buffer free
-        commit(B(7 + st));   // V stage free
-        commit(B(17));       // O updated through tile j
+        for (int k = 0; k < kKeys / 16; ++k)  // 16 keys = 8 packed bf16x2 TMEM columns
+          mma_ts(tO, pa + k * 8, sdesc(va + k * 16 * 128, kRows * 128), id_pv, (j | k) != 0);
+        commit(B(kVEmpty + vs));  // V stage free
+        commit(B(kPvDone));       // O updated through tile j
       };
       // In-order issue with blocking (HW-suspending) waits: S_{j+1} first (its K
-      // tile is prefetched two tiles ahead, so it is normally already there),
-      // then PV_j once softmax has written P_j.
+      // tile is prefetched NS tiles ahead, so it is normally already there),
+      // then PV_j once softmax has written P_j. S_{j+2} (same TMEM columns as
+      // P_j) is issued after PV_j, and tcgen05 MMAs of one thread run in order.
       for (int j = 0; j < n_kt; ++j) {
         if (j == 0) {
-          mbar_wait(B(1), 0);
+          mbar_wait(B(kKFull), 0);
           TRACE(0, 0);
           issue_s(0);
         }
         if (j + 1 < n_kt) {
-          const int s1 = (j + 1) & 1, ph1 = ((j + 1) >> 1) & 1;
-          mbar_wait(B(1 + s1), ph1);
-          mbar_wait(B(11 + s1), ph1 ^ 1);
+          mbar_wait(B(kKFull + (j + 1) % NS), ((j + 1) / NS) & 1);
+          mbar_wait(B(kSEmpty + ((j + 1) & 1)), (((j + 1) >> 1) & 1) ^ 1);
           TRACE(0, j + 1);
           issue_s(j + 1);
         }
-        mbar_wait(B(13 + (j & 1)), (j >> 1) & 1);
-        mbar_wait(B(5 + (j & 1)), (j >> 1) & 1);
+        mbar_wait(B(kPFull + (j & 1)), (j >> 1) & 1);
+        mbar_wait(B(kVFull + j % NS), (j / NS) & 1);
         TRACE(1, j);
         issue_pv(j);
-      }
-      int ns = n_kt, npv = n_kt;  // event-driven variant below disabled
-      while (npv < n_kt) {
-        // S_ns needs K_ns and a free S buffer (softmax already read S_{ns-2}):
-        // it may run ahead of PV so the next softmax never waits on the pipe
-        if (ns < n_kt && mbar_ready(B(1 + (ns & 1)), (ns >> 1) & 1) &&
-            mbar_ready(B(11 + (ns & 1)), ((ns >> 1) & 1) ^ 1)) {
-          TRACE(0, ns);
-          issue_s(ns++);
-          continue;
-        }
-        // PV_npv needs P_npv (softmax) and V_npv
-        if (npv < ns && mbar_ready(B(13 + (npv & 1)), (npv >> 1) & 1) &&
-            mbar_ready(B(5 + (npv & 1)), (npv >> 1) & 1)) {
-          TRACE(1, npv);
-          issue_pv(npv++);
-          continue;
-        }
-        __nanosleep(64);  // back off: this warp shares an SMSP with a softmax warp
       }
     }
     __syncwarp();  // reconverge before the CTA-wide (aligned) barrier below
   } else {
-    // ===================== softmax / correction (warps 0-3) =====================
-    const int r = threadIdx.x;  // query row = TMEM lane
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // ===================== softmax / correction (warps 0-7) =====================
+    constexpr int HK = kKeys / 2;  // key columns per half
+    const int qd = warp & 3, hf = warp >> 2;
+    const int r = qd * 32 + lane;  // query row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int qpos = pos0 + q0 + r;
+    float* xch = reinterpret_cast<float*>(gbase + S::kX);  // [half][row]
+    // the two warps of a row quarter meet on named barrier 1 + qd (64 threads)
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(1 + qd) : "memory"); };
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kt; ++j) {
       const int st = j & 1;
-      mbar_wait(B(9 + st), (j >> 1) & 1);
+      mbar_wait(B(kSFull + st), (j >> 1) & 1);
       if (threadIdx.x == 0) TRACE(2, j);
       fence_after();
-      const uint32_t ts = tmem + lane_off + st * 128;
-      const int key0 = j * kKeys;
-      const bool diag = key0 + kKeys - 1 > pos0 + q0 || key0 + kKeys > n_keys;
-      // the whole 128-column row of S_j in registers: 4 loads, one wait
-      uint32_t v[kKeys];
+      const uint32_t ts = tmem + lane_off + st * 128 + hf * HK;
+      const int key0 = j * kKeys + hf * HK;
+      const bool diag = j * kKeys + kKeys - 1 > pos0 + q0 || j * kKeys + kKeys > n_keys;
+      uint32_t v[HK];
       TLD32(ts + 0, (v + 0));
       TLD32(ts + 32, (v + 32));
-      TLD32(ts + 64, (v + 64));
-      TLD32(ts + 96, (v + 96));
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       fence_before();
-      mbar_arrive(B(11 + st));  // S[st] consumed: the next QK^T may overwrite it
-      float mx = -INFINITY;
+      mbar_arrive(B(kSEmpty + st));  // S[st] read: S_{j+2} may be issued (it runs after PV_j)
+      // row max over raw scores (scale > 0 commutes with max), 8 independent chains
+      float m8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
       if (diag) {
 #pragma unroll
-        for (int i = 0; i < kKeys; ++i) {
+        for (int i = 0; i < HK; ++i) {
           const int key = key0 + i;
-          const float x = (key > qpos || key >= n_keys) ? -INFINITY : __uint_as_float(v[i]) * scale_log2;
-          v[i] = __float_as_uint(x);
-          mx = fmaxf(mx, x);
+          if (key > qpos || key >= n_keys) v[i] = __float_as_uint(-INFINITY);
+          m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < kKeys; ++i) {
-          const float x = __uint_as_float(v[i]) * scale_log2;
-          v[i] = __float_as_uint(x);
-          mx = fmaxf(mx, x);
-        }
+        for (int i = 0; i < HK; ++i) m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
       }
-      // lazy rescale: move the reference max only when it grows by > 8 (log2)
+      const float mh = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      xch[hf * kRows + r] = mh;
+      pair_sync();
+      const float mx = fmaxf(mh, xch[(hf ^ 1) * kRows + r]) * scale_log2;
+      pair_sync();  // both halves read before either overwrites its slot next tile
+      // lazy rescale: move the reference max only when it grows by > 8 (log2);
+      // both halves see the same mx, so they agree on m_used and alpha
       float alpha = 1.f;
       if (mx > m_used + 8.f) {
         alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
         m_used = mx;
       }
       const float mref = m_used == -INFINITY ? 0.f : m_used;
-      // the P buffer of tile j was last read by PV_{j-2}
-      if (j >= 2) mbar_wait(B(15 + st), ((j >> 1) & 1) ^ 1);
-      uint8_t* prow = gbase + S::kPo + st * S::kP;
-      float sum = 0.f;
+      // P_j (bf16 pairs) overwrites this half's 32 TMEM columns of S_j's
+      // buffer: both halves have loaded S_j (the max exchange above), and
+      // PV_{j-2}, the last reader of these columns, retired before S_j landed.
+      float s8[8];
 #pragma unroll
-      for (int q = 0; q < kKeys / 8; ++q) {  // 8 keys per 16-byte chunk
-        float p[8];
+      for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+      uint32_t pk[HK / 2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          p[i] = fast_exp2(__uint_as_float(v[8 * q + i]) - mref);  // exp2(-inf) = 0 for masked keys
-          sum += p[i];
-        }
-        *reinterpret_cast<uint4*>(prow + swz(r, q)) =
-            make_uint4(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]), pack_bf16x2(p[4], p[5]),
-                       pack_bf16x2(p[6], p[7]));
+      for (int i = 0; i < HK; i += 2) {
+        // exp2(s * scale - mref): one FFMA + one MUFU; masked keys give exp2(-inf) = 0
+        const float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), scale_log2, -mref));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), scale_log2, -mref));
+        s8[i & 7] += p0;
+        s8[(i + 1) & 7] += p1;
+        pk[i / 2] = pack_bf16x2(p0, p1);
       }
-      l = l * alpha + sum;
+      TST32(tmem + lane_off + st * 128 + hf * (HK / 2), pk);
+      l = l * alpha + (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7])));
       // Wait for PV_{j-1} every iteration (keeps this waiter at most one phase
-      // behind pv_done, so parity waits stay unambiguous), then rescale O if
-      // the reference max moved: O holds P_0..P_{j-1} V.
+      // behind pv_done, so parity waits stay unambiguous), then rescale this
+      // half's O columns if the reference max moved: O holds P_0..P_{j-1} V.
       if (j > 0) {
-        mbar_wait(B(17), (j - 1) & 1);
+        mbar_wait(B(kPvDone), (j - 1) & 1);
         fence_after();
       }
       // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY lane
       // of the warp needs it (the others multiply by 1)
       if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t v[32];
-          TLD32(tmem + lane_off + 256 + c * 32, v);
+        for (int c = 0; c < HD / 64; ++c) {
+          uint32_t o[32];
+          const uint32_t to = tmem + lane_off + 256 + hf * (HD / 2) + c * 32;
+          TLD32(to, o);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          TST32(tmem + lane_off + 256 + c * 32, v);
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          TST32(to, o);
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // P (and any O rescale) in TMEM
       fence_before();
-      mbar_arrive(B(13 + st));
+      mbar_arrive(B(kPFull + st));
       if (threadIdx.x == 0) TRACE(3, j);
     }
-    // epilogue: O / l -> bf16
-    mbar_wait(B(17), (n_kt - 1) & 1);
+    // epilogue: O / (l_0 + l_1) -> bf16, each half writes its HD/2 columns
+    xch[hf * kRows + r] = l;
+    pair_sync();
+    const float lt = l + xch[(hf ^ 1) * kRows + r];
+    mbar_wait(B(kPvDone), (n_kt - 1) & 1);
+    fence_after();
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    const int grow = q0 + r;
+#pragma unroll 1
+    for (int c = 0; c < HD / 64; ++c) {
+      uint32_t o[32];
+      TLD32(tmem + lane_off + 256 + hf * (HD / 2) + c * 32, o);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (grow < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + h * HD + hf * (HD / 2) + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+#ifdef WS_ATTN_TRACE
+  if (threadIdx.x == 0 && cta_id < 4096) g_attn_cta[cta_id][1] = attn_gtimer();
+#endif
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
+// Two q heads of one GQA group per CTA (even group sizes, TMA page gathers):
+// tiles A and B are the same 128 query positions of heads h0 and h0 + 1, so
+// every K_j / V_j tile gathered from the pool feeds 256 query rows — half the
+// TMA boxes per MMA of the one-head kernel. TMEM: S_A [0,128) S_B [128,256)
+// O_A [256, 256+HD) O_B [256+HD, 256+2HD); P_X (bf16) overwrites S_X in place
+// and PV reads it from TMEM. The MMA warp ping-pongs the tiles —
+//   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+// — so softmax A(j+1) overlaps PV_B(j) / S_B(j+1) and softmax B(j) overlaps
+// PV_A(j) / S_A(j+1): the exp2 stream of one tile hides under the tensor work
+// of the other. Warps 0-3 = softmax A, 4-7 = softmax B (thread = query row),
+// warp 8 = TMEM alloc + MMA issue, warps 9-12 = producers.
+namespace pair2 {
+constexpr int NS2 = 2;
+// 12 warps: 3 per SM sub-partition, so each thread may hold 168 registers
+// (the softmax row of S_j is 128 of them)
+constexpr int kThreads2 = 384;
+template <int HD>
+struct Smem {
+  static constexpr int kTile = kRows * HD * 2;
+  static constexpr int kQ = 0;                      // Q_A, Q_B
+  static constexpr int kK = kQ + 2 * kTile;         // NS2 stages
+  static constexpr int kV = kK + NS2 * kTile;       // NS2 stages
+  static constexpr int kBar = kV + NS2 * kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+constexpr int kQFull = 0, kKFull = 1, kKEmpty = kKFull + NS2, kVFull = kKEmpty + NS2, kVEmpty = kVFull + NS2,
+              kSFull = kVEmpty + NS2, kPFull = kSFull + 2, kPvDone = kPFull + 2, kTmemSlot = kPvDone + 2;
+}  // namespace pair2
+
+template <int HD>
+__global__ void __launch_bounds__(pair2::kThreads2, 1)
+    attn_tc2_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, KvGeom kv, int layer, int seq, int rows,
+                    int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
+  using pair2::NS2;
+  using S = pair2::Smem<HD>;
+  constexpr int CH = HD / 8;
+  pdl_trigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t bar = base + S::kBar;
+  auto B = [&](int i) { return bar + 8 * i; };
+  volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + S::kBar + pair2::kTmemSlot * 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (rows + kRows - 1) / kRows;
+  const int qt = n_qt - 1 - blockIdx.y;  // heaviest query tiles first
+  const int h0 = 2 * blockIdx.x;
+  const int kvh = h0 / (heads / kv.kv_heads);
+  const int q0 = qt * kRows;
+  const int n_keys = pos0 + min(rows, q0 + kRows);
+  const int n_kt = (n_keys + kKeys - 1) / kKeys;
+  const int ldq = (heads + 2 * kv.kv_heads) * HD;
+
+  if (threadIdx.x == 0) {
+    mbar_init(B(pair2::kQFull), 96);
+    for (int i = 0; i < NS2; ++i) {
+      mbar_init(B(pair2::kKFull + i), 1);
+      mbar_init(B(pair2::kKEmpty + i), 1);
+      mbar_init(B(pair2::kVFull + i), 1);
+      mbar_init(B(pair2::kVEmpty + i), 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(B(pair2::kSFull + x), 1);
+      mbar_init(B(pair2::kPFull + x), 128);
+      mbar_init(B(pair2::kPvDone + x), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // K/V rows a tile does not load keep stale data; start from finite zeros
+  for (int i = threadIdx.x; i < 2 * NS2 * S::kTile / 16; i += pair2::kThreads2)
+    reinterpret_cast<uint4*>(gbase + S::kK)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(B(pair2::kTmemSlot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp >= 9) {
+    // ===================== producers =====================
+    const int t = threadIdx.x - 288;
+    for (int i = t; i < 2 * kRows * CH; i += 96) {  // Q of both heads
+      const int x = i / (kRows * CH), r = (i / CH) % kRows, c = i % CH;
+      const int gr = q0 + r;
+      const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + (h0 + x) * HD + c * 8;
+      cp_async16(gbase + S::kQ + x * S::kTile + swz(r, c), src, gr < rows);
+    }
+    cp_async_arrive(B(pair2::kQFull));
+    const bool is_v = warp == 10;
+    const int u = lane;
+    if (warp < 11) {  // warp 9 gathers K, warp 10 gathers V
+      const int32_t* bt = kv.block_tables + (int64_t)seq * kv.max_blocks;
+      const int64_t plane = kv.plane(layer, is_v ? 1 : 0, kvh);
+      const uint32_t ring = is_v ? S::kV : S::kK;
+      const int full0 = is_v ? pair2::kVFull : pair2::kKFull, empty0 = is_v ? pair2::kVEmpty : pair2::kKEmpty;
+      const int rows_pp = (int)(kv.page_size / (HD * 2));
+      const int plane_rows = (int)(plane / HD);
+      auto row_of = [&](int j) {  // lane g: page row of key group g (16 tokens) of tile j
+        const int key0 = j * kKeys + (u & 7) * 16;
+        const int blk = key0 / kv.tpb, slot = key0 - blk * kv.tpb;
+        return key0 < n_keys ? bt[blk] * rows_pp + plane_rows + slot : 0;
+      };
+      int y_next = row_of(0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % NS2;
+        const int y = y_next;
+        if (j + 1 < n_kt) y_next = row_of(j + 1);
+        const int groups = min(kKeys / 16, (n_keys - j * kKeys + 15) / 16);
+        if (u == 0) {
+          mbar_wait(B(empty0 + st), ((j / NS2) & 1) ^ 1);
+          tma_expect(B(full0 + st), (uint32_t)(groups * (HD / 64) * 2048));
+        }
+        for (int g = 0; g < groups; ++g) {
+          const int yg = __shfl_sync(0xffffffffu, y, g);
+          if (u == 0) {
+#pragma unroll
+            for (int hh = 0; hh < HD / 64; ++hh)
+              tma_load_2d(base + ring + st * S::kTile + hh * (kRows * 128) + g * 2048, &kvmap, B(full0 + st),
+                          hh * 64, yg);
+          }
+        }
+      }
+    }
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc(kKeys, false), id_pv = idesc(HD, true);
+      mbar_wait(B(pair2::kQFull), 0);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      auto issue_s = [&](int x, int j) {  // S_x = Q_x K_j^T
+        fence_after();
+        const uint32_t qa = base + S::kQ + x * S::kTile, ka = base + S::kK + (j % NS2) * S::kTile;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * (kRows * 128) + (k & 3) * 32;
+          mma(tmem + x * 128, sdesc(qa + off, 16), sdesc(ka + off, 16), id_s, k > 0);
+        }
+        commit(B(pair2::kSFull + x));
+      };
+      auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j (P_x bf16 in S_x's TMEM columns)
+        fence_after();
+        const uint32_t pa = tmem + x * 128, va = base + S::kV + (j % NS2) * S::kTile;
+        const uint32_t to = tmem + 256 + x * HD;
+#pragma unroll
+        for (int k = 0; k < kKeys / 16; ++k)
+          mma_ts(to, pa + k * 8, sdesc(va + k * 16 * 128, kRows * 128), id_pv, (j | k) != 0);
+        commit(B(pair2::kPvDone + x));
+      };
+      mbar_wait(B(pair2::kKFull), 0);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      commit(B(pair2::kKEmpty));
+      for (int j = 0; j < n_kt; ++j) {
+        const bool more = j + 1 < n_kt;
+        mbar_wait(B(pair2::kVFull + j % NS2), (j / NS2) & 1);
+        mbar_wait(B(pair2::kPFull + 0), j & 1);
+        issue_pv(0, j);
+        if (more) {
+          mbar_wait(B(pair2::kKFull + (j + 1) % NS2), ((j + 1) / NS2) & 1);
+          issue_s(0, j + 1);  // after PV_A(j) in the same in-order pipe: P_A(j) is read first
+        }
+        mbar_wait(B(pair2::kPFull + 1), j & 1);
+        issue_pv(1, j);
+        commit(B(pair2::kVEmpty + j % NS2));
+        if (more) {
+          issue_s(1, j + 1);
+          commit(B(pair2::kKEmpty + (j + 1) % NS2));
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== softmax (warps 0-3: tile A, 4-7: tile B) =====================
+    const int x = warp >> 2, qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const uint32_t tS = tmem + lane_off + x * 128, tO = tmem + lane_off + 256 + x * HD;
+    const int qpos = pos0 + q0 + r;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(B(pair2::kSFull + x), j & 1);
+      fence_after();
+      const int key0 = j * kKeys;
+      const bool diag = key0 + kKeys - 1 > pos0 + q0 || key0 + kKeys > n_keys;
+      uint32_t v[kKeys];
+      TLD32(tS + 0, (v + 0));
+      TLD32(tS + 32, (v + 32));
+      TLD32(tS + 64, (v + 64));
+      TLD32(tS + 96, (v + 96));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      float m8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < kKeys; ++i) {
+          const int key = key0 + i;
+          if (key > qpos || key >= n_keys) v[i] = __float_as_uint(-INFINITY);
+          m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kKeys; ++i) m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
+      float alpha = 1.f;
+      if (mx > m_used + 8.f) {  // lazy rescale (exact: O/l share the reference max)
+        alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
+        m_used = mx;
+      }
+      const float mref = m_used == -INFINITY ? 0.f : m_used;
+      float s8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < kKeys; i += 2) {  // P packed in place: v[i/2] = bf16x2(p_i, p_{i+1})
+        const float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), scale_log2, -mref));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), scale_log2, -mref));
+        s8[i & 7] += p0;
+        s8[(i + 1) & 7] += p1;
+        v[i / 2] = pack_bf16x2(p0, p1);
+      }
+      l = l * alpha + (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7])));
+      // P_j overwrites S_j's first 64 columns (this thread's row only)
+      TST32(tS + 0, (v + 0));
+      TST32(tS + 32, (v + 32));
+      if (j > 0) {  // O_x holds P_0..P_{j-1} V once PV_x(j-1) retired
+        mbar_wait(B(pair2::kPvDone + x), (j - 1) & 1);
+        fence_after();
+      }
+      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          TLD32(tO + c * 32, o);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          TST32(tO + c * 32, o);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      fence_before();
+      mbar_arrive(B(pair2::kPFull + x));
+    }
+    mbar_wait(B(pair2::kPvDone + x), (n_kt - 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const int grow = q0 + r;
 #pragma unroll 1
     for (int c = 0; c < HD / 32; ++c) {
-      uint32_t v[32];
-      TLD32(tmem + lane_off + 256 + c * 32, v);
+      uint32_t o[32];
+      TLD32(tO + c * 32, o);
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       if (grow < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + h * HD + c * 32);
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + (h0 + x) * HD + c * 32);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          dst[q] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * q]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
-                              pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
+          dst[q] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+                              pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
       }
     }
   }
@@ -511,16 +812,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // 2D view of the page window as rows of HD bf16 (one token of one K or V
 // plane per row), 8-row x 64-column boxes with 128B swizzle.
-bool window_map(CUtensorMap* map, const KvGeom& kv, int hd) {
+bool window_map(CUtensorMap* map, const KvGeom& kv, int hd, int box_rows = 16) {
   const Driver* d = driver();
   if (!d) return false;
   cuuint64_t dims[2] = {(cuuint64_t)hd, (cuuint64_t)(kv.n_pages * kv.page_size / (hd * 2))};
   cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
-  cuuint32_t box[2] = {64, 16};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.window, dims, strides, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int attn_dbg() {
+  static const int v = getenv("WS_ATTN_DBG") ? atoi(getenv("WS_ATTN_DBG")) : 0;
+  return v;
 }
 
 template <int HD, bool TMA>
@@ -534,7 +840,7 @@ void launch_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int se
   dim3 grid(heads, (rows + kRows - 1) / kRows);
   count_launch();
   launch_pdl(attn_tc_kernel<HD, TMA>, dim3(grid), dim3(kThreads), Smem<HD>::kBytes, st, qkv, out, kv, layer, seq, rows, pos0, heads,
-                                                                    scale * 1.4426950408889634f, map);
+                                                                    scale * 1.4426950408889634f, map, attn_dbg());
 }
 
 template <int HD>
@@ -546,11 +852,23 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
   static int64_t map_pages = 0;
   bool tma = kv.tpb % 16 == 0 && kv.page_size % (HD * 2) == 0;
   if (tma && (map_window != kv.window || map_pages != kv.n_pages)) {
-    tma = window_map(&map, kv, HD);
+    tma = window_map(&map, kv, HD, (attn_dbg() & 1) ? 128 : 16);
     map_window = tma ? kv.window : nullptr;
     map_pages = tma ? kv.n_pages : 0;
   }
-  if (tma)
+  static const bool pair_heads = !(getenv("WS_ATTN_PAIR") && getenv("WS_ATTN_PAIR")[0] == '0');
+  if (tma && pair_heads && (heads / kv.kv_heads) % 2 == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           pair2::Smem<HD>::kBytes);
+      attr = true;
+    }
+    count_launch();
+    launch_pdl(attn_tc2_kernel<HD>, dim3(heads / 2, (rows + kRows - 1) / kRows), dim3(pair2::kThreads2),
+               pair2::Smem<HD>::kBytes, st, qkv, out, kv, layer, seq, rows, pos0, heads, scale * 1.4426950408889634f,
+               map);
+  } else if (tma)
     launch_impl<HD, true>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, map, st);
   else
     launch_impl<HD, false>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, map, st);
@@ -562,6 +880,10 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
 extern "C" int ws_attn_trace(long long* out) {
   cudaDeviceSynchronize();
   return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess ? 0 : 6;
+}
+extern "C" int ws_attn_cta_trace(long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_attn_cta, sizeof(g_attn_cta)) == cudaSuccess ? 0 : 6;
 }
 #endif
 

@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int P_BM = 128, P_BN = 256, P_BNH = 128, P_STAGES = 6;
 constexpr int P_A_BYTES = P_BM * BK * 2, P_B_BYTES = P_BNH * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_STG_BYTES = 4 * 2 * 4096;  // epilogue staging: 2 x (32 rows x 128 B) per epilogue warp
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + P_STG_BYTES + 1024 + 256;
 constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(P_BN >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
 
@@ -387,15 +388,180 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// ---- coalesced epilogue: TMEM -> registers -> swizzled smem box -> TMA ----
+// The tcgen05.ld 32x32b shape gives each thread one accumulator row, so direct
+// global stores from registers touch 32 lines per warp instruction (one per
+// row). Instead each epilogue warp writes its 32 rows x 128 B into a
+// SWIZZLE_128B staging box (16-byte chunk j of row r at chunk j ^ (r & 7):
+// conflict-free) and one lane issues a TMA store — or a TMA reduce-add for the
+// fp32 residual, so x += acc is a single coalesced async op per 32x32 box.
+// Two boxes per warp alternate; a box is rewritten only after the TMA engine
+// has read it (bulk wait_group.read 1).
+__device__ __forceinline__ void stage_f32(uint32_t buf, int lane, const uint32_t* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(buf + lane * 128 + ((j ^ (lane & 7)) << 4)),
+                 "r"(v[4 * j]), "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                 : "memory");
+}
+// 32 bf16 values = chunks [4 * half, 4 * half + 4) of this lane's 128 B row
+__device__ __forceinline__ void stage_bf16(uint32_t buf, int lane, int half, const float* f) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(buf + lane * 128 + (((half * 4 + j) ^ (lane & 7)) << 4)),
+                 "r"(pack_bf16x2(f[8 * j], f[8 * j + 1])), "r"(pack_bf16x2(f[8 * j + 2], f[8 * j + 3])),
+                 "r"(pack_bf16x2(f[8 * j + 4], f[8 * j + 5])), "r"(pack_bf16x2(f[8 * j + 6], f[8 * j + 7]))
+                 : "memory");
+}
+
+struct Stager {
+  uint32_t base;  // this warp's two 4 KB boxes
+  int lane, b = 0;
+  __device__ uint32_t acquire() {  // a box the TMA engine has finished reading
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+    __syncwarp();
+    return base + b * 4096;
+  }
+  // make the generic-proxy smem writes visible to TMA, then store/reduce the box at (x, y)
+  template <bool ADD>
+  __device__ void issue(const CUtensorMap* map, int x, int y) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    const uint32_t src = base + b * 4096;
+    if (lane == 0) {
+      if constexpr (ADD)
+        asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+                     "r"(x), "r"(y), "r"(src)
+                     : "memory");
+      else
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+                     "r"(x), "r"(y), "r"(src)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    b ^= 1;
+  }
+  __device__ void drain() {  // all issued TMA stores complete (global writes done)
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+  }
+};
+
+// One 128-row x 256-column accumulator (this warp: rows row0..row0+31) through
+// the staging boxes.
+template <int MODE>
+__device__ __forceinline__ void epilogue_tile_tma(const TcEpilogue& ep, const CUtensorMap* map_c, Stager& st,
+                                                  uint32_t tacc, int row0, int n0) {
+  const int lane = st.lane;
+  if constexpr (MODE == (int)Epi::kAddF32 || MODE == (int)Epi::kStoreF32) {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v[32];
+      TMEM_LD32(tacc + c * 32, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      stage_f32(st.acquire(), lane, v);
+      st.issue<MODE == (int)Epi::kAddF32>(map_c, n0 + c * 32, row0);
+    }
+  } else if constexpr (MODE == (int)Epi::kSwiGLU) {
+    // tile columns [0,128) = gate block, [128,256) = matching up block -> 128 output columns
+#pragma unroll 1
+    for (int c = 0; c < 4; c += 2) {
+      const uint32_t buf = st.acquire();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t g[32], u[32];
+        TMEM_LD32(tacc + (c + h) * 32, g);
+        TMEM_LD32(tacc + 128 + (c + h) * 32, u);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = __uint_as_float(g[j]);
+          f[j] = x / (1.f + __expf(-x)) * __uint_as_float(u[j]);
+        }
+        stage_bf16(buf, lane, h, f);
+      }
+      st.issue<false>(map_c, n0 / 2 + c * 32, row0);
+    }
+  } else {  // kStoreBf16 / kBiasBf16: 64 columns per box
+#pragma unroll 1
+    for (int c = 0; c < 8; c += 2) {
+      const uint32_t buf = st.acquire();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[32];
+        TMEM_LD32(tacc + (c + h) * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        if constexpr (MODE == (int)Epi::kBiasBf16) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += bf2f(ep.bias[n0 + (c + h) * 32 + j]);
+        }
+        stage_bf16(buf, lane, h, f);
+      }
+      st.issue<false>(map_c, n0 + c * 32, row0);
+    }
+  }
+}
+
+// Work schedule of the pair kernel: units go round-robin to the pairs, so
+// all pairs run the same k-range of neighbouring tiles at the same time and
+// each weight block is read from HBM once (L2 reuse). A unit is a whole tile
+// (splits = 1) or, for the fp32 residual epilogue (x += A.B^T, the O and down
+// projections), one of `splits` k-slices of a tile: unit u = (slice u / tiles,
+// tile u % tiles). Splitting turns a partial last wave (128 tiles on 74 pairs
+// = 1.73 waves run as 2) into several short ones (512 slices = 6.92 waves).
+// Slices of a tile reduce-add into x in slice order: slice q waits until
+// flags[tile] says slice q-1 has landed — one fixed summation order, so
+// results are deterministic. Slice q-1 sits `tiles` units earlier (more than
+// one wave), so the wait is almost never taken, and a pair only ever waits
+// on an earlier unit: no deadlock while all pairs are resident.
+struct SkParams {
+  int splits;
+  uint32_t* flags;  // [tiles][2 ranks]: epoch * 16 + slices of this CTA's rows landed
+  uint32_t epoch;
+  int dbg;  // WS_SK_DBG bits (timing experiments): 1 = no wait, 4 = rotate k order, 8 = trace
+};
+
+struct TileIter {
+  int u, step, units, tiles, splits, KB;
+  __device__ TileIter(int pair, int n_pairs, int tiles_, int splits_, int kb)
+      : u(pair), step(n_pairs), units(tiles_ * splits_), tiles(tiles_), splits(splits_), KB(kb) {}
+  __device__ bool next(int& tile, int& q, int& kb0, int& kb1) {
+    if (u >= units) return false;
+    tile = u % tiles;
+    q = u / tiles;
+    kb0 = q * KB / splits;
+    kb1 = (q + 1) * KB / splits;
+    u += step;
+    return true;
+  }
+};
+
+// WS_SK_DBG bit 8: per-CTA globaltimer trace [cta][0 start, 1-3 segment
+// accumulators ready, 4-6 segment epilogues done, 7 end] (tools/gemm_trace.py)
+__device__ long long g_gemm_trace[148][8];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                    int N, int K, const __grid_constant__ TcEpilogue ep) {
+                    int N, int K, const __grid_constant__ TcEpilogue ep, const __grid_constant__ SkParams sk,
+                    const __grid_constant__ CUtensorMap map_c) {
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
-  const uint32_t bars = base + P_STAGES * P_STAGE_BYTES;
+  const uint32_t stg = base + P_STAGES * P_STAGE_BYTES;  // 1024-aligned staging boxes
+  const uint32_t bars = stg + P_STG_BYTES;
   auto full = [&](int s) { return bars + 8 * s; };
   auto empty = [&](int s) { return bars + 8 * (P_STAGES + s); };
   auto tfull = [&](int b) { return bars + 8 * (2 * P_STAGES + b); };
@@ -413,6 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map_c) : "memory");
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < P_STAGES; ++s) {
@@ -436,13 +603,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot_ptr;
   pdl_wait();  // everything above is prologue; global data from here on
 
+  int tile, sq, kb0, kb1;
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < tiles; t += n_pairs) {
-        const int m0 = (t % m_blocks) * 256 + rank * P_BM, n0 = (t / m_blocks) * P_BN + rank * P_BNH;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+      TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
+      while (it.next(tile, sq, kb0, kb1)) {
+        const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN + rank * P_BNH;
+        const int rot = (sk.dbg & 4) ? (pair * 17) % (kb1 - kb0) : 0;
+        for (int i = kb0; i < kb1; ++i) {
+          const int kb = kb0 + (i - kb0 + rot) % (kb1 - kb0);
           mbar_wait(empty(stage), phase ^ 1);
           const uint32_t sa = base + stage * P_STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(full(stage), 2 * P_STAGE_BYTES);  // both CTAs' bytes
@@ -471,11 +642,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < tiles; t += n_pairs) {
+      TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
+      while (it.next(tile, sq, kb0, kb1)) {
         mbar_wait(tempty(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * P_BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int i = kb0; i < kb1; ++i) {
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * P_STAGE_BYTES;
@@ -485,7 +657,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2), "r"((uint32_t)((kb | k) != 0)));
+                "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2),
+                "r"((uint32_t)(i != kb0 || k != 0)));
           asm volatile(
               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
                   empty(stage)),
@@ -510,15 +683,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;
-    int acc = 0;
+    const int r_in = q * 32 + lane;  // this thread's row inside the CTA's 128
+    const bool tr = (sk.dbg & 8) && r_in == 0;
+    Stager st{stg + (uint32_t)q * 8192, lane};
+    if (tr) g_gemm_trace[blockIdx.x][0] = gtimer();
+    int acc = 0, seg = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < tiles; t += n_pairs) {
-      const int m0 = (t % m_blocks) * 256 + rank * P_BM, n0 = (t / m_blocks) * P_BN;
+    TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
+    while (it.next(tile, sq, kb0, kb1)) {
+      const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN;
       mbar_wait(tfull(acc), acc_phase);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
-      epilogue_tile<MODE>(ep, tmem + ((uint32_t)(q * 32) << 16) + acc * P_BN, row < M ? row : -1, n0, N,
-                          ep.kv.head_dim);
+      if (tr && seg < 3) g_gemm_trace[blockIdx.x][1 + seg] = gtimer();
+      const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * P_BN;
+      const int row0 = m0 + q * 32;
+      if constexpr (MODE == (int)Epi::kAddF32) {
+        if (sk.splits > 1) {
+          // k-slice sq of this tile: reduce-add after slice sq-1 has landed
+          const uint32_t* f = sk.flags + tile * 2 + rank;  // this CTA's 128 rows of the tile
+          if (sq > 0 && r_in == 0 && !(sk.dbg & 1)) {
+            uint32_t v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+            } while (v != sk.epoch * 16 + sq);
+          }
+          epi_bar();
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        }
+      }
+      if constexpr (MODE == (int)Epi::kRopeKV) {
+        const int row = m0 + r_in;
+        epilogue_tile<MODE>(ep, tacc, row < M ? row : -1, n0, N, ep.kv.head_dim);
+      } else {
+        epilogue_tile_tma<MODE>(ep, &map_c, st, tacc, row0, n0);
+      }
       tc_fence_before();
       // release this accumulator to the leader's MMA thread (remote arrive)
       asm volatile(
@@ -529,8 +727,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if constexpr (MODE == (int)Epi::kAddF32) {
+        if (sk.splits > 1 && sq + 1 < sk.splits) {
+          // publish: this CTA's 128 rows of slice sq are in x
+          st.drain();
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          __threadfence();
+          epi_bar();
+          if (r_in == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk.flags + tile * 2 + rank),
+                         "r"(sk.epoch * 16 + sq + 1)
+                         : "memory");
+        }
+      }
+      if (tr && seg < 3) g_gemm_trace[blockIdx.x][4 + seg] = gtimer();
+      ++seg;
     }
+    st.drain();  // staging smem must outlive the TMA reads
   }
+  if ((sk.dbg & 8) && threadIdx.x == 128) g_gemm_trace[blockIdx.x][7] = gtimer();
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -549,6 +764,21 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) 
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Epilogue store map: row-major [rows, cols] of `elem` bytes, 32-row boxes of
+// 128 B (32 fp32 or 64 bf16), SWIZZLE_128B to match the staging layout.
+bool make_out_map(CUtensorMap* map, const void* ptr, int rows, int cols, int elem) {
+  const Driver* d = driver();
+  if (!d || ((uintptr_t)ptr & 15) || (cols * elem) % 16) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * elem};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem), 32};
+  cuuint32_t estr[2] = {1, 1};
+  return d->cuTensorMapEncodeTiled(map, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                   2, const_cast<void*>(ptr), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -574,8 +804,61 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
   launch_pdl(gemm_tc_kernel<MODE>, dim3(grid), dim3(THREADS), SMEM_BYTES, st, ma, mb, M, N, K, e);
 }
 
+// Per-device slice counters of the split schedule (one per tile).
+struct SkScratch {
+  uint32_t* flags = nullptr;
+  uint32_t epoch = 0;
+};
+constexpr int kMaxSplitTiles = 4096;
+
+bool sk_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WS_STREAMK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Slices per tile for the residual (x += A.B^T) GEMMs: the split with the best
+// wave efficiency units / (waves * pairs), at least 8 k-blocks per slice so a
+// slice's mainloop still hides the previous slice's epilogue.
+SkParams sk_schedule(int mode, int tiles, int n_pairs, int k_blocks) {
+  SkParams p{};
+  p.splits = 1;
+  p.dbg = getenv("WS_SK_DBG") ? atoi(getenv("WS_SK_DBG")) : 0;
+  if (!sk_enabled() || mode != (int)Epi::kAddF32 || tiles > kMaxSplitTiles || tiles % n_pairs == 0) return p;
+  double best = (double)tiles / (double)(((tiles + n_pairs - 1) / n_pairs) * n_pairs);
+  int best_s = 1;
+  for (int s = 2; s <= 8 && k_blocks / s >= 8; ++s) {
+    const int units = tiles * s;
+    const double eff = (double)units / (double)(((units + n_pairs - 1) / n_pairs) * n_pairs);
+    if (eff > best + 0.01) {
+      best = eff;
+      best_s = s;
+    }
+  }
+  if (best_s == 1) return p;
+  static SkScratch scratch[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SkScratch& sc = scratch[dev & 15];
+  if (!sc.flags) {
+    if (cudaMalloc(&sc.flags, 2 * kMaxSplitTiles * sizeof(uint32_t)) != cudaSuccess) return p;
+    cudaMemset(sc.flags, 0, 2 * kMaxSplitTiles * sizeof(uint32_t));
+  }
+  // a counter left by an earlier launch is below epoch * 16 (splits < 16)
+  if (++sc.epoch >= (1u << 27)) {
+    cudaMemset(sc.flags, 0, 2 * kMaxSplitTiles * sizeof(uint32_t));
+    sc.epoch = 1;
+  }
+  p.splits = best_s;
+  p.flags = sc.flags;
+  p.epoch = sc.epoch;
+  return p;
+}
+
 template <int MODE>
-void launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
+bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
                   cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
@@ -583,9 +866,19 @@ void launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
     attr = true;
   }
   const int tiles = ((M + 255) / 256) * (N / P_BN);
-  const int grid = 2 * (tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+  const int n_pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+  CUtensorMap mc = ma;  // RoPE mode stores directly; the map is unused there
+  if constexpr (MODE == (int)Epi::kAddF32 || MODE == (int)Epi::kStoreF32) {
+    if (!make_out_map(&mc, e.C, M, N, 4)) return false;
+  } else if constexpr (MODE == (int)Epi::kSwiGLU) {
+    if (!make_out_map(&mc, e.C, M, N / 2, 2)) return false;
+  } else if constexpr (MODE != (int)Epi::kRopeKV) {
+    if (!make_out_map(&mc, e.C, M, N, 2)) return false;
+  }
+  const SkParams sk = sk_schedule(MODE, tiles, n_pairs, K / BK);
   count_launch();
-  launch_pdl(gemm_tc2_kernel<MODE>, dim3(grid), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e);
+  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, sk, mc);
+  return true;
 }
 
 int g_pair_mode = -1;  // -1: unset (env WS_GEMM_PAIR, default on), 0 off, 1 on
@@ -605,14 +898,14 @@ bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const
   if (use_pair(M)) {
     if (!make_map(&ma, A, M, K, P_BM) || !make_map(&mb, B, N, K, P_BNH)) return false;
     switch (e.mode) {
-      case Epi::kStoreBf16: launch_mode2<0>(ma, mb, M, N, K, e, st); break;
-      case Epi::kBiasBf16: launch_mode2<1>(ma, mb, M, N, K, e, st); break;
-      case Epi::kAddF32: launch_mode2<2>(ma, mb, M, N, K, e, st); break;
-      case Epi::kStoreF32: launch_mode2<3>(ma, mb, M, N, K, e, st); break;
-      case Epi::kSwiGLU: launch_mode2<4>(ma, mb, M, N, K, e, st); break;
-      case Epi::kRopeKV: launch_mode2<5>(ma, mb, M, N, K, e, st); break;
+      case Epi::kStoreBf16: return launch_mode2<0>(ma, mb, M, N, K, e, st);
+      case Epi::kBiasBf16: return launch_mode2<1>(ma, mb, M, N, K, e, st);
+      case Epi::kAddF32: return launch_mode2<2>(ma, mb, M, N, K, e, st);
+      case Epi::kStoreF32: return launch_mode2<3>(ma, mb, M, N, K, e, st);
+      case Epi::kSwiGLU: return launch_mode2<4>(ma, mb, M, N, K, e, st);
+      case Epi::kRopeKV: return launch_mode2<5>(ma, mb, M, N, K, e, st);
     }
-    return true;
+    return false;
   }
   if (!make_map(&ma, A, M, K, BM) || !make_map(&mb, B, N, K, BN)) return false;
   switch (e.mode) {
@@ -637,3 +930,7 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, 
 }
 
 }  // namespace ws
+
+extern "C" int ws_gemm_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, ws::g_gemm_trace, sizeof(ws::g_gemm_trace)) == cudaSuccess ? 0 : 6;
+}

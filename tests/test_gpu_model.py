@@ -361,3 +361,71 @@ def test_decode_gqa_shapes_match_oracle(lib, shape, lens):
         w.release()
     finally:
         w.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 4096, 4096), (2048, 4096, 14336), (2048, 6144, 4096), (1000, 28672, 4096),
+                                   (700, 19200, 512)])
+def test_gemm_pair_split_deterministic(lib, M, N, K):
+    """Pair-kernel shapes whose 256x256 tile count is not a multiple of the 74
+    SM pairs: the residual epilogue (x += A.B^T) runs k-sliced tiles whose
+    slices reduce-add into x in slice order (TMA reduce, flag-ordered), the
+    other epilogues store through the TMA staging boxes. Every epilogue
+    against fp32; reruns are bit-identical."""
+    import ctypes as C
+
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    ref = A.float() @ B.float().T
+
+    def run(epi, out):
+        lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, epi,
+                 C.c_void_p(out.data_ptr()), None, 3, None)
+        torch.cuda.synchronize()
+
+    f1, f2 = torch.empty(M, N, device="cuda"), torch.empty(M, N, device="cuda")
+    run(3, f1)
+    run(3, f2)
+    assert _rel(f1, ref) < 1e-4  # fp32 accumulation-order noise at K = 14336
+    assert torch.equal(f1, f2)
+    base = torch.randn(M, N, device="cuda", generator=g)
+    x1, x2 = base.clone(), base.clone()
+    run(2, x1)
+    run(2, x2)
+    assert _rel(x1, base + ref) < 1e-4
+    assert torch.equal(x1, x2)
+    act = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    run(4, act)
+    assert _rel(act.float(), _swiglu_ref(A, B)) < 1e-2
+
+
+def test_wide_prefill_matches_oracle(lib):
+    """Llama-3-8B layer widths (d 4096, 32/8 heads, ffn 14336), 2 layers, 1024
+    tokens: pair-kernel GEMMs with the fused RoPE/KV-append and SwiGLU
+    epilogues and k-sliced residual GEMMs; logits against the fp32 oracle and
+    a decode step over the KV they appended."""
+    from paper_2512_09472_b200 import models as M
+
+    cfg = M.TINY.with_(name="wide", hidden=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336, layers=2,
+                       vocab=4096)
+    w, host = _worker(cfg, pool_pages=640)
+    try:
+        weights = O.unpack(cfg, cfg.layout(), host.clone())
+        w.prewarm(cfg.name, layers=cfg.layers)
+        w.switch_memory(cfg.name)
+        prompt = _prompt(cfg, 5, 1024)
+        s = w.open_seq(1024 + 4)
+        w.prefill(s, prompt.cuda())
+        got = w.logits[: cfg.vocab].float().cpu()
+        ref, past = O.forward(cfg, weights, prompt.long())
+        assert _rel(got, ref[-1]) < LOGIT_RTOL
+        tok = int(ref[-1].argmax())
+        logits, _ = w.decode(torch.tensor([s], dtype=torch.int32, device="cuda"),
+                             torch.tensor([1024], dtype=torch.int32, device="cuda"),
+                             torch.tensor([tok], dtype=torch.int32, device="cuda"), 1025)
+        ref2, _ = O.forward(cfg, weights, [tok], pos0=1024, past=past)
+        assert _rel(logits[0].float().cpu(), ref2[0]) < LOGIT_RTOL
+        w.close_seq(s)
+        w.release()
+    finally:
+        w.close()

@@ -35,3 +35,20 @@ if __name__ == "__main__":
     names = ["S issued", "PV issued", "softmax got S", "softmax P done"]
     for e in range(4):
         print(f"{names[e]:16s}", " ".join(f"{(x - t0) if x else -1:7d}" for x in t[e]))
+    cta = (C.c_longlong * (4096 * 3))()
+    N.lib.ws_attn_cta_trace(cta)
+    rows = [(cta[i * 3], cta[i * 3 + 1], cta[i * 3 + 2]) for i in range(32 * 16)]
+    g0 = min(r[0] for r in rows)
+    ends = sorted((r[1] - g0) / 1e3 for r in rows)
+    print(f"CTAs: last end {ends[-1]:.1f} us; median end {ends[len(ends) // 2]:.1f}")
+    per_sm = {}
+    for (a, b, sm) in rows:
+        per_sm.setdefault(sm, []).append(((a - g0) / 1e3, (b - g0) / 1e3))
+    busy = sorted(sum(b - a for a, b in v) for v in per_sm.values())
+    last = sorted(max(b for a, b in v) for v in per_sm.values())
+    print(f"SMs used {len(per_sm)}; busy us min {busy[0]:.1f} med {busy[len(busy)//2]:.1f} max {busy[-1]:.1f}; "
+          f"last end min {last[0]:.1f} max {last[-1]:.1f}")
+    for qt in range(16):
+        durs = [(rows[qt * 32 + h][1] - rows[qt * 32 + h][0]) / 1e3 for h in range(32)]
+        st = [(rows[qt * 32 + h][0] - g0) / 1e3 for h in range(32)]
+        print(f"grid row {qt:2d} (q tile {15 - qt:2d}): start {min(st):6.1f}-{max(st):6.1f} dur {min(durs):5.1f}-{max(durs):5.1f} us")
