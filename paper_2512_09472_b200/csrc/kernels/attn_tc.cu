@@ -35,7 +35,7 @@ constexpr int kRows = 128, kKeys = 128, kThreads = 416;
 #ifdef WS_ATTN_TRACE
 // debug timeline of block (0,0): [event][j] = clock64 (events: 0 S issued,
 // 1 PV issued, 2 softmax got S, 3 softmax released P)
-__device__ long long g_attn_trace[4][64];
+__device__ long long g_attn_trace[8][64];
 #define TRACE(ev, j) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) g_attn_trace[ev][j] = clock64(); } while (0)
 // per-CTA [start (after pdl_wait), end, smid] in globaltimer ns, grid order
@@ -531,20 +531,70 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+// ---- packed fp32 helpers (sm_100 FFMA2 / FADD2 / 3-input FMNMX) and a
+// polynomial exp2 on the FMA pipe: a share of the softmax exponentials skip
+// the MUFU unit, which is the softmax's throughput limit (FA4's trick).
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair: x = n + f, n = round(x), f in [-0.5, 0.5]; 2^f by a cubic
+// (max rel. error 7.7e-5, far below bf16's 3.9e-3 for P); 2^n added to the
+// exponent field. x is clamped at -125 (2^-125 ~ 0 next to the row sum >= 1).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  const float2 xf = up2(x);
+  const uint64_t xm = pk2(fmaxf(xf.x, -125.f), fmaxf(xf.y, -125.f));
+  const uint64_t t = fadd2(xm, pk2(12582912.f, 12582912.f));  // 1.5 * 2^23: rounds to an integer
+  const uint64_t n = fadd2(t, pk2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(n, pk2(-1.f, -1.f), xm);
+  uint64_t p = ffma2(f, pk2(0.05508868f, 0.05508868f), pk2(0.24260405f, 0.24260405f));
+  p = ffma2(p, f, pk2(0.69327624f, 0.69327624f));
+  p = ffma2(p, f, pk2(0.99992894f, 0.99992894f));
+  const float2 tf = up2(t), pf = up2(p);
+  return pk2(__uint_as_float(__float_as_uint(pf.x) + (__float_as_uint(tf.x) << 23)),
+             __uint_as_float(__float_as_uint(pf.y) + (__float_as_uint(tf.y) << 23)));
+}
+
 // ---------------------------------------------------------------------------
-// Two q heads of one GQA group per CTA (even group sizes, TMA page gathers):
-// tiles A and B are the same 128 query positions of heads h0 and h0 + 1, so
-// every K_j / V_j tile gathered from the pool feeds 256 query rows — half the
-// TMA boxes per MMA of the one-head kernel. TMEM: S_A [0,128) S_B [128,256)
-// O_A [256, 256+HD) O_B [256+HD, 256+2HD); P_X (bf16) overwrites S_X in place
-// and PV reads it from TMEM. The MMA warp ping-pongs the tiles —
-//   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
-// — so softmax A(j+1) overlaps PV_B(j) / S_B(j+1) and softmax B(j) overlaps
-// PV_A(j) / S_A(j+1): the exp2 stream of one tile hides under the tensor work
-// of the other. Warps 0-3 = softmax A, 4-7 = softmax B (thread = query row),
-// warp 8 = TMEM alloc + MMA issue, warps 9-12 = producers.
+// Persistent attention, two q heads of one GQA group per work item (even
+// group sizes, TMA page gathers). An item = the same 128 query positions of
+// heads h0 and h0 + 1 (tiles A and B), so every K_j / V_j tile gathered from
+// the pool feeds 256 query rows. Items run heaviest first (latest query tile)
+// and are dealt to the resident CTAs in a snake order (round r: CTA c takes
+// item r*G + c, or r*G + G-1-c on odd rounds), which balances the causal
+// triangle like LPT without atomics. Across items nothing drains: the K/V
+// rings keep streaming, the next item's Q is loaded as soon as the last QK^T
+// of the current one retired, and its first QK^T runs while the softmax warps
+// still store the previous output.
+// TMEM: S_A [0,128) S_B [128,256) O_A [256, 256+HD) O_B [256+HD, 256+2HD);
+// P_X (bf16) overwrites S_X in place and PV reads it from TMEM. The MMA warp
+// ping-pongs the tiles — PV_A(j), S_A(j+1), PV_B(j), S_B(j+1) — so the exp2
+// stream of one tile runs under the tensor work of the other.
+// Warps 0-3 softmax A, 4-7 softmax B (thread = query row), 8 TMEM alloc + MMA
+// issue, 9 K gather, 10 V gather, 11 Q loads.
 namespace pair2 {
-constexpr int NS2 = 2;
+constexpr int NSK = 3, NSV = 2;  // K tiles are needed a full softmax earlier than V tiles
 // 12 warps: 3 per SM sub-partition, so each thread may hold 168 registers
 // (the softmax row of S_j is 128 of them)
 constexpr int kThreads2 = 384;
@@ -552,20 +602,36 @@ template <int HD>
 struct Smem {
   static constexpr int kTile = kRows * HD * 2;
   static constexpr int kQ = 0;                      // Q_A, Q_B
-  static constexpr int kK = kQ + 2 * kTile;         // NS2 stages
-  static constexpr int kV = kK + NS2 * kTile;       // NS2 stages
-  static constexpr int kBar = kV + NS2 * kTile;
+  static constexpr int kK = kQ + 2 * kTile;         // NSK stages
+  static constexpr int kV = kK + NSK * kTile;       // NSV stages
+  static constexpr int kBar = kV + NSV * kTile;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
-constexpr int kQFull = 0, kKFull = 1, kKEmpty = kKFull + NS2, kVFull = kKEmpty + NS2, kVEmpty = kVFull + NS2,
-              kSFull = kVEmpty + NS2, kPFull = kSFull + 2, kPvDone = kPFull + 2, kTmemSlot = kPvDone + 2;
+constexpr int kQFull = 0, kQEmpty = 2, kKFull = 4, kKEmpty = kKFull + NSK, kVFull = kKEmpty + NSK,
+              kVEmpty = kVFull + NSV, kSFull = kVEmpty + NSV, kPFull = kSFull + 2, kPvDone = kPFull + 2,
+              kOFree = kPvDone + 2, kTmemSlot = kOFree + 2;
+
+struct Item {
+  int qt, h0, q0, n_keys, n_kt;
+};
+__device__ __forceinline__ bool item_of(int r, int c, int G, int n_items, int n_hp, int n_qt, int rows, int pos0,
+                                        Item& it) {
+  const int i = r * G + ((r & 1) ? G - 1 - c : c);
+  if (i >= n_items) return false;
+  it.qt = n_qt - 1 - i / n_hp;
+  it.h0 = 2 * (i % n_hp);
+  it.q0 = it.qt * kRows;
+  it.n_keys = pos0 + min(rows, it.q0 + kRows);
+  it.n_kt = (it.n_keys + kKeys - 1) / kKeys;
+  return true;
+}
 }  // namespace pair2
 
 template <int HD>
 __global__ void __launch_bounds__(pair2::kThreads2, 1)
     attn_tc2_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, KvGeom kv, int layer, int seq, int rows,
                     int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
-  using pair2::NS2;
+  using namespace pair2;
   using S = pair2::Smem<HD>;
   constexpr int CH = HD / 8;
   pdl_trigger();
@@ -578,20 +644,21 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
   volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + S::kBar + pair2::kTmemSlot * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_qt = (rows + kRows - 1) / kRows;
-  const int qt = n_qt - 1 - blockIdx.y;  // heaviest query tiles first
-  const int h0 = 2 * blockIdx.x;
-  const int kvh = h0 / (heads / kv.kv_heads);
-  const int q0 = qt * kRows;
-  const int n_keys = pos0 + min(rows, q0 + kRows);
-  const int n_kt = (n_keys + kKeys - 1) / kKeys;
+  const int n_qt = (rows + kRows - 1) / kRows, n_hp = heads / 2, n_items = n_qt * n_hp;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int group = heads / kv.kv_heads;
   const int ldq = (heads + 2 * kv.kv_heads) * HD;
 
   if (threadIdx.x == 0) {
-    mbar_init(B(pair2::kQFull), 96);
-    for (int i = 0; i < NS2; ++i) {
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(B(pair2::kQFull + x), 32);
+      mbar_init(B(pair2::kQEmpty + x), 1);
+    }
+    for (int i = 0; i < NSK; ++i) {
       mbar_init(B(pair2::kKFull + i), 1);
       mbar_init(B(pair2::kKEmpty + i), 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
       mbar_init(B(pair2::kVFull + i), 1);
       mbar_init(B(pair2::kVEmpty + i), 1);
     }
@@ -599,11 +666,12 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
       mbar_init(B(pair2::kSFull + x), 1);
       mbar_init(B(pair2::kPFull + x), 128);
       mbar_init(B(pair2::kPvDone + x), 1);
+      mbar_init(B(pair2::kOFree + x), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // K/V rows a tile does not load keep stale data; start from finite zeros
-  for (int i = threadIdx.x; i < 2 * NS2 * S::kTile / 16; i += pair2::kThreads2)
+  // K/V rows a tile does not load keep stale (finite) data; start from zeros
+  for (int i = threadIdx.x; i < (NSK + NSV) * S::kTile / 16; i += pair2::kThreads2)
     reinterpret_cast<uint4*>(gbase + S::kK)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (warp == 8) {
@@ -615,47 +683,56 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
+  if (threadIdx.x == 0) TRACE(0, 0);  // CTA start (after the PDL wait)
 
-  if (warp >= 9) {
-    // ===================== producers =====================
-    const int t = threadIdx.x - 288;
-    for (int i = t; i < 2 * kRows * CH; i += 96) {  // Q of both heads
-      const int x = i / (kRows * CH), r = (i / CH) % kRows, c = i % CH;
-      const int gr = q0 + r;
-      const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + (h0 + x) * HD + c * 8;
-      cp_async16(gbase + S::kQ + x * S::kTile + swz(r, c), src, gr < rows);
+  Item it;
+  if (warp == 11) {
+    // ===================== Q loads (one warp) =====================
+    for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
+      for (int x = 0; x < 2; ++x) {
+        // Q_x is free once the previous item's last QK^T on tile x retired
+        if (r > 0) mbar_wait(B(pair2::kQEmpty + x), (r - 1) & 1);
+        for (int i = lane; i < kRows * CH; i += 32) {
+          const int rr = i / CH, cc = i % CH;
+          const int gr = it.q0 + rr;
+          const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + (it.h0 + x) * HD + cc * 8;
+          cp_async16(gbase + S::kQ + x * S::kTile + swz(rr, cc), src, gr < rows);
+        }
+        cp_async_arrive(B(pair2::kQFull + x));
+      }
     }
-    cp_async_arrive(B(pair2::kQFull));
+  } else if (warp == 9 || warp == 10) {
+    // ===================== K (warp 9) / V (warp 10) page gathers =====================
     const bool is_v = warp == 10;
-    const int u = lane;
-    if (warp < 11) {  // warp 9 gathers K, warp 10 gathers V
-      const int32_t* bt = kv.block_tables + (int64_t)seq * kv.max_blocks;
-      const int64_t plane = kv.plane(layer, is_v ? 1 : 0, kvh);
-      const uint32_t ring = is_v ? S::kV : S::kK;
-      const int full0 = is_v ? pair2::kVFull : pair2::kKFull, empty0 = is_v ? pair2::kVEmpty : pair2::kKEmpty;
-      const int rows_pp = (int)(kv.page_size / (HD * 2));
-      const int plane_rows = (int)(plane / HD);
-      auto row_of = [&](int j) {  // lane g: page row of key group g (16 tokens) of tile j
-        const int key0 = j * kKeys + (u & 7) * 16;
+    const int32_t* bt = kv.block_tables + (int64_t)seq * kv.max_blocks;
+    const uint32_t ring = is_v ? S::kV : S::kK;
+    const int full0 = is_v ? pair2::kVFull : pair2::kKFull, empty0 = is_v ? pair2::kVEmpty : pair2::kKEmpty;
+    const int rows_pp = (int)(kv.page_size / (HD * 2));
+    const int ns = is_v ? NSV : NSK;
+    int g = 0;  // tiles issued so far (ring position)
+    for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
+      const int plane_rows = (int)(kv.plane(layer, is_v ? 1 : 0, it.h0 / group) / HD);
+      auto row_of = [&](int j) {  // lane u: page row of key group u (16 tokens) of tile j
+        const int key0 = j * kKeys + (lane & 7) * 16;
         const int blk = key0 / kv.tpb, slot = key0 - blk * kv.tpb;
-        return key0 < n_keys ? bt[blk] * rows_pp + plane_rows + slot : 0;
+        return key0 < it.n_keys ? bt[blk] * rows_pp + plane_rows + slot : 0;
       };
       int y_next = row_of(0);
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % NS2;
+      for (int j = 0; j < it.n_kt; ++j, ++g) {
+        const int st = g % ns;
         const int y = y_next;
-        if (j + 1 < n_kt) y_next = row_of(j + 1);
-        const int groups = min(kKeys / 16, (n_keys - j * kKeys + 15) / 16);
-        if (u == 0) {
-          mbar_wait(B(empty0 + st), ((j / NS2) & 1) ^ 1);
+        if (j + 1 < it.n_kt) y_next = row_of(j + 1);
+        const int groups = min(kKeys / 16, (it.n_keys - j * kKeys + 15) / 16);
+        if (lane == 0) {
+          mbar_wait(B(empty0 + st), ((g / ns) & 1) ^ 1);
           tma_expect(B(full0 + st), (uint32_t)(groups * (HD / 64) * 2048));
         }
-        for (int g = 0; g < groups; ++g) {
-          const int yg = __shfl_sync(0xffffffffu, y, g);
-          if (u == 0) {
+        for (int gg = 0; gg < groups; ++gg) {
+          const int yg = __shfl_sync(0xffffffffu, y, gg);
+          if (lane == 0) {
 #pragma unroll
             for (int hh = 0; hh < HD / 64; ++hh)
-              tma_load_2d(base + ring + st * S::kTile + hh * (kRows * 128) + g * 2048, &kvmap, B(full0 + st),
+              tma_load_2d(base + ring + st * S::kTile + hh * (kRows * 128) + gg * 2048, &kvmap, B(full0 + st),
                           hh * 64, yg);
           }
         }
@@ -665,11 +742,9 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
     // ===================== MMA issuer =====================
     if (lane == 0) {
       constexpr uint32_t id_s = idesc(kKeys, false), id_pv = idesc(HD, true);
-      mbar_wait(B(pair2::kQFull), 0);
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      auto issue_s = [&](int x, int j) {  // S_x = Q_x K_j^T
+      auto issue_s = [&](int x, int kt) {  // S_x = Q_x K^T (K ring tile kt)
         fence_after();
-        const uint32_t qa = base + S::kQ + x * S::kTile, ka = base + S::kK + (j % NS2) * S::kTile;
+        const uint32_t qa = base + S::kQ + x * S::kTile, ka = base + S::kK + (kt % NSK) * S::kTile;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (kRows * 128) + (k & 3) * 32;
@@ -677,126 +752,162 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         }
         commit(B(pair2::kSFull + x));
       };
-      auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j (P_x bf16 in S_x's TMEM columns)
+      auto issue_pv = [&](int x, int kt, bool first) {  // O_x += P_x V (P_x bf16 in S_x's TMEM columns)
         fence_after();
-        const uint32_t pa = tmem + x * 128, va = base + S::kV + (j % NS2) * S::kTile;
+        const uint32_t pa = tmem + x * 128, va = base + S::kV + (kt % NSV) * S::kTile;
         const uint32_t to = tmem + 256 + x * HD;
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k)
-          mma_ts(to, pa + k * 8, sdesc(va + k * 16 * 128, kRows * 128), id_pv, (j | k) != 0);
+          mma_ts(to, pa + k * 8, sdesc(va + k * 16 * 128, kRows * 128), id_pv, (!first || k != 0) ? 1u : 0u);
         commit(B(pair2::kPvDone + x));
       };
-      mbar_wait(B(pair2::kKFull), 0);
-      issue_s(0, 0);
-      issue_s(1, 0);
-      commit(B(pair2::kKEmpty));
-      for (int j = 0; j < n_kt; ++j) {
-        const bool more = j + 1 < n_kt;
-        mbar_wait(B(pair2::kVFull + j % NS2), (j / NS2) & 1);
-        mbar_wait(B(pair2::kPFull + 0), j & 1);
-        issue_pv(0, j);
-        if (more) {
-          mbar_wait(B(pair2::kKFull + (j + 1) % NS2), ((j + 1) / NS2) & 1);
-          issue_s(0, j + 1);  // after PV_A(j) in the same in-order pipe: P_A(j) is read first
-        }
-        mbar_wait(B(pair2::kPFull + 1), j & 1);
-        issue_pv(1, j);
-        commit(B(pair2::kVEmpty + j % NS2));
-        if (more) {
-          issue_s(1, j + 1);
-          commit(B(pair2::kKEmpty + (j + 1) % NS2));
+      int g = 0;  // global tile counter (ring position and per-step barrier parity)
+      for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
+        const bool single = it.n_kt == 1;
+        mbar_wait(B(pair2::kKFull + g % NSK), (g / NSK) & 1);
+        if (r == 0) TRACE(2, 63);
+        // S_X(0) may overwrite the previous item's P_X: its PV was issued earlier (in-order pipe)
+        mbar_wait(B(pair2::kQFull + 0), r & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue_s(0, g);
+        if (single) commit(B(pair2::kQEmpty + 0));
+        mbar_wait(B(pair2::kQFull + 1), r & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue_s(1, g);
+        if (single) commit(B(pair2::kQEmpty + 1));
+        commit(B(pair2::kKEmpty + g % NSK));
+        for (int j = 0; j < it.n_kt; ++j, ++g) {
+          const bool more = j + 1 < it.n_kt;
+          mbar_wait(B(pair2::kVFull + g % NSV), (g / NSV) & 1);
+          mbar_wait(B(pair2::kPFull + 0), g & 1);
+          if (j == 0 && r > 0) mbar_wait(B(pair2::kOFree + 0), (r - 1) & 1);  // previous O_A read out
+          if (r == 0) TRACE(1, j);
+          issue_pv(0, g, j == 0);
+          if (more) {
+            mbar_wait(B(pair2::kKFull + (g + 1) % NSK), ((g + 1) / NSK) & 1);
+            if (r == 0) TRACE(0, j + 1);
+            issue_s(0, g + 1);  // after PV_A(j) in the same in-order pipe: P_A(j) is read first
+            if (j + 2 == it.n_kt) commit(B(pair2::kQEmpty + 0));  // last QK^T of tile A: Q_A free
+          }
+          mbar_wait(B(pair2::kPFull + 1), g & 1);
+          if (j == 0 && r > 0) mbar_wait(B(pair2::kOFree + 1), (r - 1) & 1);
+          issue_pv(1, g, j == 0);
+          commit(B(pair2::kVEmpty + g % NSV));
+          if (more) {
+            issue_s(1, g + 1);
+            if (j + 2 == it.n_kt) commit(B(pair2::kQEmpty + 1));
+            commit(B(pair2::kKEmpty + (g + 1) % NSK));
+          }
         }
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < 8) {
     // ===================== softmax (warps 0-3: tile A, 4-7: tile B) =====================
     const int x = warp >> 2, qd = warp & 3;
-    const int r = qd * 32 + lane;
+    const int rl = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const uint32_t tS = tmem + lane_off + x * 128, tO = tmem + lane_off + 256 + x * HD;
-    const int qpos = pos0 + q0 + r;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(B(pair2::kSFull + x), j & 1);
-      fence_after();
-      const int key0 = j * kKeys;
-      const bool diag = key0 + kKeys - 1 > pos0 + q0 || key0 + kKeys > n_keys;
-      uint32_t v[kKeys];
-      TLD32(tS + 0, (v + 0));
-      TLD32(tS + 32, (v + 32));
-      TLD32(tS + 64, (v + 64));
-      TLD32(tS + 96, (v + 96));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      float m8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
-      if (diag) {
-#pragma unroll
-        for (int i = 0; i < kKeys; ++i) {
-          const int key = key0 + i;
-          if (key > qpos || key >= n_keys) v[i] = __float_as_uint(-INFINITY);
-          m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < kKeys; ++i) m8[i & 7] = fmaxf(m8[i & 7], __uint_as_float(v[i]));
-      }
-      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * scale_log2;
-      float alpha = 1.f;
-      if (mx > m_used + 8.f) {  // lazy rescale (exact: O/l share the reference max)
-        alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
-        m_used = mx;
-      }
-      const float mref = m_used == -INFINITY ? 0.f : m_used;
-      float s8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s8[i] = 0.f;
-#pragma unroll
-      for (int i = 0; i < kKeys; i += 2) {  // P packed in place: v[i/2] = bf16x2(p_i, p_{i+1})
-        const float p0 = fast_exp2(fmaf(__uint_as_float(v[i]), scale_log2, -mref));
-        const float p1 = fast_exp2(fmaf(__uint_as_float(v[i + 1]), scale_log2, -mref));
-        s8[i & 7] += p0;
-        s8[(i + 1) & 7] += p1;
-        v[i / 2] = pack_bf16x2(p0, p1);
-      }
-      l = l * alpha + (((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7])));
-      // P_j overwrites S_j's first 64 columns (this thread's row only)
-      TST32(tS + 0, (v + 0));
-      TST32(tS + 32, (v + 32));
-      if (j > 0) {  // O_x holds P_0..P_{j-1} V once PV_x(j-1) retired
-        mbar_wait(B(pair2::kPvDone + x), (j - 1) & 1);
+    int g = 0;
+    for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
+      const int qpos = pos0 + it.q0 + rl;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < it.n_kt; ++j, ++g) {
+        mbar_wait(B(pair2::kSFull + x), g & 1);
+        if (threadIdx.x == 0 && r == 0) TRACE(2, j);
         fence_after();
-      }
-      if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
-#pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t o[32];
-          TLD32(tO + c * 32, o);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int key0 = j * kKeys;
+        const bool diag = key0 + kKeys - 1 > pos0 + it.q0 || key0 + kKeys > it.n_keys;
+        uint32_t v[kKeys];
+        TLD32(tS + 0, (v + 0));
+        TLD32(tS + 32, (v + 32));
+        TLD32(tS + 64, (v + 64));
+        TLD32(tS + 96, (v + 96));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (threadIdx.x == 0 && r == 0) TRACE(4, j);
+        if (diag) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          TST32(tO + c * 32, o);
+          for (int i = 0; i < kKeys; ++i)
+            if (key0 + i > qpos || key0 + i >= it.n_keys) v[i] = __float_as_uint(-INFINITY);
         }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-      fence_before();
-      mbar_arrive(B(pair2::kPFull + x));
-    }
-    mbar_wait(B(pair2::kPvDone + x), (n_kt - 1) & 1);
-    fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const int grow = q0 + r;
-#pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      TLD32(tO + c * 32, o);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (grow < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + (h0 + x) * HD + c * 32);
+        // row max over raw scores (scale > 0 commutes with max): 3-input max, 4 chains
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int i = 0; i < kKeys; i += 8) {
+          m0 = fmax3(m0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          m1 = fmax3(m1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+          m2 = fmax3(m2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+          m3 = fmax3(m3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+        }
+        const float mx = fmax3(m0, m1, fmaxf(m2, m3)) * scale_log2;
+        float alpha = 1.f;
+        if (mx > m_used + 8.f) {  // lazy rescale (exact: O/l share the reference max)
+          alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
+          m_used = mx;
+        }
+        const float mref = m_used == -INFINITY ? 0.f : m_used;
+        if (threadIdx.x == 0 && r == 0) TRACE(5, j);
+        // p = exp2(s * scale - mref) two at a time (FFMA2); 3 of every 8 pairs on
+        // the FMA-pipe polynomial, the rest on MUFU; P packed in place as bf16x2
+        const uint64_t sc2 = pk2(scale_log2, scale_log2), nm2 = pk2(-mref, -mref);
+        uint64_t s2[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s2[i] = 0;
+#pragma unroll
+        for (int q = 0; q < kKeys / 2; ++q) {
+          const uint64_t x2 = ffma2(pk2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1])), sc2, nm2);
+          uint64_t p2;
+          if ((q & 7) < 3) {
+            p2 = exp2_poly2(x2);
+          } else {
+            const float2 xf = up2(x2);
+            p2 = pk2(fast_exp2(xf.x), fast_exp2(xf.y));
+          }
+          s2[q & 3] = fadd2(s2[q & 3], p2);
+          const float2 pf = up2(p2);
+          v[q] = pack_bf16x2(pf.x, pf.y);
+        }
+        const float2 sa = up2(fadd2(fadd2(s2[0], s2[1]), fadd2(s2[2], s2[3])));
+        l = l * alpha + (sa.x + sa.y);
+        if (threadIdx.x == 0 && r == 0) TRACE(6, j);
+        TST32(tS + 0, (v + 0));  // P_j overwrites S_j's first 64 columns (this thread's row)
+        TST32(tS + 32, (v + 32));
+        if (j > 0) {  // O_x holds P_0..P_{j-1} V once PV_x(j-1) retired
+          mbar_wait(B(pair2::kPvDone + x), (g - 1) & 1);
+          fence_after();
+        }
+        if (threadIdx.x == 0 && r == 0) TRACE(7, j);
+        if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
+#pragma unroll 1
+          for (int cc = 0; cc < HD / 32; ++cc) {
+            uint32_t o[32];
+            TLD32(tO + cc * 32, o);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            TST32(tO + cc * 32, o);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        fence_before();
+        mbar_arrive(B(pair2::kPFull + x));
+        if (threadIdx.x == 0 && r == 0) TRACE(3, j);
+      }
+      // epilogue: O_x / l -> bf16 rows of head h0 + x; O_x is released as soon as it is in registers
+      mbar_wait(B(pair2::kPvDone + x), (g - 1) & 1);
+      fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint32_t o[HD];
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) TLD32(tO + cc * 32, (o + cc * 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      fence_before();
+      mbar_arrive(B(pair2::kOFree + x));
+      const int grow = it.q0 + rl;
+      if (grow < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + (it.h0 + x) * HD);
+#pragma unroll
+        for (int q = 0; q < HD / 8; ++q)
           dst[q] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
                               pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
                               pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
@@ -807,6 +918,12 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
   fence_before();
   __syncthreads();
   fence_after();
+  if (threadIdx.x == 0) TRACE(1, 63);  // CTA done
+#ifdef WS_ATTN_TRACE
+  if (threadIdx.x == 0 && c < 4096) {
+    g_attn_cta[c][1] = attn_gtimer();
+  }
+#endif
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
@@ -865,7 +982,8 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
       attr = true;
     }
     count_launch();
-    launch_pdl(attn_tc2_kernel<HD>, dim3(heads / 2, (rows + kRows - 1) / kRows), dim3(pair2::kThreads2),
+    const int items = (heads / 2) * ((rows + kRows - 1) / kRows);
+    launch_pdl(attn_tc2_kernel<HD>, dim3(items < kNumSMs ? items : kNumSMs), dim3(pair2::kThreads2),
                pair2::Smem<HD>::kBytes, st, qkv, out, kv, layer, seq, rows, pos0, heads, scale * 1.4426950408889634f,
                map);
   } else if (tma)
