@@ -264,18 +264,29 @@ __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEp
   float4 sum[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) sum[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-  for (int cc = c_first; cc <= c_last; ++cc) {  // k order
-    const int slot = unit == it_begin(cc, G, total) / kbs ? 0 : 1;
-    const float* src = args.partial + ((int64_t)cc * 2 + slot) * slot_floats;
+  // contributors in k order, 8 at a time: their loads are all in flight
+  // before the (ordered) adds, so the tail costs one L2 round trip, not one per contributor
+  for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+    float4 p[8][NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const float4 p = __ldcg(reinterpret_cast<const float4*>(src + ((int64_t)j * kRows + i) * Mp) + q4);
-      sum[j].x += p.x;
-      sum[j].y += p.y;
-      sum[j].z += p.z;
-      sum[j].w += p.w;
+    for (int k = 0; k < 8; ++k) {
+      const int cc = c0 + k;
+      const int slot = cc <= c_last && unit == it_begin(cc, G, total) / kbs ? 0 : 1;
+      const float* src = args.partial + ((int64_t)(cc <= c_last ? cc : c_last) * 2 + slot) * slot_floats;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        p[k][j] = cc <= c_last ? __ldcg(reinterpret_cast<const float4*>(src + ((int64_t)j * kRows + i) * Mp) + q4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        sum[j].x += p[k][j].x;
+        sum[j].y += p[k][j].y;
+        sum[j].z += p[k][j].z;
+        sum[j].w += p[k][j].w;
+      }
   }
   float v[4] = {sum[0].x, sum[0].y, sum[0].z, sum[0].w};
   if constexpr (NB == 2) {
@@ -337,14 +348,24 @@ __global__ void __launch_bounds__(256) skinny_rope_fixup_kernel(const __grid_con
   const int c_last = cta_of((int64_t)(unit + 1) * kbs - 1, G, total);
   const int64_t slot_floats = (int64_t)kRows * Mp;
   float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
-#pragma unroll 4
-  for (int cc = c_first; cc <= c_last; ++cc) {
-    const int slot = unit == it_begin(cc, G, total) / kbs ? 0 : 1;
-    const float* src = args.partial + ((int64_t)cc * 2 + slot) * slot_floats;
-    const float4 pa = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_a - unit * kRows) * Mp) + q4);
-    const float4 pb = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_b - unit * kRows) * Mp) + q4);
-    sa.x += pa.x; sa.y += pa.y; sa.z += pa.z; sa.w += pa.w;
-    sb.x += pb.x; sb.y += pb.y; sb.z += pb.z; sb.w += pb.w;
+  for (int c0 = c_first; c0 <= c_last; c0 += 8) {  // loads of 8 contributors in flight, k-ordered adds
+    float4 pa[8], pb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int cc = c0 + k <= c_last ? c0 + k : c_last;
+      const int slot = unit == it_begin(cc, G, total) / kbs ? 0 : 1;
+      const float* src = args.partial + ((int64_t)cc * 2 + slot) * slot_floats;
+      const bool ok = c0 + k <= c_last;
+      pa[k] = ok ? __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_a - unit * kRows) * Mp) + q4)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      pb[k] = ok ? __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(col_b - unit * kRows) * Mp) + q4)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sa.x += pa[k].x; sa.y += pa[k].y; sa.z += pa[k].z; sa.w += pa[k].w;
+      sb.x += pb[k].x; sb.y += pb[k].y; sb.z += pb[k].z; sb.w += pb[k].w;
+    }
   }
   const float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
   const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
