@@ -30,6 +30,8 @@ if os.environ.get("WS_DEBUG_WAIT"):  # watchdog build of the mbarrier waits (deb
     CUDA_ONLY.append("-DWS_DEBUG_WAIT")
 if os.environ.get("WS_ATTN_TRACE"):  # clock64 timeline of one attention CTA (debugging only)
     CUDA_ONLY.append("-DWS_ATTN_TRACE")
+if os.environ.get("WS_GEMM_TRACE"):  # per-CTA globaltimer timeline of the pair GEMM (debugging only)
+    CUDA_ONLY.append("-DWS_GEMM_TRACE")
 
 
 def _nvcc() -> str:

@@ -129,14 +129,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  pdl_wait();  // prologue above; global data from here on
+  // Weights are immutable: the producer fills the first ring stages with W
+  // tiles before waiting for the previous kernel (PDL), so a short GEMM's
+  // weight stream overlaps the tail of the kernel before it; activations
+  // (the previous kernel's output) are loaded after the wait. Every other
+  // thread waits up front.
+  const int pre = (warp == 0 && lane == 0) ? min(S, it1 - it0) : 0;
+  if (warp == 0 && lane == 0) {
+    for (int k = 0; k < pre; ++k) {
+      const int it = it0 + k, unit = it / kbs, kb = it % kbs;
+      const uint32_t sa = base + k * args.stage_bytes;
+      tc::mbar_expect_tx(full(k), args.stage_bytes);
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        tc::tma_load_2d(sa + j * kW_BYTES, &map_w, full(k), kb * kBK, (unit * NB + j) * kRows);
+    }
+  }
+  pdl_wait();  // global data produced by earlier kernels from here on
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int it = it0; it < it1; ++it) {
+      for (int k = 0; k < pre; ++k)
+        tc::tma_load_2d(base + k * args.stage_bytes + NB * kW_BYTES, &map_a, full(k), ((it0 + k) % kbs) * kBK, 0);
+      int stage = pre == S ? 0 : pre;
+      uint32_t phase = pre == S ? 1 : 0;
+      for (int it = it0 + pre; it < it1; ++it) {
         const int unit = it / kbs, kb = it % kbs;
         tc::mbar_wait(empty(stage), phase ^ 1);
         const uint32_t sa = base + stage * args.stage_bytes;

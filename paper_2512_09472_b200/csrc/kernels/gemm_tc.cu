@@ -506,55 +506,42 @@ __device__ __forceinline__ void epilogue_tile_tma(const TcEpilogue& ep, const CU
   }
 }
 
-// Work schedule of the pair kernel: units go round-robin to the pairs, so
-// all pairs run the same k-range of neighbouring tiles at the same time and
-// each weight block is read from HBM once (L2 reuse). A unit is a whole tile
-// (splits = 1) or, for the fp32 residual epilogue (x += A.B^T, the O and down
-// projections), one of `splits` k-slices of a tile: unit u = (slice u / tiles,
-// tile u % tiles). Splitting turns a partial last wave (128 tiles on 74 pairs
-// = 1.73 waves run as 2) into several short ones (512 slices = 6.92 waves).
-// Slices of a tile reduce-add into x in slice order: slice q waits until
-// flags[tile] says slice q-1 has landed — one fixed summation order, so
-// results are deterministic. Slice q-1 sits `tiles` units earlier (more than
-// one wave), so the wait is almost never taken, and a pair only ever waits
-// on an earlier unit: no deadlock while all pairs are resident.
-struct SkParams {
-  int splits;
-  uint32_t* flags;  // [tiles][2 ranks]: epoch * 16 + slices of this CTA's rows landed
-  uint32_t epoch;
-  int dbg;  // WS_SK_DBG bits (timing experiments): 1 = no wait, 4 = rotate k order, 8 = trace
-};
-
+// Work schedule of the pair kernel: tiles go round-robin to the pairs (m
+// fastest), so all pairs run the same k-range of neighbouring tiles at the
+// same time and each weight block is read from HBM once (L2 reuse).
+// (Stream-K and lock-step k-slicing of the partial last wave were measured:
+// contiguous stream-K ranges lose the lock-step L2 reuse — down 237 vs 171 us
+// — and k-slices only break even once each slice is long enough to hide the
+// slice epilogue, so the plain schedule stays.)
 struct TileIter {
-  int u, step, units, tiles, splits, KB;
-  __device__ TileIter(int pair, int n_pairs, int tiles_, int splits_, int kb)
-      : u(pair), step(n_pairs), units(tiles_ * splits_), tiles(tiles_), splits(splits_), KB(kb) {}
-  __device__ bool next(int& tile, int& q, int& kb0, int& kb1) {
-    if (u >= units) return false;
-    tile = u % tiles;
-    q = u / tiles;
-    kb0 = q * KB / splits;
-    kb1 = (q + 1) * KB / splits;
-    u += step;
+  int t, step, tiles;
+  __device__ TileIter(int pair, int n_pairs, int tiles_) : t(pair), step(n_pairs), tiles(tiles_) {}
+  __device__ bool next(int& tile) {
+    if (t >= tiles) return false;
+    tile = t;
+    t += step;
     return true;
   }
 };
 
-// WS_SK_DBG bit 8: per-CTA globaltimer trace [cta][0 start, 1-3 segment
-// accumulators ready, 4-6 segment epilogues done, 7 end] (tools/gemm_trace.py)
+// WS_GEMM_TRACE build: per-CTA globaltimer trace [cta][0 start, 1-3 tile
+// accumulators ready, 4-6 tile epilogues issued, 7 end] (tools/gemm_trace.py)
 __device__ long long g_gemm_trace[148][8];
+#ifdef WS_GEMM_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
-
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                    int N, int K, const __grid_constant__ TcEpilogue ep, const __grid_constant__ SkParams sk,
+                    int N, int K, const __grid_constant__ TcEpilogue ep,
                     const __grid_constant__ CUtensorMap map_c) {
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -601,38 +588,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
-  pdl_wait();  // everything above is prologue; global data from here on
+  auto load_a = [&](uint32_t sa, uint32_t bar, int kb, int m0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%3, %4}], [%2];\n" ::"r"(sa),
+        "l"(&map_a), "r"(bar), "r"(kb * BK), "r"(m0)
+        : "memory");
+  };
+  auto load_b = [&](uint32_t sa, uint32_t bar, int kb, int n0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%3, %4}], [%2];\n" ::"r"(sa + P_A_BYTES),
+        "l"(&map_b), "r"(bar), "r"(kb * BK), "r"(n0)
+        : "memory");
+  };
+  // The weight operand (B) is immutable: the producer fills the first ring
+  // stages with B tiles before the PDL wait, so they stream in under the tail
+  // of the previous kernel; A (the previous kernel's output) follows the wait.
+  int tile;
+  int pre = 0, pre_m0 = 0;
+  if (warp == 0 && lane == 0) {
+    TileIter it(pair, n_pairs, tiles);
+    if (it.next(tile)) {
+      pre = min(P_STAGES, k_blocks);
+      pre_m0 = (tile % m_blocks) * 256 + rank * P_BM;
+      const int n0 = (tile / m_blocks) * P_BN + rank * P_BNH;
+      for (int s = 0; s < pre; ++s) {
+        if (rank == 0) mbar_expect_tx(full(s), 2 * P_STAGE_BYTES);  // both CTAs' bytes
+        load_b(base + s * P_STAGE_BYTES, full(s) & peer_mask, s, n0);
+      }
+    }
+  }
+  pdl_wait();  // global data produced by earlier kernels from here on
 
-  int tile, sq, kb0, kb1;
   if (warp == 0) {
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
-      while (it.next(tile, sq, kb0, kb1)) {
+      for (int s = 0; s < pre; ++s) load_a(base + s * P_STAGE_BYTES, full(s) & peer_mask, s, pre_m0);
+      int stage = pre % P_STAGES;
+      uint32_t phase = pre == P_STAGES ? 1 : 0;
+      int skip = pre;  // k-blocks of the first tile already issued
+      TileIter it(pair, n_pairs, tiles);
+      while (it.next(tile)) {
         const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN + rank * P_BNH;
-        const int rot = (sk.dbg & 4) ? (pair * 17) % (kb1 - kb0) : 0;
-        for (int i = kb0; i < kb1; ++i) {
-          const int kb = kb0 + (i - kb0 + rot) % (kb1 - kb0);
+        for (int kb = skip; kb < k_blocks; ++kb) {
           mbar_wait(empty(stage), phase ^ 1);
           const uint32_t sa = base + stage * P_STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(full(stage), 2 * P_STAGE_BYTES);  // both CTAs' bytes
           const uint32_t bar = full(stage) & peer_mask;
-          asm volatile(
-              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-              "[%1, {%3, %4}], [%2];\n" ::"r"(sa),
-              "l"(&map_a), "r"(bar), "r"(kb * BK), "r"(m0)
-              : "memory");
-          asm volatile(
-              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-              "[%1, {%3, %4}], [%2];\n" ::"r"(sa + P_A_BYTES),
-              "l"(&map_b), "r"(bar), "r"(kb * BK), "r"(n0)
-              : "memory");
+          load_a(sa, bar, kb, m0);
+          load_b(sa, bar, kb, n0);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+        skip = 0;
       }
     }
     __syncwarp();
@@ -642,12 +652,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
-      while (it.next(tile, sq, kb0, kb1)) {
+      TileIter it(pair, n_pairs, tiles);
+      while (it.next(tile)) {
         mbar_wait(tempty(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * P_BN;
-        for (int i = kb0; i < kb1; ++i) {
+        for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * P_STAGE_BYTES;
@@ -658,7 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
                 "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2),
-                "r"((uint32_t)(i != kb0 || k != 0)));
+                "r"((uint32_t)(kb != 0 || k != 0)));
           asm volatile(
               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
                   empty(stage)),
@@ -684,38 +694,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int r_in = q * 32 + lane;  // this thread's row inside the CTA's 128
-    const bool tr = (sk.dbg & 8) && r_in == 0;
+    const bool tr = kTrace && r_in == 0;
     Stager st{stg + (uint32_t)q * 8192, lane};
     if (tr) g_gemm_trace[blockIdx.x][0] = gtimer();
     int acc = 0, seg = 0;
     uint32_t acc_phase = 0;
-    TileIter it(pair, n_pairs, tiles, sk.splits, k_blocks);
-    while (it.next(tile, sq, kb0, kb1)) {
+    TileIter it(pair, n_pairs, tiles);
+    while (it.next(tile)) {
       const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN;
       mbar_wait(tfull(acc), acc_phase);
       tc_fence_after();
       if (tr && seg < 3) g_gemm_trace[blockIdx.x][1 + seg] = gtimer();
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * P_BN;
-      const int row0 = m0 + q * 32;
-      if constexpr (MODE == (int)Epi::kAddF32) {
-        if (sk.splits > 1) {
-          // k-slice sq of this tile: reduce-add after slice sq-1 has landed
-          const uint32_t* f = sk.flags + tile * 2 + rank;  // this CTA's 128 rows of the tile
-          if (sq > 0 && r_in == 0 && !(sk.dbg & 1)) {
-            uint32_t v;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
-            } while (v != sk.epoch * 16 + sq);
-          }
-          epi_bar();
-          asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        }
-      }
       if constexpr (MODE == (int)Epi::kRopeKV) {
         const int row = m0 + r_in;
         epilogue_tile<MODE>(ep, tacc, row < M ? row : -1, n0, N, ep.kv.head_dim);
       } else {
-        epilogue_tile_tma<MODE>(ep, &map_c, st, tacc, row0, n0);
+        epilogue_tile_tma<MODE>(ep, &map_c, st, tacc, m0 + q * 32, n0);
       }
       tc_fence_before();
       // release this accumulator to the leader's MMA thread (remote arrive)
@@ -727,25 +722,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
-      if constexpr (MODE == (int)Epi::kAddF32) {
-        if (sk.splits > 1 && sq + 1 < sk.splits) {
-          // publish: this CTA's 128 rows of slice sq are in x
-          st.drain();
-          asm volatile("fence.proxy.async.global;\n" ::: "memory");
-          __threadfence();
-          epi_bar();
-          if (r_in == 0)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk.flags + tile * 2 + rank),
-                         "r"(sk.epoch * 16 + sq + 1)
-                         : "memory");
-        }
-      }
       if (tr && seg < 3) g_gemm_trace[blockIdx.x][4 + seg] = gtimer();
       ++seg;
     }
     st.drain();  // staging smem must outlive the TMA reads
   }
-  if ((sk.dbg & 8) && threadIdx.x == 128) g_gemm_trace[blockIdx.x][7] = gtimer();
+  if (kTrace && threadIdx.x == 128) g_gemm_trace[blockIdx.x][7] = gtimer();
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -804,59 +786,6 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
   launch_pdl(gemm_tc_kernel<MODE>, dim3(grid), dim3(THREADS), SMEM_BYTES, st, ma, mb, M, N, K, e);
 }
 
-// Per-device slice counters of the split schedule (one per tile).
-struct SkScratch {
-  uint32_t* flags = nullptr;
-  uint32_t epoch = 0;
-};
-constexpr int kMaxSplitTiles = 4096;
-
-bool sk_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("WS_STREAMK");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// Slices per tile for the residual (x += A.B^T) GEMMs: the split with the best
-// wave efficiency units / (waves * pairs), at least 8 k-blocks per slice so a
-// slice's mainloop still hides the previous slice's epilogue.
-SkParams sk_schedule(int mode, int tiles, int n_pairs, int k_blocks) {
-  SkParams p{};
-  p.splits = 1;
-  p.dbg = getenv("WS_SK_DBG") ? atoi(getenv("WS_SK_DBG")) : 0;
-  if (!sk_enabled() || mode != (int)Epi::kAddF32 || tiles > kMaxSplitTiles || tiles % n_pairs == 0) return p;
-  double best = (double)tiles / (double)(((tiles + n_pairs - 1) / n_pairs) * n_pairs);
-  int best_s = 1;
-  for (int s = 2; s <= 8 && k_blocks / s >= 8; ++s) {
-    const int units = tiles * s;
-    const double eff = (double)units / (double)(((units + n_pairs - 1) / n_pairs) * n_pairs);
-    if (eff > best + 0.01) {
-      best = eff;
-      best_s = s;
-    }
-  }
-  if (best_s == 1) return p;
-  static SkScratch scratch[16];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  SkScratch& sc = scratch[dev & 15];
-  if (!sc.flags) {
-    if (cudaMalloc(&sc.flags, 2 * kMaxSplitTiles * sizeof(uint32_t)) != cudaSuccess) return p;
-    cudaMemset(sc.flags, 0, 2 * kMaxSplitTiles * sizeof(uint32_t));
-  }
-  // a counter left by an earlier launch is below epoch * 16 (splits < 16)
-  if (++sc.epoch >= (1u << 27)) {
-    cudaMemset(sc.flags, 0, 2 * kMaxSplitTiles * sizeof(uint32_t));
-    sc.epoch = 1;
-  }
-  p.splits = best_s;
-  p.flags = sc.flags;
-  p.epoch = sc.epoch;
-  return p;
-}
-
 template <int MODE>
 bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
                   cudaStream_t st) {
@@ -875,9 +804,8 @@ bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
   } else if constexpr (MODE != (int)Epi::kRopeKV) {
     if (!make_out_map(&mc, e.C, M, N, 2)) return false;
   }
-  const SkParams sk = sk_schedule(MODE, tiles, n_pairs, K / BK);
   count_launch();
-  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, sk, mc);
+  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, mc);
   return true;
 }
 

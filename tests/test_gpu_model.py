@@ -365,12 +365,11 @@ def test_decode_gqa_shapes_match_oracle(lib, shape, lens):
 
 @pytest.mark.parametrize("M,N,K", [(2048, 4096, 4096), (2048, 4096, 14336), (2048, 6144, 4096), (1000, 28672, 4096),
                                    (700, 19200, 512)])
-def test_gemm_pair_split_deterministic(lib, M, N, K):
-    """Pair-kernel shapes whose 256x256 tile count is not a multiple of the 74
-    SM pairs: the residual epilogue (x += A.B^T) runs k-sliced tiles whose
-    slices reduce-add into x in slice order (TMA reduce, flag-ordered), the
-    other epilogues store through the TMA staging boxes. Every epilogue
-    against fp32; reruns are bit-identical."""
+def test_gemm_pair_tma_epilogues_deterministic(lib, M, N, K):
+    """CTA-pair kernel shapes with partial last waves and rows past M: the
+    residual epilogue (x += A.B^T) is a TMA reduce-add of each 32x32 box, the
+    fp32 / bf16 / SwiGLU epilogues are TMA stores through the swizzled staging
+    boxes. Every epilogue against fp32; reruns are bit-identical."""
     import ctypes as C
 
     g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)

@@ -1,6 +1,8 @@
-"""Per-CTA globaltimer timeline of one pair-GEMM launch (needs WS_SK_DBG=8).
+"""Per-CTA globaltimer timeline of one pair-GEMM launch (library built with
+WS_GEMM_TRACE=1, e.g. `touch csrc/kernels/gemm_tc.cu; WS_GEMM_TRACE=1 python -c
+"from paper_2512_09472_b200 import build; build.build()"`).
 
-    WS_SK_DBG=8 python tools/gemm_trace.py --shape o
+    python tools/gemm_trace.py --shape o
 """
 import argparse
 import ctypes as C
