@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--config3", default=str(ROOT / "profiles" / "r1_config3_switch_burst_1000.json"))
     ap.add_argument("--days", type=int, default=3)
     ap.add_argument("--out", default=str(ROOT / "profiles" / "r1_config5_replay.json"))
+    ap.add_argument("--artifacts", default=str(ROOT / "profiles" / "r1_config5_artifacts"),
+                    help="reference-format requests.csv / decisions.jsonl (metrics.py:137-242) per arm")
     a = ap.parse_args()
     bench = json.loads(Path(a.bench).read_text())
     c3 = json.loads(Path(a.config3).read_text()) if Path(a.config3).exists() else None
@@ -76,6 +78,13 @@ def main():
         t0 = time.perf_counter()
         ours = run_measured(engine, cfg, reqs, policy, measured, shapes)
         row["b200_measured"] = _summ(ours, time.perf_counter() - t0)
+        if policy == "warmserve" and a.artifacts:
+            # the reference's own artifact writer on both arms: byte-comparable formats
+            row["artifacts"] = {
+                "reference_modeled": [str(Path(p).relative_to(ROOT)) for p in
+                                      ref.write_artifacts(Path(a.artifacts) / "reference_modeled")],
+                "b200_measured": [str(Path(p).relative_to(ROOT)) for p in
+                                  ours.write_artifacts(Path(a.artifacts) / "b200_measured")]}
         out["policies"][policy] = row
         print(policy, json.dumps(row), flush=True)
     Path(a.out).write_text(json.dumps(out, indent=1))
