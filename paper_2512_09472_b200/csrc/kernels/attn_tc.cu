@@ -219,7 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int q0 = qt * kRows;
   const int n_keys = pos0 + min(rows, q0 + kRows);
   const int n_kt = (n_keys + kKeys - 1) / kKeys;
-  const int ldq = (heads + 2 * kv.kv_heads) * HD;
+  // HD is the smem / TMEM tile width; the model's head_dim may be smaller
+  // (Phi-3: 96 in 128-wide tiles): Q/K/V columns past it are zero, so S and
+  // the first hd columns of O are exact and the rest is never stored.
+  const int hd = kv.head_dim;
+  const int ldq = (heads + 2 * kv.kv_heads) * hd;
 
   if (threadIdx.x == 0) {
     mbar_init(B(kQFull), 128);
@@ -268,8 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = t; i < kRows * CH; i += 128) {
       const int r = i / CH, c = i % CH;
       const int gr = q0 + r;
-      const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + h * HD + c * 8;
-      cp_async16(gbase + S::kQ + swz(r, c), src, gr < rows);
+      const bf16* src = qkv + (int64_t)(gr < rows ? gr : 0) * ldq + h * hd + (c * 8 < hd ? c * 8 : 0);
+      cp_async16(gbase + S::kQ + swz(r, c), src, gr < rows && c * 8 < hd);
     }
     cp_async_arrive(B(kQFull));
     const bool is_v = t >= 64;
@@ -334,8 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ok = key < n_keys;
         const int32_t page = bt[ok ? blk : 0];
         const bf16* row = reinterpret_cast<const bf16*>(wbase + (int64_t)page * kv.page_size) + plane +
-                          (int64_t)(ok ? slot : 0) * HD;
-        cp_async16(dst + swz(r, c), row + c * 8, ok);
+                          (int64_t)(ok ? slot : 0) * hd;
+        cp_async16(dst + swz(r, c), row + (c * 8 < hd ? c * 8 : 0), ok && c * 8 < hd);
         r += RS;
         key += RS;
         slot += RS;
@@ -511,8 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t o[32];
       TLD32(tmem + lane_off + 256 + hf * (HD / 2) + c * 32, o);
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (grow < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + h * HD + hf * (HD / 2) + c * 32);
+      if (grow < rows && hf * (HD / 2) + c * 32 < hd) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * hd + h * hd + hf * (HD / 2) + c * 32);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           dst[q] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
@@ -967,7 +971,7 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
   static CUtensorMap map;
   static const char* map_window = nullptr;
   static int64_t map_pages = 0;
-  bool tma = kv.tpb % 16 == 0 && kv.page_size % (HD * 2) == 0;
+  bool tma = kv.head_dim == HD && kv.tpb % 16 == 0 && kv.page_size % (HD * 2) == 0;
   if (tma && (map_window != kv.window || map_pages != kv.n_pages)) {
     tma = window_map(&map, kv, HD, (attn_dbg() & 1) ? 128 : 16);
     map_window = tma ? kv.window : nullptr;
@@ -1007,7 +1011,7 @@ extern "C" int ws_attn_cta_trace(long long* out) {
 
 bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows,
                             int pos0, int heads, float scale, cudaStream_t st) {
-  if (kv.head_dim == 128)
+  if (kv.head_dim == 128 || kv.head_dim == 96)  // 96 runs in zero-padded 128-wide tiles
     dispatch<128>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
   else if (kv.head_dim == 64)
     dispatch<64>(qkv, out, kv, layer, seq, rows, pos0, heads, scale, st);
