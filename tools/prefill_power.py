@@ -30,8 +30,14 @@ def main():
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--gap-ms", type=float, default=0.0)
     ap.add_argument("--pool-pages", type=int, default=9216)
+    ap.add_argument("--tp", type=int, default=1,
+                    help="time one rank's shard (tp.shard_config) on this GPU: the per-rank compute of a "
+                         "TP prefill, allreduce excluded; the lm_head stays whole")
     a = ap.parse_args()
     cfg = M.ALL[a.model]
+    if a.tp > 1:
+        from paper_2512_09472_b200.tp import shard_config
+        cfg = shard_config(cfg, a.tp).with_(lm_head_rows=0)
     w = UniversalWorker(0, pool_pages=a.pool_pages, max_tokens=max(a.tokens, 256))
     w.register(cfg, None)
     w.prewarm(cfg.name, layers=cfg.layers)
@@ -64,7 +70,7 @@ def main():
     ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     clk = [float(r.split(",")[1]) for r in out.strip().splitlines() if r.count(",") >= 3]
     pw = [float(r.split(",")[2]) for r in out.strip().splitlines() if r.count(",") >= 3]
-    res = {"model": cfg.name, "tokens": a.tokens, "gap_ms": a.gap_ms, "ms": [round(x, 3) for x in ms],
+    res = {"model": cfg.name, "tp": a.tp, "tokens": a.tokens, "gap_ms": a.gap_ms, "ms": [round(x, 3) for x in ms],
            "ms_first3": ms[:3], "ms_median_last_half": sorted(ms[len(ms) // 2:])[len(ms) // 4],
            "sm_mhz": clk, "power_w": pw}
     print(json.dumps(res))
