@@ -195,7 +195,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 template <int HD, bool TMA>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, KvGeom kv, int layer, int seq,
-                   int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap, int dbg) {
+                   int rows, int pos0, int heads, float scale_log2, const __grid_constant__ CUtensorMap kvmap) {
   using S = Smem<HD>;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   pdl_trigger();
@@ -307,8 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(B(empty0 + st), ((j / NS) & 1) ^ 1);
             tma_expect(B(full0 + st), (uint32_t)(groups * (HD / 64) * 2048));
           }
-          const int gstep = (dbg & 1) ? 8 : 1;  // timing experiment: 128-row boxes (wrong data)
-          for (int g = 0; g < groups; g += gstep) {
+          for (int g = 0; g < groups; ++g) {
             const int yg = __shfl_sync(0xffffffffu, y, g);
             if (u == 0) {
 #pragma unroll
@@ -933,22 +932,18 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
 
 // 2D view of the page window as rows of HD bf16 (one token of one K or V
 // plane per row), 8-row x 64-column boxes with 128B swizzle.
-bool window_map(CUtensorMap* map, const KvGeom& kv, int hd, int box_rows = 16) {
+bool window_map(CUtensorMap* map, const KvGeom& kv, int hd) {
   const Driver* d = driver();
   if (!d) return false;
   cuuint64_t dims[2] = {(cuuint64_t)hd, (cuuint64_t)(kv.n_pages * kv.page_size / (hd * 2))};
   cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {64, 16};
   cuuint32_t estr[2] = {1, 1};
   return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.window, dims, strides, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int attn_dbg() {
-  static const int v = getenv("WS_ATTN_DBG") ? atoi(getenv("WS_ATTN_DBG")) : 0;
-  return v;
-}
 
 template <int HD, bool TMA>
 void launch_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows, int pos0,
@@ -961,7 +956,7 @@ void launch_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int se
   dim3 grid(heads, (rows + kRows - 1) / kRows);
   count_launch();
   launch_pdl(attn_tc_kernel<HD, TMA>, dim3(grid), dim3(kThreads), Smem<HD>::kBytes, st, qkv, out, kv, layer, seq, rows, pos0, heads,
-                                                                    scale * 1.4426950408889634f, map, attn_dbg());
+                                                                    scale * 1.4426950408889634f, map);
 }
 
 template <int HD>
@@ -973,7 +968,7 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
   static int64_t map_pages = 0;
   bool tma = kv.head_dim == HD && kv.tpb % 16 == 0 && kv.page_size % (HD * 2) == 0;
   if (tma && (map_window != kv.window || map_pages != kv.n_pages)) {
-    tma = window_map(&map, kv, HD, (attn_dbg() & 1) ? 128 : 16);
+    tma = window_map(&map, kv, HD);
     map_window = tma ? kv.window : nullptr;
     map_pages = tma ? kv.n_pages : 0;
   }
