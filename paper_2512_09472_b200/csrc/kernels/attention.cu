@@ -232,7 +232,7 @@ template <int HD>
 __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
-    int n_splits, int split_keys) {
+    int n_splits, int split_keys, bf16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   using S = DecodeSmem<HD>;
@@ -406,6 +406,10 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
       acc += f * row[d];
       l += f * row[HD + 1];
     }
+    if (n_splits == 1) {  // the whole context in this CTA: final output, no combine pass
+      out[(int64_t)b * heads * HD + (kvh * G + g) * HD + d] = f2bf(l > 0.f ? acc / l : 0.f);
+      continue;
+    }
     float* dst = part + (((int64_t)b * heads + kvh * G + g) * n_splits + split) * (HD + 2);
     dst[d] = acc;
     if (d == 0) {
@@ -480,10 +484,13 @@ void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const 
   const int split_keys = ((max_ctx + n_splits - 1) / n_splits + kDecKeys - 1) / kDecKeys * kDecKeys;
   n_splits = (max_ctx + split_keys - 1) / split_keys;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
-  count_launch(2);
+  count_launch();
   launch_pdl(attn_decode_kernel<HD>, grid, dim3(kDecWarps * 32), S::kBytes, st, qkv, kv, layer, seqs, ctx, heads,
-             scale * 1.4426950408889634f, scratch, n_splits, split_keys);
-  launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
+             scale * 1.4426950408889634f, scratch, n_splits, split_keys, out);
+  if (n_splits > 1) {
+    count_launch();
+    launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
+  }
 }
 
 }  // namespace
