@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
                         d0 = torch.cuda.Event(enable_timing=True)
                         d0.record(w.compute)
                     pos = torch.full((B,), ctx + i, dtype=torch.int32, device="cuda")
-                    _, tok = w.decode(sd, pos, tok, ctx + i + 1)
+                    _, tok = w.decode_graphed(sd, pos, tok, ctx + i + 1)
                 d1 = torch.cuda.Event(enable_timing=True)
                 d1.record(w.compute)
             torch.cuda.synchronize()
@@ -454,7 +454,8 @@ def run_ours(args, rank, world, local_rank):
                     pk["bf16_tflops_sustained"], "algorithmic_tflop": cfg.prefill_flops(S) / 1e12},
         "decode": {"per_batch": decode, "bound": "hbm", "peak_gbs": peaks()[0]["hbm_gbs"],
                    "bytes": "all weights except the embedding table + every sequence's K/V, per step",
-                   "path": "UniversalWorker.decode: skinny stream-K tcgen05 GEMMs + paged GQA decode attention"},
+                   "path": "UniversalWorker.decode_graphed (CUDA-graph replay of decode): skinny stream-K tcgen05 GEMMs + "
+                           "paged GQA decode attention"},
         "roofline": {"bound": "tensor", "kernel": "prefill gate/up GEMM 2048x28672x4096 (tensor-core path)",
                      "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "peak_kind": kind + " burst",

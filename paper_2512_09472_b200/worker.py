@@ -80,6 +80,7 @@ class UniversalWorker:
         self.logits = None
         self.next_tok = torch.zeros(256, dtype=torch.int32, device=self.dev)
         self.open_seqs: set[int] = set()
+        self._graphs: dict = {}  # (model, batch, ctx bucket) -> (CUDAGraph, static seqs, pos, tokens)
 
     # ------------------------------------------------------------ models
     def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32,
@@ -104,6 +105,7 @@ class UniversalWorker:
         v = max(m.cfg.vocab for m in self.models.values())
         if self.logits is None or self.logits.numel() < 256 * v:
             self.logits = torch.empty(256 * v, dtype=torch.float32, device=self.dev)
+        self._graphs.clear()  # captured decode steps hold the old workspace / logits pointers
         return e
 
     def set_gemm_impl(self, impl: int) -> None:
@@ -249,6 +251,43 @@ class UniversalWorker:
         if caller != self.compute:
             caller.wait_stream(self.compute)
         return self.logits[: n * e.cfg.vocab].view(n, e.cfg.vocab), self.next_tok[:n]
+
+    def decode_graphed(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor,
+                       max_ctx: int, ctx_bucket: int = 256):
+        """decode() replayed from a CUDA graph: the step's ~13 kernels per layer
+        (PDL edges included) go out as one launch, so a small batch is not
+        bound by host launch issue. One graph per (model, batch, context
+        bucket): the attention grid is sized for the bucket and every CTA
+        clips to its sequence's length, so results equal decode() with
+        max_ctx = the bucket. Inputs are copied into the graph's static
+        buffers on the compute stream."""
+        n = seqs_dev.numel()
+        cap = -(-max_ctx // ctx_bucket) * ctx_bucket
+        key = (self.active_model, n, cap)
+        ent = self._graphs.get(key)
+        caller = torch.cuda.current_stream(self.dev)
+        if caller != self.compute:
+            self.compute.wait_stream(caller)
+        if ent is None:
+            st = [torch.empty_like(seqs_dev), torch.empty_like(pos_dev), torch.empty_like(tokens_dev)]
+            with torch.cuda.stream(self.compute):
+                for d, s in zip(st, (seqs_dev, pos_dev, tokens_dev)):
+                    d.copy_(s)
+                self.decode(*st, cap)  # first use allocates the split-K scratch outside the capture
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.compute):
+                    self.decode(*st, cap)
+            ent = self._graphs[key] = (g, *st)
+        g, s_seqs, s_pos, s_tok = ent
+        with torch.cuda.stream(self.compute):
+            s_seqs.copy_(seqs_dev, non_blocking=True)
+            s_pos.copy_(pos_dev, non_blocking=True)
+            s_tok.copy_(tokens_dev, non_blocking=True)
+            g.replay()
+        if caller != self.compute:
+            caller.wait_stream(self.compute)
+        vocab = self.models[self.active_model].cfg.vocab
+        return self.logits[: n * vocab].view(n, vocab), self.next_tok[:n]
 
     # ------------------------------------------------------------ activation
     def activate_instance(self, name: str, prompt_host: torch.Tensor, source: torch.Tensor | None = None,

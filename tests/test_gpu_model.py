@@ -428,3 +428,33 @@ def test_wide_prefill_matches_oracle(lib):
         w.release()
     finally:
         w.close()
+
+
+def test_decode_graphed_matches_eager(tiny):
+    """The CUDA-graph decode step replays the same kernels as decode() with
+    max_ctx = the context bucket: bit-identical logits and tokens, and a new
+    batch's inputs are picked up by the replay (static input buffers)."""
+    cfg, w, weights = tiny
+    if w.slot(cfg.name) is None:
+        w.prewarm(cfg.name, layers=cfg.layers)
+    w.switch_memory(cfg.name)
+    lens = [40, 7, 300]
+    seqs = []
+    for i, n in enumerate(lens):
+        s = w.open_seq(n + 8)
+        w.prefill(s, _prompt(cfg, 900 + i, n).cuda())
+        seqs.append(s)
+    sd = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    for step in range(3):
+        pos = torch.tensor([n + step for n in lens], dtype=torch.int32, device="cuda")
+        tok = torch.tensor([11 + step, 22, 33 * step], dtype=torch.int32, device="cuda")
+        # both write the same KV slots (pos) with the same values, so either order is fine
+        ref, ref_tok = w.decode(sd, pos, tok, 512)
+        ref, ref_tok = ref.clone(), ref_tok.clone()
+        got, got_tok = w.decode_graphed(sd, pos, tok, int(pos.max()) + 1, ctx_bucket=512)
+        assert torch.equal(got, ref), step
+        assert torch.equal(got_tok, ref_tok), step
+    assert len(w._graphs) == 1
+    for s in seqs:
+        w.close_seq(s)
+    w.release()
