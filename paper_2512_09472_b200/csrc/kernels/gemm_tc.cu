@@ -509,17 +509,44 @@ __device__ __forceinline__ void epilogue_tile_tma(const TcEpilogue& ep, const CU
 // Work schedule of the pair kernel: tiles go round-robin to the pairs (m
 // fastest), so all pairs run the same k-range of neighbouring tiles at the
 // same time and each weight block is read from HBM once (L2 reuse).
-// (Stream-K and lock-step k-slicing of the partial last wave were measured:
-// contiguous stream-K ranges lose the lock-step L2 reuse — down 237 vs 171 us
-// — and k-slices only break even once each slice is long enough to hide the
-// slice epilogue, so the plain schedule stays.)
+// Residual GEMMs (x += A.B^T) with a partial last wave and a long K (the down
+// projection: 128 tiles on 74 pairs) cut only the tiles of that last wave
+// into `slices` k-slices dealt round-robin after the full waves: 54 tiles x 4
+// slices run as 3 rounds of quarter tiles instead of one round of whole tiles
+// on 54 of the 74 pairs. Slices of a tile reduce-add into x in slice order
+// (slice q waits on the tile's flag for slice q-1, which ran one round
+// earlier): one summation order, deterministic. (Stream-K ranges and slicing
+// every tile were measured slower: they lose the lock-step L2 reuse of the
+// full waves.)
+struct TailSched {
+  int dp_tiles;     // tiles [0, dp_tiles) whole; the rest sliced
+  int slices;       // 1 = no tail slicing
+  uint32_t* flags;  // [tail tile][2 ranks]: epoch * 16 + slices landed
+  uint32_t epoch;
+};
+
 struct TileIter {
-  int t, step, tiles;
-  __device__ TileIter(int pair, int n_pairs, int tiles_) : t(pair), step(n_pairs), tiles(tiles_) {}
-  __device__ bool next(int& tile) {
-    if (t >= tiles) return false;
-    tile = t;
-    t += step;
+  int t, step, dp, tail, units, slices, KB;
+  int u;
+  __device__ TileIter(int pair, int n_pairs, int tiles, const TailSched& s, int kb)
+      : t(pair), step(n_pairs), dp(s.dp_tiles), tail(tiles - s.dp_tiles), units((tiles - s.dp_tiles) * s.slices),
+        slices(s.slices), KB(kb), u(-1) {}
+  // tile, slice q, k-blocks [kb0, kb1)
+  __device__ bool next(int& tile, int& q, int& kb0, int& kb1) {
+    if (t < dp) {
+      tile = t;
+      q = 0;
+      kb0 = 0;
+      kb1 = KB;
+      t += step;
+      return true;
+    }
+    u = u < 0 ? t - dp : u + step;  // first tail unit continues the round-robin
+    if (u >= units) return false;
+    tile = dp + u % tail;
+    q = u / tail;
+    kb0 = q * KB / slices;
+    kb1 = (q + 1) * KB / slices;
     return true;
   }
 };
@@ -542,7 +569,7 @@ template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                     int N, int K, const __grid_constant__ TcEpilogue ep,
-                    const __grid_constant__ CUtensorMap map_c) {
+                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TailSched sched) {
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -605,17 +632,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   // The weight operand (B) is immutable: the producer fills the first ring
   // stages with B tiles before the PDL wait, so they stream in under the tail
   // of the previous kernel; A (the previous kernel's output) follows the wait.
-  int tile;
-  int pre = 0, pre_m0 = 0;
+  int tile, sq, kb0, kb1;
+  int pre = 0, pre_m0 = 0, pre_kb0 = 0;
   if (warp == 0 && lane == 0) {
-    TileIter it(pair, n_pairs, tiles);
-    if (it.next(tile)) {
-      pre = min(P_STAGES, k_blocks);
+    TileIter it(pair, n_pairs, tiles, sched, k_blocks);
+    if (it.next(tile, sq, kb0, kb1)) {
+      pre = min(P_STAGES, kb1 - kb0);
       pre_m0 = (tile % m_blocks) * 256 + rank * P_BM;
+      pre_kb0 = kb0;
       const int n0 = (tile / m_blocks) * P_BN + rank * P_BNH;
       for (int s = 0; s < pre; ++s) {
         if (rank == 0) mbar_expect_tx(full(s), 2 * P_STAGE_BYTES);  // both CTAs' bytes
-        load_b(base + s * P_STAGE_BYTES, full(s) & peer_mask, s, n0);
+        load_b(base + s * P_STAGE_BYTES, full(s) & peer_mask, kb0 + s, n0);
       }
     }
   }
@@ -623,14 +651,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int s = 0; s < pre; ++s) load_a(base + s * P_STAGE_BYTES, full(s) & peer_mask, s, pre_m0);
+      for (int s = 0; s < pre; ++s) load_a(base + s * P_STAGE_BYTES, full(s) & peer_mask, pre_kb0 + s, pre_m0);
       int stage = pre % P_STAGES;
       uint32_t phase = pre == P_STAGES ? 1 : 0;
-      int skip = pre;  // k-blocks of the first tile already issued
-      TileIter it(pair, n_pairs, tiles);
-      while (it.next(tile)) {
+      int skip = pre;  // k-blocks of the first unit already issued
+      TileIter it(pair, n_pairs, tiles, sched, k_blocks);
+      while (it.next(tile, sq, kb0, kb1)) {
         const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN + rank * P_BNH;
-        for (int kb = skip; kb < k_blocks; ++kb) {
+        for (int kb = kb0 + skip; kb < kb1; ++kb) {
           mbar_wait(empty(stage), phase ^ 1);
           const uint32_t sa = base + stage * P_STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(full(stage), 2 * P_STAGE_BYTES);  // both CTAs' bytes
@@ -652,12 +680,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      TileIter it(pair, n_pairs, tiles);
-      while (it.next(tile)) {
+      TileIter it(pair, n_pairs, tiles, sched, k_blocks);
+      while (it.next(tile, sq, kb0, kb1)) {
         mbar_wait(tempty(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * P_BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * P_STAGE_BYTES;
@@ -668,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
                 "l"(da + (uint64_t)(2 * k)), "l"(db + (uint64_t)(2 * k)), "r"(kIdesc2),
-                "r"((uint32_t)(kb != 0 || k != 0)));
+                "r"((uint32_t)(kb != kb0 || k != 0)));
           asm volatile(
               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
                   empty(stage)),
@@ -699,13 +727,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (tr) g_gemm_trace[blockIdx.x][0] = gtimer();
     int acc = 0, seg = 0;
     uint32_t acc_phase = 0;
-    TileIter it(pair, n_pairs, tiles);
-    while (it.next(tile)) {
+    TileIter it(pair, n_pairs, tiles, sched, k_blocks);
+    while (it.next(tile, sq, kb0, kb1)) {
       const int m0 = (tile % m_blocks) * 256 + rank * P_BM, n0 = (tile / m_blocks) * P_BN;
       mbar_wait(tfull(acc), acc_phase);
       tc_fence_after();
       if (tr && seg < 3) g_gemm_trace[blockIdx.x][1 + seg] = gtimer();
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * P_BN;
+      const bool sliced = MODE == (int)Epi::kAddF32 && tile >= sched.dp_tiles && sched.slices > 1;
+      uint32_t* flag = sched.flags + (tile - sched.dp_tiles) * 2 + rank;  // this CTA's 128 rows of the tile
+      if (sliced && sq > 0) {  // slice sq reduce-adds after slice sq-1 of this tile has landed
+        if (r_in == 0) {
+          uint32_t v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+          } while (v != sched.epoch * 16 + sq);
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      }
       if constexpr (MODE == (int)Epi::kRopeKV) {
         const int row = m0 + r_in;
         epilogue_tile<MODE>(ep, tacc, row < M ? row : -1, n0, N, ep.kv.head_dim);
@@ -721,6 +761,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (sliced && sq + 1 < sched.slices) {  // publish: slice sq of these 128 rows is in x
+        st.drain();
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (r_in == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(flag), "r"(sched.epoch * 16 + sq + 1)
+                       : "memory");
       }
       if (tr && seg < 3) g_gemm_trace[blockIdx.x][4 + seg] = gtimer();
       ++seg;
@@ -786,6 +835,49 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
   launch_pdl(gemm_tc_kernel<MODE>, dim3(grid), dim3(THREADS), SMEM_BYTES, st, ma, mb, M, N, K, e);
 }
 
+// Tail slicing for residual GEMMs (see TailSched): the slice count with the
+// shortest tail, only when every slice keeps >= 48 k-blocks (long enough to
+// hide the slice's reduce-add epilogue behind the next slice's mainloop).
+TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks) {
+  TailSched p{};
+  p.dp_tiles = tiles;
+  p.slices = 1;
+  static const bool on = !(getenv("WS_TAIL_SLICES") && getenv("WS_TAIL_SLICES")[0] == '0');
+  if (!on || mode != (int)Epi::kAddF32 || tiles <= n_pairs || tiles % n_pairs == 0) return p;
+  const int dp = tiles / n_pairs * n_pairs, tail = tiles - dp;
+  double best = 1.0;  // tail time in whole-tile units without slicing
+  int best_s = 1;
+  for (int s = 2; s <= 4 && k_blocks / s >= 48; ++s) {
+    const double t = (double)((tail * s + n_pairs - 1) / n_pairs) / s;
+    if (t < best - 0.01) {
+      best = t;
+      best_s = s;
+    }
+  }
+  if (best_s == 1 || tail > 4096) return p;
+  struct Flags {
+    uint32_t* f = nullptr;
+    uint32_t epoch = 0;
+  };
+  static Flags flags[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Flags& fl = flags[dev & 15];
+  if (!fl.f) {
+    if (cudaMalloc(&fl.f, 2 * 4096 * sizeof(uint32_t)) != cudaSuccess) return p;
+    cudaMemset(fl.f, 0, 2 * 4096 * sizeof(uint32_t));
+  }
+  if (++fl.epoch >= (1u << 27)) {  // a flag left by an earlier launch is below epoch * 16
+    cudaMemset(fl.f, 0, 2 * 4096 * sizeof(uint32_t));
+    fl.epoch = 1;
+  }
+  p.dp_tiles = dp;
+  p.slices = best_s;
+  p.flags = fl.f;
+  p.epoch = fl.epoch;
+  return p;
+}
+
 template <int MODE>
 bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, const TcEpilogue& e,
                   cudaStream_t st) {
@@ -804,8 +896,9 @@ bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
   } else if constexpr (MODE != (int)Epi::kRopeKV) {
     if (!make_out_map(&mc, e.C, M, N, 2)) return false;
   }
+  const TailSched sched = tail_schedule(MODE, tiles, n_pairs, K / BK);
   count_launch();
-  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, mc);
+  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, mc, sched);
   return true;
 }
 
