@@ -99,11 +99,11 @@ def test_gemv_against_fp32(lib, M):
     assert _rel(out, A.float() @ B.float().T) < 1e-5
 
 
-def _worker(cfg, seed=11, pool_pages=64):
+def _worker(cfg, seed=11, pool_pages=64, max_tokens=1024):
     from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat
     from paper_2512_09472_b200.worker import UniversalWorker
 
-    w = UniversalWorker(0, pool_pages=pool_pages, max_tokens=1024)
+    w = UniversalWorker(0, pool_pages=pool_pages, max_tokens=max_tokens)
     flat = synth_flat(cfg, seed=seed, device="cuda")
     host = pinned_host_copy(flat)
     w.register(cfg, host)
@@ -398,31 +398,34 @@ def test_gemm_pair_tma_epilogues_deterministic(lib, M, N, K):
     assert _rel(act.float(), _swiglu_ref(A, B)) < 1e-2
 
 
-def test_wide_prefill_matches_oracle(lib):
-    """Llama-3-8B layer widths (d 4096, 32/8 heads, ffn 14336), 2 layers, 1024
-    tokens: pair-kernel GEMMs with the fused RoPE/KV-append and SwiGLU
-    epilogues and k-sliced residual GEMMs; logits against the fp32 oracle and
-    a decode step over the KV they appended."""
+@pytest.mark.parametrize("S", [1024, 1537])
+def test_wide_prefill_matches_oracle(lib, S):
+    """Llama-3-8B layer widths (d 4096, 32/8 heads, ffn 14336), 2 layers:
+    pair-kernel GEMMs with the fused RoPE/KV-append, SwiGLU and TMA residual
+    epilogues, the persistent two-head attention; 1537 tokens leaves a
+    one-row last m-block and a one-query last attention tile (rows past the
+    prompt clipped by the TMA stores). Logits against the fp32 oracle and a
+    decode step over the KV they appended."""
     from paper_2512_09472_b200 import models as M
 
     cfg = M.TINY.with_(name="wide", hidden=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336, layers=2,
                        vocab=4096)
-    w, host = _worker(cfg, pool_pages=640)
+    w, host = _worker(cfg, pool_pages=640, max_tokens=2048)
     try:
         weights = O.unpack(cfg, cfg.layout(), host.clone())
         w.prewarm(cfg.name, layers=cfg.layers)
         w.switch_memory(cfg.name)
-        prompt = _prompt(cfg, 5, 1024)
-        s = w.open_seq(1024 + 4)
+        prompt = _prompt(cfg, 5, S)
+        s = w.open_seq(S + 4)
         w.prefill(s, prompt.cuda())
         got = w.logits[: cfg.vocab].float().cpu()
         ref, past = O.forward(cfg, weights, prompt.long())
         assert _rel(got, ref[-1]) < LOGIT_RTOL
         tok = int(ref[-1].argmax())
         logits, _ = w.decode(torch.tensor([s], dtype=torch.int32, device="cuda"),
-                             torch.tensor([1024], dtype=torch.int32, device="cuda"),
-                             torch.tensor([tok], dtype=torch.int32, device="cuda"), 1025)
-        ref2, _ = O.forward(cfg, weights, [tok], pos0=1024, past=past)
+                             torch.tensor([S], dtype=torch.int32, device="cuda"),
+                             torch.tensor([tok], dtype=torch.int32, device="cuda"), S + 1)
+        ref2, _ = O.forward(cfg, weights, [tok], pos0=S, past=past)
         assert _rel(logits[0].float().cpu(), ref2[0]) < LOGIT_RTOL
         w.close_seq(s)
         w.release()
