@@ -17,6 +17,9 @@
 // together and the weight tile is read from HBM once (L2 reuse).
 #include <cuda.h>
 
+#include <map>
+#include <mutex>
+
 #include "../common.h"
 #include "../driver.h"
 #include "device.cuh"
@@ -838,7 +841,7 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
 // Tail slicing for residual GEMMs (see TailSched): the slice count with the
 // shortest tail, only when every slice keeps >= 48 k-blocks (long enough to
 // hide the slice's reduce-add epilogue behind the next slice's mainloop).
-TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks) {
+TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks, cudaStream_t st) {
   TailSched p{};
   p.dp_tiles = tiles;
   p.slices = 1;
@@ -855,20 +858,24 @@ TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks) {
     }
   }
   if (best_s == 1 || tail > 4096) return p;
+  // one flag array per (device, stream): launches on a stream are ordered, so
+  // they can share it; concurrent streams must not (a waiter compares for equality)
   struct Flags {
     uint32_t* f = nullptr;
     uint32_t epoch = 0;
   };
-  static Flags flags[16];
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, Flags> all;
   int dev = 0;
   cudaGetDevice(&dev);
-  Flags& fl = flags[dev & 15];
+  std::lock_guard<std::mutex> lk(mu);
+  Flags& fl = all[{dev, st}];
   if (!fl.f) {
     if (cudaMalloc(&fl.f, 2 * 4096 * sizeof(uint32_t)) != cudaSuccess) return p;
-    cudaMemset(fl.f, 0, 2 * 4096 * sizeof(uint32_t));
+    cudaMemsetAsync(fl.f, 0, 2 * 4096 * sizeof(uint32_t), st);
   }
   if (++fl.epoch >= (1u << 27)) {  // a flag left by an earlier launch is below epoch * 16
-    cudaMemset(fl.f, 0, 2 * 4096 * sizeof(uint32_t));
+    cudaMemsetAsync(fl.f, 0, 2 * 4096 * sizeof(uint32_t), st);
     fl.epoch = 1;
   }
   p.dp_tiles = dp;
@@ -896,7 +903,7 @@ bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
   } else if constexpr (MODE != (int)Epi::kRopeKV) {
     if (!make_out_map(&mc, e.C, M, N, 2)) return false;
   }
-  const TailSched sched = tail_schedule(MODE, tiles, n_pairs, K / BK);
+  const TailSched sched = tail_schedule(MODE, tiles, n_pairs, K / BK, st);
   count_launch();
   launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, mc, sched);
   return true;
