@@ -108,6 +108,7 @@ SIGNATURES: dict[str, list] = {
     "ws_streamer_create": [i32, P(vp)],
     "ws_streamer_destroy": [vp],
     "ws_streamer_start": [vp, vp, vp, P(i64), i32, vp],
+    "ws_streamer_start_packed": [vp, vp, vp, P(i64), i32, vp, i64, vp, vp],
     "ws_streamer_wait": [vp, i32, vp],
     "ws_streamer_times": [vp, P(f32), i32],
 }

@@ -104,6 +104,11 @@ void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
 // vocab shards [tp][rows][vs] into logits [rows][tp*vs].
 void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st);
 void launch_gather_vocab(const float* gathered, float* logits, int tp, int rows, int vs, cudaStream_t st);
+// Packed bf16 weight ranges (unpack.cu): section offsets of a packed range
+// of n values with n_esc escapes, and the two-pass rebuild into dst.
+void packed_sections(int64_t n, int64_t n_esc, int64_t* codes_off, int64_t* idx_off, int64_t* exp_off,
+                     int64_t* total);
+void launch_unpack_bf16(void* dst, const void* packed, int64_t n, int e_base, int64_t n_esc, cudaStream_t st);
 // Logits (fp32) for M rows and their argmax.
 void launch_argmax(const float* logits, int M, int V, int32_t* out, float* scratch, cudaStream_t st);
 

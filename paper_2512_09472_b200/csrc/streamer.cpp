@@ -7,9 +7,11 @@
 #include <vector>
 
 #include "common.h"
+#include "kernels/ops.cuh"
 
 struct ws_streamer {
-  std::vector<cudaEvent_t> done;  // per range, timing-enabled
+  std::vector<cudaEvent_t> done;    // per range, timing-enabled: the range is usable
+  std::vector<cudaEvent_t> copied;  // packed mode: the range's packed bytes are in staging
   cudaEvent_t start = nullptr;
   int32_t started = 0;
 };
@@ -38,6 +40,8 @@ int ws_streamer_destroy(ws_streamer* s) {
   if (s->start) cudaEventDestroy(s->start);
   for (auto e : s->done)
     if (e) cudaEventDestroy(e);
+  for (auto e : s->copied)
+    if (e) cudaEventDestroy(e);
   delete s;
   return WS_OK;
 }
@@ -56,6 +60,44 @@ int ws_streamer_start(ws_streamer* s, void* dst_base, const void* src_base, cons
                               cudaMemcpyDefault, st));
     WS_CUDA(cudaEventRecord(s->done[i], st));
   }
+  s->started = n;
+  return WS_OK;
+}
+
+int ws_streamer_start_packed(ws_streamer* s, void* dst_base, const void* packed_base, const int64_t* desc,
+                             int32_t n, void* staging, int64_t staging_bytes, void* copy_stream,
+                             void* unpack_stream) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  if (n < 0 || n > (int32_t)s->done.size()) WS_FAIL(WS_ERR_INVALID, "too many ranges");
+  if (!staging || ((uintptr_t)staging & 255)) WS_FAIL(WS_ERR_INVALID, "staging must be 256-byte aligned");
+  const int64_t half = staging_bytes / 2 / 256 * 256;  // two alternating slots
+  if (s->copied.size() < s->done.size()) {
+    s->copied.resize(s->done.size(), nullptr);
+    for (auto& e : s->copied)
+      if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+        WS_FAIL(WS_ERR_CUDA, "cudaEventCreate failed");
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    const int64_t* d = desc + 6 * i;
+    if (d[5] > half) WS_FAIL(WS_ERR_INVALID, "packed range %d (%lld B) exceeds the staging slot (%lld B)", i,
+                             (long long)d[5], (long long)half);
+    if (d[3] < 0 || d[3] > 240) WS_FAIL(WS_ERR_INVALID, "exponent base out of range");
+  }
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(copy_stream);
+  cudaStream_t us = reinterpret_cast<cudaStream_t>(unpack_stream);
+  WS_CUDA(cudaEventRecord(s->start, cs));
+  for (int32_t i = 0; i < n; ++i) {
+    // desc[i] = {dst_offset, packed_offset, n_values, e_base, n_escapes, packed_bytes}
+    const int64_t* d = desc + 6 * i;
+    char* slot = static_cast<char*>(staging) + (i & 1) * half;
+    if (i >= 2) WS_CUDA(cudaStreamWaitEvent(cs, s->done[i - 2], 0));  // slot free once range i-2 unpacked
+    WS_CUDA(cudaMemcpyAsync(slot, static_cast<const char*>(packed_base) + d[1], (size_t)d[5], cudaMemcpyDefault, cs));
+    WS_CUDA(cudaEventRecord(s->copied[i], cs));
+    WS_CUDA(cudaStreamWaitEvent(us, s->copied[i], 0));
+    ws::launch_unpack_bf16(static_cast<char*>(dst_base) + d[0], slot, d[2], (int)d[3], d[4], us);
+    WS_CUDA(cudaEventRecord(s->done[i], us));
+  }
+  WS_CUDA(cudaGetLastError());
   s->started = n;
   return WS_OK;
 }

@@ -53,3 +53,84 @@ def pinned_host_copy(flat_dev: torch.Tensor) -> torch.Tensor:
     host = torch.empty(flat_dev.numel(), dtype=flat_dev.dtype, pin_memory=True)
     host.copy_(flat_dev)
     return host
+
+
+# ---------------------------------------------------------------- packed stream
+def _align(v: int, a: int) -> int:
+    return (v + a - 1) // a * a
+
+
+def packed_sections(n: int, n_esc: int) -> tuple[int, int, int, int]:
+    """(codes, idx, exp, total) byte offsets of a packed range — the layout
+    ws::packed_sections uses (csrc/kernels/unpack.cu)."""
+    codes = _align(n, 16)
+    idx = _align(codes + (n + 1) // 2, 16)
+    exp = _align(idx + 4 * n_esc, 16)
+    return codes, idx, exp, _align(exp + n_esc, 16)
+
+
+class PackedImage:
+    """Losslessly packed host image of a model's streamable ranges (every
+    decoder layer, then final norm + lm_head), for the packed cold-start
+    stream (ws_streamer_start_packed). Per bf16 weight: one byte of
+    sign|mantissa plus a 4-bit exponent code relative to the range's densest
+    15-exponent window; values outside it are escapes (position + exponent).
+    Random-init and trained bf16 weights both sit in a few exponents, so a
+    range packs to ~12 bits per weight: ~25% fewer bytes over PCIe."""
+
+    def __init__(self, blob: torch.Tensor, desc: list[list[int]], ranges: list[tuple[int, int, int]]):
+        self.blob = blob      # pinned uint8
+        self.desc = desc      # per range: [dst_off, packed_off, n_values, e_base, n_escapes, packed_bytes]
+        self.ranges = ranges  # layout.stream_ranges(0): layers 0..L-1, then the tail
+
+    def rows(self, first_layer: int) -> list[list[int]]:
+        """desc rows streamed when layers [0, first_layer) are resident."""
+        return self.desc[first_layer:]
+
+    @property
+    def max_range_bytes(self) -> int:
+        return max(d[5] for d in self.desc)
+
+
+def pack_range(v: torch.Tensor) -> tuple[torch.Tensor, int, int]:
+    """Pack one range of bf16 values (1-D tensor, any device): returns the
+    packed bytes (same device), the exponent base and the escape count."""
+    u = v.view(torch.int16).to(torch.int32) & 0xFFFF
+    n = u.numel()
+    e = (u >> 7) & 0xFF
+    hist = torch.bincount(e, minlength=256).cpu()
+    cs = torch.cat([torch.zeros(1, dtype=hist.dtype), hist.cumsum(0)])
+    base = int(torch.argmax(cs[15:256] - cs[0:241]))  # window [base, base + 15), base <= 240
+    code = e - base
+    esc = (code < 0) | (code > 14)
+    code = code.masked_fill(esc, 15)
+    lo = (((u >> 8) & 0x80) | (u & 0x7F)).to(torch.uint8)
+    if n % 2:
+        code = torch.cat([code, code.new_zeros(1)])
+    codes = (code[0::2] | (code[1::2] << 4)).to(torch.uint8)
+    idx = esc.nonzero().flatten().to(torch.int32)
+    exps = e[idx.long()].to(torch.uint8)
+    n_esc = idx.numel()
+    c_off, i_off, e_off, total = packed_sections(n, n_esc)
+    out = torch.zeros(total, dtype=torch.uint8, device=v.device)
+    out[:n] = lo
+    out[c_off:c_off + codes.numel()] = codes
+    out[i_off:i_off + 4 * n_esc] = idx.view(torch.uint8)
+    out[e_off:e_off + n_esc] = exps
+    return out, base, n_esc
+
+
+def pack_stream(cfg: ModelConfig, flat: torch.Tensor) -> PackedImage:
+    """PackedImage of every streamable range of ``flat`` (the bf16 slot image;
+    packing runs where ``flat`` lives — on the GPU it takes seconds)."""
+    ranges = cfg.layout().stream_ranges(0)
+    parts, desc, off = [], [], 0
+    for dst, src, nbytes in ranges:
+        blob, base, n_esc = pack_range(flat[src // 2: (src + nbytes) // 2])
+        desc.append([dst, off, nbytes // 2, base, n_esc, blob.numel()])
+        parts.append(blob)
+        off += _align(blob.numel(), 256)
+    host = torch.empty(off, dtype=torch.uint8, pin_memory=True)
+    for d, p in zip(desc, parts):
+        host[d[1]:d[1] + p.numel()].copy_(p)
+    return PackedImage(host, desc, ranges)

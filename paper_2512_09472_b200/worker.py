@@ -36,6 +36,7 @@ class ModelEntry:
     host: torch.Tensor | None  # pinned bf16 image: cold-start source
     handle: C.c_void_p
     peer: torch.Tensor | None = None  # optional peer-device image (NVLink source)
+    packed: object | None = None      # weights.PackedImage: the packed cold-start stream
 
 
 @dataclass
@@ -47,8 +48,8 @@ class ActivationResult:
     switch_ms: float               # host clock of the memory switch (ledger + kernel launch)
     switch_kernel_ms: float
     streamed_layers: int
-    streamed_bytes: int
-    stream_ms: float               # copy stream: start -> last layer landed
+    streamed_bytes: int            # bytes over the link (packed bytes on the packed stream)
+    stream_ms: float               # copy stream: start -> last layer landed (unpacked)
     evicted: list = field(default_factory=list)
     seq: int = -1
 
@@ -81,6 +82,8 @@ class UniversalWorker:
         self.next_tok = torch.zeros(256, dtype=torch.int32, device=self.dev)
         self.open_seqs: set[int] = set()
         self._graphs: dict = {}  # (model, batch, ctx bucket) -> (CUDAGraph, static seqs, pos, tokens)
+        self.unpack = torch.cuda.Stream(self.dev)  # packed stream: rebuilds bf16 ranges in the slot
+        self._staging = None
 
     # ------------------------------------------------------------ models
     def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32,
@@ -107,6 +110,14 @@ class UniversalWorker:
             self.logits = torch.empty(256 * v, dtype=torch.float32, device=self.dev)
         self._graphs.clear()  # captured decode steps hold the old workspace / logits pointers
         return e
+
+    def set_packed(self, name: str, packed) -> None:
+        """Attach a weights.PackedImage: cold activations of ``name`` then
+        stream the packed ranges (fewer PCIe bytes) instead of the bf16 image."""
+        self.models[name].packed = packed
+        need = 2 * (-(-packed.max_range_bytes // 256) * 256)
+        if self._staging is None or self._staging.numel() < need:
+            self._staging = torch.empty(need, dtype=torch.uint8, device=self.dev)
 
     def set_gemm_impl(self, impl: int) -> None:
         for e in self.models.values():
@@ -306,7 +317,17 @@ class UniversalWorker:
         k = slot.layers_loaded
         stream_from = None
         streamed = 0
-        if k < L:
+        if k < L and source is None and e.packed is not None:
+            rows = e.packed.rows(k)
+            flat = (C.c_int64 * (6 * len(rows)))(*[v for r in rows for v in r])
+            self.copy.wait_stream(self.compute)  # copy after the switch (pages owned)
+            self.unpack.wait_stream(self.compute)
+            N.call("ws_streamer_start_packed", self.streamer, C.c_void_p(slot.va),
+                   C.c_void_p(e.packed.blob.data_ptr()), flat, len(rows), C.c_void_p(self._staging.data_ptr()),
+                   self._staging.numel(), C.c_void_p(self.copy.cuda_stream), C.c_void_p(self.unpack.cuda_stream))
+            stream_from = k
+            streamed = sum(r[5] for r in rows)
+        elif k < L:
             src = source if source is not None else e.host
             ranges = e.layout.stream_ranges(k)
             flat = (C.c_int64 * (3 * len(ranges)))(*[v for r in ranges for v in r])
