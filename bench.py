@@ -197,7 +197,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2512_09472_b200 import models as M
     from paper_2512_09472_b200.cluster import catchup_stall_ms, required_prewarm_layers
     from paper_2512_09472_b200.devmem import view
-    from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat
+    from paper_2512_09472_b200.weights import pack_stream, pinned_host_copy, synth_flat
     from paper_2512_09472_b200.worker import UniversalWorker
 
     dev = local_rank
@@ -220,6 +220,9 @@ def run_ours(args, rank, world, local_rank):
     t_setup = time.perf_counter()
     flat = synth_flat(cfg, seed=rank, device="cuda")
     host = pinned_host_copy(flat)
+    t_pack = time.perf_counter()
+    packed = pack_stream(cfg, flat)  # lossless packed host image of the streamable ranges
+    pack_s = time.perf_counter() - t_pack
     del flat
     torch.cuda.empty_cache()
     w = UniversalWorker(dev, pool_pages=args.pool_pages, max_tokens=max(S, 256))
@@ -234,7 +237,7 @@ def run_ours(args, rank, world, local_rank):
     # clocks are sampled across every timed region below (cold, warm, value)
     clk = Clocks(dev).__enter__()
     time.sleep(0.5)  # let nvidia-smi start sampling before the first timed step
-    # ---- cold starts (e2e): layers k..L + lm_head stream over PCIe each step
+    # ---- cold starts, plain bf16 stream: layers k..L + lm_head over PCIe each step
     cold = []
     for i in range(Wm + K):
         if i:
@@ -244,6 +247,18 @@ def run_ours(args, rank, world, local_rank):
         w.release()
         if i >= Wm:
             cold.append(r)
+    # ---- cold starts (e2e), packed stream: the same ranges losslessly packed on
+    #      the host (~25% fewer PCIe bytes), unpacked on the GPU per layer
+    w.set_packed(cfg.name, packed)
+    cold_packed = []
+    for i in range(Wm + K):
+        w.drop_suffix(cfg.name, args.prewarm_layers)
+        barrier()
+        r = w.activate_instance(cfg.name, prompt_pinned)
+        w.release()
+        if i >= Wm:
+            cold_packed.append(r)
+    w.models[cfg.name].packed = None
     # ---- cold starts from an HBM-resident image of the model on this GPU: the
     #      stand-in for a peer GPU's copy (an NVLink 5 peer is
     #      capped at ~900 GB/s, this source is faster), showing what layer
@@ -399,8 +414,9 @@ def run_ours(args, rank, world, local_rank):
         traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
 
     cold_ttft = [r.ttft_ms for r in cold]
+    packed_ttft = [r.ttft_ms for r in cold_packed]
     warm_ttft = [r.ttft_ms for r in warm]
-    cold_total_s = max_over_ranks(sum(cold_ttft) / 1e3)
+    cold_total_s = max_over_ranks(sum(packed_ttft) / 1e3)
     e2e_value = world * K * S / cold_total_s
     clk_sum = clk.summary()
 
@@ -422,12 +438,19 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "no flush needed: 16 GB of weights per step > 126 MB L2",
                    "pool_pages": args.pool_pages},
         "e2e": {"value": e2e_value, "unit": "tokens/s",
-                "h2d_bytes_per_step": int(statistics.median(r.streamed_bytes for r in cold)) + S * 4,
+                "h2d_bytes_per_step": int(statistics.median(r.streamed_bytes for r in cold_packed)) + S * 4,
                 "d2h_bytes_per_step": 4,
-                "path": "UniversalWorker.activate_instance (cold): switch_memory + layer streaming + prefill"},
-        "ttft_ms": {"cold_p50": pct(cold_ttft, 50), "cold_p99": pct(cold_ttft, 99),
+                "path": "UniversalWorker.activate_instance (cold, packed stream): switch_memory + packed layer "
+                        "streaming from pinned host memory + GPU unpack + prefill"},
+        "ttft_ms": {"cold_p50": pct(packed_ttft, 50), "cold_p99": pct(packed_ttft, 99),
+                    "cold_over_warm_p50": pct(packed_ttft, 50) / pct(warm_ttft, 50),
+                    "cold_packed_streamed_bytes": cold_packed[0].streamed_bytes,
+                    "cold_packed_stream_ms_p50": pct([r.stream_ms for r in cold_packed], 50),
+                    "pack_ratio": cold_packed[0].streamed_bytes / cold[0].streamed_bytes,
+                    "pack_setup_s": pack_s,
+                    "cold_plain_p50": pct(cold_ttft, 50), "cold_plain_p99": pct(cold_ttft, 99),
                     "warm_p50": pct(warm_ttft, 50), "warm_p99": pct(warm_ttft, 99),
-                    "cold_over_warm_p50": pct(cold_ttft, 50) / pct(warm_ttft, 50), "target_ratio": 1.2,
+                    "cold_plain_over_warm_p50": pct(cold_ttft, 50) / pct(warm_ttft, 50), "target_ratio": 1.2,
                     "cold_device_p50": pct([r.device_ms for r in cold], 50),
                     "stream_ms_p50": pct([r.stream_ms for r in cold], 50),
                     "streamed_bytes": cold[0].streamed_bytes, "stream_gbs_p50": stream_gbs,
