@@ -109,6 +109,8 @@ void launch_gather_vocab(const float* gathered, float* logits, int tp, int rows,
 void packed_sections(int64_t n, int64_t n_esc, int64_t* codes_off, int64_t* idx_off, int64_t* exp_off,
                      int64_t* total);
 void launch_unpack_bf16(void* dst, const void* packed, int64_t n, int e_base, int64_t n_esc, cudaStream_t st);
+void huff_sections(int64_t n, int64_t* lut_off, int64_t* offs_off, int64_t* words_off);
+void launch_unpack_huff(void* dst, const void* packed, int64_t n, cudaStream_t st);
 // Logits (fp32) for M rows and their argmax.
 void launch_argmax(const float* logits, int M, int V, int32_t* out, float* scratch, cudaStream_t st);
 

@@ -1,5 +1,14 @@
 // Lossless bf16 weight unpacking for the packed layer stream (cold start).
 //
+// Format 1 (Huffman, the default): lo[n] as below, then the exponents as a
+// length-limited (<= 12 bit) canonical Huffman code, LSB-first, in blocks of
+// 1024 weights whose bitstreams start on 32-bit words:
+//   lo [n] | lut [4096] u16 (symbol | length << 8, indexed by the next 12 bits)
+//        | block word offsets [ceil(n/1024)] u32 | words [] u32
+// ~10.6 bits per weight (the exponent entropy is ~2.6 bits). One thread
+// decodes one block through a shared-memory LUT and writes 16-byte vectors.
+//
+// Format 0 (fixed 4-bit codes):
 // A bf16 weight is sign(1) | exponent(8) | mantissa(7). Trained and
 // synthetic weights use a narrow band of exponents (entropy ~2.5 bits), so
 // the host image of each streamed range is stored as
@@ -51,6 +60,61 @@ __global__ void __launch_bounds__(256) unpack_bf16_kernel(uint16_t* __restrict__
   }
 }
 
+constexpr int kHuffBlock = 1024, kHuffBits = 12;
+
+__global__ void __launch_bounds__(128) unpack_huff_kernel(uint16_t* __restrict__ dst, const uint8_t* __restrict__ lo,
+                                                          const uint16_t* __restrict__ lut_g,
+                                                          const uint32_t* __restrict__ offs,
+                                                          const uint32_t* __restrict__ words, int64_t n) {
+  __shared__ uint16_t lut[1 << kHuffBits];
+  for (int i = threadIdx.x; i < (1 << kHuffBits); i += blockDim.x) lut[i] = lut_g[i];
+  __syncthreads();
+  const int64_t nb = (n + kHuffBlock - 1) / kHuffBlock;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint32_t* w = words + offs[b];
+  uint64_t buf = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+  int have = 64, next = 2;
+  const int64_t v0 = b * kHuffBlock;
+  const int cnt = (int)(n - v0 < kHuffBlock ? n - v0 : kHuffBlock);
+  const uint8_t* l = lo + v0;
+  uint16_t* d = dst + v0;
+  int v = 0;
+  for (; v + 8 <= cnt; v += 8) {
+    const uint2 L = *reinterpret_cast<const uint2*>(l + v);
+    uint32_t out[4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t ent = lut[buf & ((1u << kHuffBits) - 1)];
+      const int len = ent >> 8;
+      buf >>= len;
+      have -= len;
+      if (have < 32) {
+        buf |= (uint64_t)w[next++] << have;
+        have += 32;
+      }
+      const uint32_t lb = ((k < 4 ? L.x : L.y) >> (8 * (k & 3))) & 0xFFu;
+      const uint32_t bits = bf16_bits(lb, ent & 0xFFu);
+      if (k & 1)
+        out[k >> 1] |= bits << 16;
+      else
+        out[k >> 1] = bits;
+    }
+    *reinterpret_cast<uint4*>(d + v) = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+  for (; v < cnt; ++v) {  // last block's tail
+    const uint32_t ent = lut[buf & ((1u << kHuffBits) - 1)];
+    const int len = ent >> 8;
+    buf >>= len;
+    have -= len;
+    if (have < 32) {
+      buf |= (uint64_t)w[next++] << have;
+      have += 32;
+    }
+    d[v] = (uint16_t)bf16_bits(l[v], ent & 0xFFu);
+  }
+}
+
 // escaped values carry their own exponent (runs after the bulk pass)
 __global__ void __launch_bounds__(256) unpack_escapes_kernel(uint16_t* __restrict__ dst, const uint8_t* __restrict__ lo,
                                                              const uint32_t* __restrict__ idx,
@@ -71,6 +135,23 @@ void packed_sections(int64_t n, int64_t n_esc, int64_t* codes_off, int64_t* idx_
   *idx_off = packed_align16(*codes_off + (n + 1) / 2);
   *exp_off = packed_align16(*idx_off + 4 * n_esc);
   *total = packed_align16(*exp_off + n_esc);
+}
+
+void huff_sections(int64_t n, int64_t* lut_off, int64_t* offs_off, int64_t* words_off) {
+  *lut_off = packed_align16(n);
+  *offs_off = *lut_off + 2 * (1 << kHuffBits);
+  *words_off = packed_align16(*offs_off + 4 * ((n + kHuffBlock - 1) / kHuffBlock));
+}
+
+void launch_unpack_huff(void* dst, const void* packed, int64_t n, cudaStream_t st) {
+  int64_t lut_off, offs_off, words_off;
+  huff_sections(n, &lut_off, &offs_off, &words_off);
+  const uint8_t* p = static_cast<const uint8_t*>(packed);
+  const int64_t nb = (n + kHuffBlock - 1) / kHuffBlock;
+  count_launch();
+  unpack_huff_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(
+      static_cast<uint16_t*>(dst), p, reinterpret_cast<const uint16_t*>(p + lut_off),
+      reinterpret_cast<const uint32_t*>(p + offs_off), reinterpret_cast<const uint32_t*>(p + words_off), n);
 }
 
 void launch_unpack_bf16(void* dst, const void* packed, int64_t n, int e_base, int64_t n_esc, cudaStream_t st) {

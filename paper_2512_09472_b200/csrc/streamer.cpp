@@ -81,20 +81,23 @@ int ws_streamer_start_packed(ws_streamer* s, void* dst_base, const void* packed_
     const int64_t* d = desc + 6 * i;
     if (d[5] > half) WS_FAIL(WS_ERR_INVALID, "packed range %d (%lld B) exceeds the staging slot (%lld B)", i,
                              (long long)d[5], (long long)half);
-    if (d[3] < 0 || d[3] > 240) WS_FAIL(WS_ERR_INVALID, "exponent base out of range");
+    if (d[3] != -1 && (d[3] < 0 || d[3] > 240)) WS_FAIL(WS_ERR_INVALID, "exponent base out of range");
   }
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(copy_stream);
   cudaStream_t us = reinterpret_cast<cudaStream_t>(unpack_stream);
   WS_CUDA(cudaEventRecord(s->start, cs));
   for (int32_t i = 0; i < n; ++i) {
-    // desc[i] = {dst_offset, packed_offset, n_values, e_base, n_escapes, packed_bytes}
+    // desc[i] = {dst_offset, packed_offset, n_values, e_base (-1: Huffman), n_escapes, packed_bytes}
     const int64_t* d = desc + 6 * i;
     char* slot = static_cast<char*>(staging) + (i & 1) * half;
     if (i >= 2) WS_CUDA(cudaStreamWaitEvent(cs, s->done[i - 2], 0));  // slot free once range i-2 unpacked
     WS_CUDA(cudaMemcpyAsync(slot, static_cast<const char*>(packed_base) + d[1], (size_t)d[5], cudaMemcpyDefault, cs));
     WS_CUDA(cudaEventRecord(s->copied[i], cs));
     WS_CUDA(cudaStreamWaitEvent(us, s->copied[i], 0));
-    ws::launch_unpack_bf16(static_cast<char*>(dst_base) + d[0], slot, d[2], (int)d[3], d[4], us);
+    if (d[3] < 0)
+      ws::launch_unpack_huff(static_cast<char*>(dst_base) + d[0], slot, d[2], us);
+    else
+      ws::launch_unpack_bf16(static_cast<char*>(dst_base) + d[0], slot, d[2], (int)d[3], d[4], us);
     WS_CUDA(cudaEventRecord(s->done[i], us));
   }
   WS_CUDA(cudaGetLastError());
