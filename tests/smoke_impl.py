@@ -1,7 +1,8 @@
 """__graft_entry__.smoke(): one cold activation of the tiny model (BASELINE
 config 1: layer 0 + embedding prewarmed, 512-token prompt) through the worker
-API on cuda:0, checked against the CPU fp32 oracle; plus one memory switch
-whose ledger is checked against the reference-pinned ledger oracle."""
+API on cuda:0 over the packed (Huffman) layer stream, checked against the CPU
+fp32 oracle; plus one memory switch whose ledger is checked against the
+reference-pinned ledger oracle."""
 
 from __future__ import annotations
 
@@ -12,14 +13,16 @@ def run_smoke() -> None:
     from oracle import ledger as OL
     from oracle import llama_fp32 as O
     from paper_2512_09472_b200 import models as M
-    from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat
+    from paper_2512_09472_b200.weights import pack_stream, pinned_host_copy, synth_flat
     from paper_2512_09472_b200.worker import UniversalWorker
 
     assert torch.cuda.is_available(), "smoke needs cuda:0"
     cfg = M.TINY
     w = UniversalWorker(0, pool_pages=64, max_tokens=1024)
-    host = pinned_host_copy(synth_flat(cfg, seed=1, device="cuda"))
+    flat = synth_flat(cfg, seed=1, device="cuda")
+    host = pinned_host_copy(flat)
     w.register(cfg, host)
+    w.set_packed(cfg.name, pack_stream(cfg, flat))
     w.prewarm(cfg.name, layers=1)
     prompt = torch.randint(0, cfg.vocab, (512,), generator=torch.Generator().manual_seed(0),
                            dtype=torch.int32).pin_memory()
@@ -39,5 +42,7 @@ def run_smoke() -> None:
         [want[0], want[1], want[2], want[4]], (want, c.free_pages, c.kv_pages_mapped)
     w.release()
     w.close()
-    print(f"smoke ok: cold TTFT {res.ttft_ms:.2f} ms, token {res.token}, logits rel err {rel:.2e}, "
+    assert res.streamed_layers == cfg.layers - 1
+    print(f"smoke ok: cold TTFT {res.ttft_ms:.2f} ms (packed stream {res.streamed_bytes} B), token {res.token}, "
+          f"logits rel err {rel:.2e}, "
           f"switch {res.switch_ms*1e3:.0f} us host / {res.switch_kernel_ms*1e3:.1f} us kernel")
