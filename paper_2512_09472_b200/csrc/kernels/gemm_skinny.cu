@@ -512,7 +512,8 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // Enough units to occupy most SMs (gate/up: 112): one whole unit per CTA.
   // No unit is split, so no fix-up pass runs, and the ~25% of idle SMs cost
   // less than the fix-up: measured 4-9% faster decode steps (B = 1..64) than
-  // stream-K over all 148 SMs.
+  // stream-K over all 148 SMs. Below ~90 units whole units lose: one SM pulls
+  // ~64 GB/s, so 32-48 CTAs cannot stream at HBM rate (down: 57 vs 25 us).
   if (units * 10 >= kNumSMs * 6 && units <= kNumSMs) grid = units;
   if (e.mode == Epi::kRopeKV && units > grid) return false;  // <= 2 segments (partial slots) per CTA
   Scratch s;
