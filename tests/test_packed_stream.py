@@ -51,8 +51,8 @@ def test_pack_ratio_on_weight_like_values():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("huffman", [True, False])
-def test_packed_activation_matches_plain(cuda_device, huffman):
+@pytest.mark.parametrize("huffman,shape", [(True, "llama"), (False, "llama"), (True, "qwen"), (True, "phi")])
+def test_packed_activation_matches_plain(cuda_device, huffman, shape):
     """Cold activation of the tiny model from the packed stream: the slot
     holds exactly the bf16 image afterwards and the logits equal the plain
     (unpacked) stream's bit for bit."""
@@ -60,7 +60,9 @@ def test_packed_activation_matches_plain(cuda_device, huffman):
     from paper_2512_09472_b200.weights import pack_stream, pinned_host_copy, synth_flat
     from paper_2512_09472_b200.worker import UniversalWorker
 
-    cfg = M.TINY
+    cfg = {"llama": M.TINY,
+           "qwen": M.TINY.with_(name="tq", qkv_bias=True, rope_theta=1e6, rms_eps=1e-6),
+           "phi": M.TINY.with_(name="tp", heads=4, kv_heads=4, head_dim=96, hidden=384, rope_theta=1e4)}[shape]
     w = UniversalWorker(cuda_device, pool_pages=64, max_tokens=1024)
     try:
         flat = synth_flat(cfg, seed=5, device="cuda")
