@@ -212,7 +212,7 @@ def run_ours(args, rank, world, local_rank):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda")
+        t = torch.tensor([x], device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -425,7 +425,7 @@ def run_ours(args, rank, world, local_rank):
     clk_sum = clk.summary()
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
         v, sample, threads, secs = cpu_prefill_sample(cfg, S, min_seconds=args.cpu_seconds)
         cpu = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "port",
                "sample": sample + f"; {secs:.1f} s of CPU work", "cpu": _cpu_model()}
@@ -542,8 +542,15 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("WS_BENCH_ONE_GPU") == "1":
+            # test hook: every rank on cuda:0 over gloo, to exercise the
+            # multi-rank path (barriers, max-over-ranks) on a one-GPU box
+            local_rank = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
