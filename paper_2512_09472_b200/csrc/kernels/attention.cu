@@ -206,6 +206,17 @@ __global__ void __launch_bounds__(kWarps * 32) attn_prefill_kernel(const bf16* _
 }
 
 // ---------------------------------------------------------------- decode
+__device__ __forceinline__ void cluster_arrive_wait() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t local, int cta) {
+  uint32_t remote;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(cta));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
 // HBM-bound: every K/V byte of the context is read once per step. Work unit =
 // (key split, kv head, sequence); the CTA's 4 warps take interleaved 16-key
 // tiles of the split, each with its own 3-stage cp.async ring, so one SM keeps
@@ -215,8 +226,9 @@ __global__ void __launch_bounds__(kWarps * 32) attn_prefill_kernel(const bf16* _
 // unnormalised partial (m, l, O) per split; a combine kernel merges the splits.
 constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = 3;
 // Split the context only until there is one CTA per SM: more, shorter CTAs
-// (4 waves of 2 per SM) measured 5-7% slower at B = 16 / 64 (prologue and
-// merge per CTA); a single sequence still gets 64-key splits.
+// measured slower (B = 16 / 64 at ~4 / ~7 CTAs per SM: 4.32 -> 4.84 / 5.84 ->
+// 6.80 ms per step: prologue and merge per CTA); a single sequence still gets
+// 64-key splits.
 constexpr int kDecTargetCtas = kNumSMs;
 
 template <int HD>
@@ -232,7 +244,7 @@ template <int HD>
 __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
-    int n_splits, int split_keys, bf16* __restrict__ out) {
+    int n_splits, int split_keys, bf16* __restrict__ out, int in_cluster) {
   pdl_trigger();
   pdl_wait();
   using S = DecodeSmem<HD>;
@@ -249,9 +261,41 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
   const int32_t* bt = kv.block_tables + (int64_t)seqs[b] * kv.max_blocks;
   const int64_t k_plane = kv.plane(layer, 0, kvh), v_plane = kv.plane(layer, 1, kvh);
 
-  auto load = [&](int stage, int t) {
+  // tpb a multiple of the 16-key tile (every model but the 70B): a tile is one
+  // contiguous 4 KB run of K (and of V) inside one page. Each lane holds the
+  // page of one of the warp's next 32 tiles (a coalesced block-table read per
+  // 32 tiles, issued 32 tiles ahead), so no tile load waits on a block-table
+  // lookup or a division by tpb.
+  const bool aligned = kv.tpb % kDecKeys == 0;
+  auto page_of = [&](int j) -> int32_t {
+    return j < my_n ? bt[(k_lo + (warp + j * kDecWarps) * kDecKeys) / kv.tpb] : 0;
+  };
+  int32_t pg_cur = 0, pg_nxt = 0;
+  if (aligned) {
+    pg_cur = page_of(lane);
+    pg_nxt = page_of(32 + lane);
+  }
+  auto load = [&](int stage, int j) {
     bf16* tk = sw + stage * 2 * S::kTile;
     bf16* tv = tk + S::kTile;
+    const int t = warp + j * kDecWarps;
+    if (aligned) {
+      if ((j & 31) == 0 && j > 0) {
+        pg_cur = pg_nxt;
+        pg_nxt = page_of(j + 32 + lane);
+      }
+      const int32_t page = __shfl_sync(0xffffffffu, pg_cur, j & 31);
+      const int key0 = k_lo + t * kDecKeys, rows = k_hi - key0;
+      const bf16* tile = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) +
+                         (int64_t)(key0 % kv.tpb) * HD;
+#pragma unroll
+      for (int i = lane; i < kDecKeys * CH; i += 32) {
+        const int r = i / CH, c = i % CH;
+        cp_async16(tk + r * ST + c * 8, tile + k_plane + i * 8, r < rows);
+        cp_async16(tv + r * ST + c * 8, tile + v_plane + i * 8, r < rows);
+      }
+      return;
+    }
 #pragma unroll
     for (int i = lane; i < kDecKeys * CH; i += 32) {
       const int r = i / CH, c = i % CH;
@@ -267,7 +311,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
   };
 #pragma unroll
   for (int s = 0; s < kDecStages - 1; ++s) {
-    if (s < my_n) load(s, warp + s * kDecWarps);
+    if (s < my_n) load(s, s);
     cp_async_commit();
   }
 
@@ -295,7 +339,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
 
   for (int it = 0; it < my_n; ++it) {
     const int nx = it + kDecStages - 1;
-    if (nx < my_n) load(nx % kDecStages, warp + nx * kDecWarps);
+    if (nx < my_n) load(nx % kDecStages, nx);
     cp_async_commit();
     cp_async_wait<kDecStages - 1>();
     __syncwarp();
@@ -410,13 +454,38 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
       out[(int64_t)b * heads * HD + (kvh * G + g) * HD + d] = f2bf(l > 0.f ? acc / l : 0.f);
       continue;
     }
-    float* dst = part + (((int64_t)b * heads + kvh * G + g) * n_splits + split) * (HD + 2);
+    // cluster: this CTA's partial stays in its shared memory; otherwise global scratch
+    float* dst = in_cluster ? red + kDecWarps * 16 * (HD + 2) + g * (HD + 2)
+                            : part + (((int64_t)b * heads + kvh * G + g) * n_splits + split) * (HD + 2);
     dst[d] = acc;
     if (d == 0) {
       dst[HD] = mx;
       dst[HD + 1] = l;
     }
   }
+  if (!in_cluster) return;
+  // The splits of one (kv head, sequence) form a thread-block cluster: after
+  // the cluster barrier every CTA merges a slice of the G x HD outputs from
+  // all splits' partials over distributed shared memory — no scratch round
+  // trip through L2 and no combine launch.
+  cluster_arrive_wait();
+  const uint32_t cp = smem_u32(red + kDecWarps * 16 * (HD + 2));
+  for (int idx = split * kDecWarps * 32 + threadIdx.x; idx < G * HD; idx += n_splits * kDecWarps * 32) {
+    const int g = idx / HD, d = idx % HD;
+    const uint32_t row = cp + 4u * (uint32_t)(g * (HD + 2));
+    float mx = -INFINITY;
+    for (int c = 0; c < n_splits; ++c) mx = fmaxf(mx, ld_dsmem_f32(row + 4u * HD, c));
+    float acc = 0.f, l = 0.f;
+    for (int c = 0; c < n_splits; ++c) {
+      const float m = ld_dsmem_f32(row + 4u * HD, c);
+      if (m == -INFINITY) continue;
+      const float f = exp2f(m - mx);
+      acc += f * ld_dsmem_f32(row + 4u * d, c);
+      l += f * ld_dsmem_f32(row + 4u * (HD + 1), c);
+    }
+    out[(int64_t)b * heads * HD + (kvh * G + g) * HD + d] = f2bf(l > 0.f ? acc / l : 0.f);
+  }
+  cluster_arrive_wait();  // no CTA leaves while its partial may still be read
 }
 
 // out[b, h] = sum_p w_p o_p / sum_p w_p l_p with w_p = 2^(m_p - max m). Warp 0
@@ -468,6 +537,61 @@ void prefill_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int s
                                                            heads, scale * 1.4426950408889634f);
 }
 
+// Largest split cluster the decode kernel may use: 16 when the non-portable
+// size schedules at this shared-memory footprint, else the portable 8;
+// WS_DEC_CLUSTER=0 disables clusters (scratch + combine kernel, A/B).
+template <typename K>
+int decode_cluster_limit(K kernel, int smem) {
+  if (const char* e = std::getenv("WS_DEC_CLUSTER")) return std::atoi(e);
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 8;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(16, 1, 1);
+  cfg.blockDim = dim3(kDecWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  return n > 0 ? 16 : 8;
+}
+
+// launch_pdl plus an optional (cluster, 1, 1) cluster shape
+template <typename... KArgs, typename... Args>
+void launch_decode(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, int cluster, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n++].val.clusterDim.z = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int HD>
 void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
                  const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
@@ -478,16 +602,22 @@ void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const 
     cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     attr = true;
   }
+  static int max_cluster = -1;
+  if (max_cluster < 0) max_cluster = decode_cluster_limit(attn_decode_kernel<HD>, S::kBytes);
   // enough (split, kv head, seq) units to fill the SMs; >= 64 keys per split
   const int units = n_seqs * kv.kv_heads;
   int n_splits = std::max(1, std::min({(kDecTargetCtas + units - 1) / units, (max_ctx + 63) / 64, kMaxSplits}));
   const int split_keys = ((max_ctx + n_splits - 1) / n_splits + kDecKeys - 1) / kDecKeys * kDecKeys;
   n_splits = (max_ctx + split_keys - 1) / split_keys;
+  // few splits (small batches): one cluster per (kv head, sequence) merges
+  // them in distributed shared memory; many (one long context): scratch + combine
+  const int in_cluster = n_splits > 1 && n_splits <= max_cluster;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
   count_launch();
-  launch_pdl(attn_decode_kernel<HD>, grid, dim3(kDecWarps * 32), S::kBytes, st, qkv, kv, layer, seqs, ctx, heads,
-             scale * 1.4426950408889634f, scratch, n_splits, split_keys, out);
-  if (n_splits > 1) {
+  launch_decode(attn_decode_kernel<HD>, grid, dim3(kDecWarps * 32), S::kBytes, in_cluster ? n_splits : 0, st, qkv,
+                kv, layer, seqs, ctx, heads, scale * 1.4426950408889634f, scratch, n_splits, split_keys, out,
+                in_cluster);
+  if (n_splits > 1 && !in_cluster) {
     count_launch();
     launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
   }

@@ -322,10 +322,12 @@ _DECODE_SHAPES = {
 
 
 @pytest.mark.parametrize("shape", sorted(_DECODE_SHAPES))
-@pytest.mark.parametrize("lens", [[700], [3 + 61 * i for i in range(12)], [20 + 3 * i for i in range(40)]])
+@pytest.mark.parametrize("lens", [[700], [2000], [3 + 61 * i for i in range(12)], [20 + 3 * i for i in range(40)]])
 def test_decode_gqa_shapes_match_oracle(lib, shape, lens):
     """Decode over the paged pool at head_dim 128/96 and GQA groups 4/7/1:
-    split-K attention (per-warp partials + combine) and the skinny tcgen05
+    split-K attention (splits merged in a thread-block cluster, or — 32
+    splits of the 2000-token context — through scratch + the combine kernel)
+    and the skinny tcgen05
     GEMMs (1, 12 and 40 rows), 4 steps against the fp32 oracle with KV past."""
     from paper_2512_09472_b200 import models as M
 
