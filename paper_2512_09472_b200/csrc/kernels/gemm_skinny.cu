@@ -13,7 +13,7 @@
 // whatever N and K are. A CTA's range is a list of segments (one per unit it
 // touches); only its first and last segment can cover part of a unit.
 //
-//   warp 0 lane 0  TMA producer: W block(s) 128x64 + A Mp x64 per stage (SW128)
+//   warp 0 lane 0  TMA producer: sub x (W block(s) 128x64 + A Mp x64) per stage (SW128)
 //   warp 1 lane 0  MMA issuer; double-buffered TMEM accumulators [128][NB*Mp]
 //   warp 2         TMEM allocation
 //   warps 4-7      epilogue: TMEM lane i = weight row i, columns = batch rows
@@ -42,12 +42,14 @@ namespace {
 
 using namespace dev;
 
-constexpr int kRows = 128, kBK = 64, kThreads = 256;
-constexpr int kW_BYTES = kRows * kBK * 2;  // 16 KiB weight tile
-constexpr int kSmemBudget = 200 * 1024;    // TMA ring, one CTA per SM
+constexpr int kRows = 128, kBox = 64, kThreads = 256;
+constexpr int kW_BYTES = kRows * kBox * 2;  // 16 KiB weight box (128 rows x 128 B, SW128)
+constexpr int kSmemBudget = 216 * 1024;     // TMA ring, one CTA per SM
 
+// An iteration covers sub (1, 2 or 4) boxes of 64 k-columns: the producer
+// fetches sub x 128 contiguous bytes of every weight row per issue.
 struct SkinnyArgs {
-  int M, N, K, Mp, stages, stage_bytes, total_iters;
+  int M, N, K, Mp, stages, stage_bytes, total_iters, sub, kbs;
   float* partial;      // [grid][2][NB*128][Mp]
 };
 
@@ -99,7 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Mp = args.Mp, G = gridDim.x, total = args.total_iters;
-  const int kbs = args.K / kBK;
+  const int kbs = args.kbs, sub = args.sub, kBK = kBox * sub;
+  const uint32_t a_off = NB * sub * kW_BYTES, a_box = args.Mp * kBox * 2;
   const int it0 = it_begin(blockIdx.x, G, total), it1 = it_begin(blockIdx.x + 1, G, total);
   const uint32_t acc_cols = NB * Mp;
   uint32_t tmem_cols = 32;
@@ -142,7 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_expect_tx(full(k), args.stage_bytes);
 #pragma unroll
       for (int j = 0; j < NB; ++j)
-        tc::tma_load_2d(sa + j * kW_BYTES, &map_w, full(k), kb * kBK, (unit * NB + j) * kRows);
+        for (int h = 0; h < sub; ++h)
+          tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox, (unit * NB + j) * kRows);
     }
   }
   pdl_wait();  // global data produced by earlier kernels from here on
@@ -151,7 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ===== TMA producer =====
       for (int k = 0; k < pre; ++k)
-        tc::tma_load_2d(base + k * args.stage_bytes + NB * kW_BYTES, &map_a, full(k), ((it0 + k) % kbs) * kBK, 0);
+        for (int h = 0; h < sub; ++h)
+          tc::tma_load_2d(base + k * args.stage_bytes + a_off + h * a_box, &map_a, full(k),
+                          ((it0 + k) % kbs) * kBK + h * kBox, 0);
       int stage = pre == S ? 0 : pre;
       uint32_t phase = pre == S ? 1 : 0;
       for (int it = it0 + pre; it < it1; ++it) {
@@ -161,8 +167,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_expect_tx(full(stage), args.stage_bytes);
 #pragma unroll
         for (int j = 0; j < NB; ++j)
-          tc::tma_load_2d(sa + j * kW_BYTES, &map_w, full(stage), kb * kBK, (unit * NB + j) * kRows);
-        tc::tma_load_2d(sa + NB * kW_BYTES, &map_a, full(stage), kb * kBK, 0);
+          for (int h = 0; h < sub; ++h)
+            tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
+                            (unit * NB + j) * kRows);
+        for (int h = 0; h < sub; ++h)
+          tc::tma_load_2d(sa + a_off + h * a_box, &map_a, full(stage), kb * kBK + h * kBox, 0);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -185,13 +194,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(full(stage), phase);
           tc::fence_after();
           const uint32_t sa = base + stage * args.stage_bytes;
-          const uint64_t db = tc::sdesc_sw128(sa + NB * kW_BYTES);
+          for (int h = 0; h < sub; ++h) {
+            const uint64_t db = tc::sdesc_sw128(sa + a_off + h * a_box);
 #pragma unroll
-          for (int j = 0; j < NB; ++j) {
-            const uint64_t da = tc::sdesc_sw128(sa + j * kW_BYTES);
+            for (int j = 0; j < NB; ++j) {
+              const uint64_t da = tc::sdesc_sw128(sa + (j * sub + h) * kW_BYTES);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle row
-              tc::mma_f16(d + j * Mp, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i > it) | k);
+              for (int k = 0; k < kBox / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle row
+                tc::mma_f16(d + j * Mp, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i > it) | h | k);
+            }
           }
           tc::commit(empty(stage));
           if (++stage == S) {
@@ -274,7 +285,7 @@ template <int MODE>
 __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEpilogue& ep, int G, int unit, int i,
                                               int q4) {
   constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
-  const int Mp = args.Mp, kbs = args.K / kBK, total = args.total_iters;
+  const int Mp = args.Mp, kbs = args.kbs, total = args.total_iters;
   const int c_first = cta_of((int64_t)unit * kbs, G, total);
   const int c_last = cta_of((int64_t)(unit + 1) * kbs - 1, G, total);
   if (c_first == c_last) return;  // whole unit: stored by the GEMM
@@ -336,7 +347,7 @@ __global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant
                                                            const __grid_constant__ TcEpilogue ep, int G) {
   pdl_trigger();
   pdl_wait();
-  const int kbs = args.K / kBK, total = args.total_iters;
+  const int kbs = args.kbs, total = args.total_iters;
   const int q4 = blockIdx.y;  // batch rows 4*q4 .. 4*q4+3
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int unit = x / kRows, i = x % kRows;
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(256) skinny_rope_fixup_kernel(const __grid_con
   pdl_trigger();
   pdl_wait();
   const KvGeom& kv = ep.kv;
-  const int Mp = args.Mp, kbs = args.K / kBK, total = args.total_iters;
+  const int Mp = args.Mp, kbs = args.kbs, total = args.total_iters;
   const int quads = Mp / 4, hd = kv.head_dim, half = hd / 2;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int unit = (int)(t / (64 * quads));
@@ -422,7 +433,7 @@ bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) 
   if (!d) return false;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)kBox, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return d->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -466,7 +477,7 @@ void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs&
   }
   count_launch();
   launch_pdl(gemm_skinny_kernel<MODE>, dim3(grid), dim3(kThreads), (size_t)smem, st, mw, ma, a, e);
-  const int kbs = a.K / kBK, units = a.total_iters / kbs;
+  const int kbs = a.kbs, units = a.total_iters / kbs;
   if constexpr (MODE == (int)Epi::kRopeKV) {
     const int64_t threads = (int64_t)units * 64 * (a.Mp / 4);
     count_launch();
@@ -493,17 +504,27 @@ bool gemm_skinny_enabled() {
 }
 
 bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st) {
-  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBK || K % kBK) return false;
+  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBox || K % kBox) return false;
   if (e.mode == Epi::kRopeKV && e.kv.head_dim != 64 && e.kv.head_dim != 128) return false;  // heads tile 128 rows
   const int NB = e.mode == Epi::kSwiGLU ? 2 : 1;
   if (N % (kRows * NB)) return false;
-  const int units = N / (kRows * NB), kbs = K / kBK;
+  // Widest iteration (up to 4 boxes = 512 contiguous bytes of each weight row
+  // per TMA issue) that divides K and still leaves a 3-stage ring: the weight
+  // stream then reaches HBM as long runs instead of 128 B pieces of 128 rows
+  // 8+ KB apart (B = 1 / 16 / 64 decode: 4.20 / 4.50 / 6.07 -> 4.04 / 4.27 /
+  // 5.89 ms per step).
+  const int mp = (M + 15) / 16 * 16;
+  int sub = 4;
+  while (sub > 1 && (K % (sub * kBox) || 3 * sub * (NB * kW_BYTES + mp * kBox * 2) > kSmemBudget)) sub /= 2;
+  const int units = N / (kRows * NB), kbs = K / (kBox * sub);
   SkinnyArgs a{};
+  a.sub = sub;
+  a.kbs = kbs;
   a.M = M;
   a.N = N;
   a.K = K;
   a.Mp = (M + 15) / 16 * 16;
-  a.stage_bytes = NB * kW_BYTES + a.Mp * kBK * 2;
+  a.stage_bytes = sub * (NB * kW_BYTES + a.Mp * kBox * 2);
   a.stages = std::max(2, std::min(12, kSmemBudget / a.stage_bytes));
   a.total_iters = units * kbs;
   const int smem = a.stages * a.stage_bytes + 1024 + 256;

@@ -275,7 +275,8 @@ def _swiglu_ref(A, W):
 
 
 @pytest.mark.parametrize("M", [1, 7, 16, 40, 128])
-@pytest.mark.parametrize("N,K", [(256, 512), (4096, 4096), (1024, 14336), (6144, 256), (12800, 512), (25600, 256)])
+@pytest.mark.parametrize("N,K", [(256, 512), (4096, 4096), (1024, 14336), (6144, 256), (12800, 512), (25600, 256),
+                                 (1024, 320)])
 def test_gemm_skinny_against_fp32(lib, M, N, K):
     """impl 4 forces the decode-shaped swap-AB split-K tcgen05 kernel; every
     epilogue, and the split-K reduction is deterministic (bit-identical reruns).
