@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--pool-pages", type=int, default=24576)
     ap.add_argument("--json", default="")
+    ap.add_argument("--graphed", action="store_true", help="CUDA-graph replay (UniversalWorker.decode_graphed)")
     a = ap.parse_args()
     cfg = M.ALL[a.model]
     batches = [int(b) for b in a.batch.split(",")]
@@ -70,7 +71,8 @@ def main():
             with torch.cuda.stream(w.compute):
                 e0.record(w.compute)
                 torch.cuda.nvtx.range_push(f"decode_b{B}")
-                _, nt = w.decode(sd, pos, tok, a.ctx + 1)
+                step = w.decode_graphed if a.graphed else w.decode
+                _, nt = step(sd, pos, tok, a.ctx + 1)
                 torch.cuda.nvtx.range_pop()
                 e1.record(w.compute)
             torch.cuda.synchronize()
