@@ -542,11 +542,11 @@ void prefill_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int s
 // WS_DEC_CLUSTER=0 disables clusters (scratch + combine kernel, A/B).
 template <typename K>
 int decode_cluster_limit(K kernel, int smem) {
-  if (const char* e = std::getenv("WS_DEC_CLUSTER")) return std::atoi(e);
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-    cudaGetLastError();
-    return 8;
-  }
+  const bool non_portable = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                            cudaSuccess;
+  if (!non_portable) cudaGetLastError();
+  if (const char* e = std::getenv("WS_DEC_CLUSTER")) return std::min(std::atoi(e), non_portable ? 16 : 8);
+  if (!non_portable) return 8;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(16, 1, 1);
   cfg.blockDim = dim3(kDecWarps * 32);
