@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=24576)
     ap.add_argument("--json", default="")
     ap.add_argument("--graphed", action="store_true", help="CUDA-graph replay (UniversalWorker.decode_graphed)")
+    ap.add_argument("--back-to-back", action="store_true", help="time all steps between two events (as bench.py)")
     a = ap.parse_args()
     cfg = M.ALL[a.model]
     batches = [int(b) for b in a.batch.split(",")]
@@ -80,6 +81,17 @@ def main():
             tok = nt.clone()
         t = sorted(times[3:])
         ms = t[len(t) // 2]
+        if a.back_to_back:
+            step = w.decode_graphed if a.graphed else w.decode
+            with torch.cuda.stream(w.compute):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(w.compute)
+                for i in range(a.steps):
+                    pos = torch.full((B,), a.ctx, dtype=torch.int32, device="cuda")
+                    _, tok = step(sd, pos, tok, a.ctx + 1)
+                e1.record(w.compute)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.steps
         nbytes = weight_bytes + B * (a.ctx + 1) * kv_tok
         r = {"batch": B, "ctx": a.ctx, "ms_per_step": ms, "min_ms": t[0], "tokens_per_s": B / ms * 1e3,
              "algorithmic_gb": nbytes / 1e9, "achieved_gbs": nbytes / ms / 1e6}
