@@ -53,6 +53,26 @@ struct SkinnyArgs {
   float* partial;      // [grid][2][NB*128][Mp]
 };
 
+// Residual producer of a folded RMSNorm (norm_role 1): x_new is final (one
+// writer per element); store it, the next projection's A = bf16(x_new * g),
+// and the warp's sum of squares over its 32 consecutive columns (a fixed
+// shuffle tree: deterministic). Called by all 32 lanes of a warp.
+__device__ __forceinline__ void norm_produce(const TcEpilogue& ep, int N, int b, int col, float x_new, float* dst) {
+  *dst = x_new;
+  ep.norm_out[(int64_t)b * N + col] = f2bf(x_new * bf2f(ep.norm_g[col]));
+  const float sq = warp_sum(x_new * x_new);
+  if ((threadIdx.x & 31) == 0) ep.row_ss[(int64_t)b * (N / 32) + col / 32] = sq;
+}
+
+// Consumer of a folded RMSNorm (norm_role 2): rsqrt(mean(x^2) + eps) of batch
+// row b from the producer's partials, one warp per row, fixed summation order.
+__device__ __forceinline__ float norm_row_scale(const TcEpilogue& ep, int b) {
+  const int n = ep.norm_d / 32;
+  float a = 0.f;
+  for (int k = threadIdx.x & 31; k < n; k += 32) a += __ldcg(ep.row_ss + (int64_t)b * n + k);
+  return rsqrtf(warp_sum(a) / (float)ep.norm_d + ep.norm_eps);
+}
+
 template <int MODE>
 __device__ __forceinline__ void store_out(const TcEpilogue& ep, const SkinnyArgs& a, int row, const float* v,
                                           int c0) {
@@ -63,9 +83,14 @@ __device__ __forceinline__ void store_out(const TcEpilogue& ep, const SkinnyArgs
     if (b >= a.M) break;
     float x = v[j];
     if constexpr (MODE == (int)Epi::kAddF32) {
-      // exactly one add per element (whole unit or reduced sum): deterministic,
-      // and a fire-and-forget reduction instead of a load-add-store chain
-      atomicAdd(static_cast<float*>(ep.C) + (int64_t)b * a.N + row, x);
+      float* dst = static_cast<float*>(ep.C) + (int64_t)b * a.N + row;
+      if (ep.norm_role == 1) {
+        norm_produce(ep, a.N, b, row, *dst + x, dst);
+      } else {
+        // exactly one add per element (whole unit or reduced sum): deterministic,
+        // and a fire-and-forget reduction instead of a load-add-store chain
+        atomicAdd(dst, x);
+      }
     } else if constexpr (MODE == (int)Epi::kStoreF32) {
       static_cast<float*>(ep.C)[(int64_t)b * a.N + row] = x;
     } else if constexpr (MODE == (int)Epi::kSwiGLU) {
@@ -224,6 +249,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = threadIdx.x - 128;
     const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int64_t slot_floats = (int64_t)NB * kRows * Mp;
+    float* s_row = reinterpret_cast<float*>(smem_raw + (bars + 8 * (2 * S + 6) - raw));  // [128] row scales
+    if (ep.norm_role == 2) {
+      for (int b = warp - 4; b < args.M; b += 4) {
+        const float sc = norm_row_scale(ep, b);
+        if (lane == 0) {
+          s_row[b] = sc;
+          if (blockIdx.x == 0) ep.row_scale[b] = sc;  // for the fix-up kernels
+        }
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the 4 epilogue warps
+    }
     int acc = 0, seg = 0;
     uint32_t acc_phase = 0;
     for (int it = it0; it < it1; ++seg) {
@@ -245,8 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           float f[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            f[q] = __uint_as_float(v[0][q]);
-            if constexpr (NB == 2) f[q] = f[q] / (1.f + __expf(-f[q])) * __uint_as_float(v[NB - 1][q]);
+            const float sc = ep.norm_role == 2 ? (c + q < args.M ? s_row[c + q] : 0.f) : 1.f;
+            f[q] = __uint_as_float(v[0][q]) * sc;
+            if constexpr (NB == 2) f[q] = f[q] / (1.f + __expf(-f[q])) * (__uint_as_float(v[NB - 1][q]) * sc);
           }
           store_out<MODE>(ep, args, out_row, f, c);
         } else {
@@ -318,8 +355,16 @@ __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEp
       }
   }
   float v[4] = {sum[0].x, sum[0].y, sum[0].z, sum[0].w};
+  float u[4] = {sum[NB - 1].x, sum[NB - 1].y, sum[NB - 1].z, sum[NB - 1].w};
+  if (ep.norm_role == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sc = q4 * 4 + k < args.M ? ep.row_scale[q4 * 4 + k] : 0.f;
+      v[k] *= sc;
+      u[k] *= sc;
+    }
+  }
   if constexpr (NB == 2) {
-    const float u[4] = {sum[1].x, sum[1].y, sum[1].z, sum[1].w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
   }
@@ -329,7 +374,11 @@ __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEp
     const int b = q4 * 4 + k;
     if (b >= args.M) break;
     if constexpr (MODE == (int)Epi::kAddF32) {
-      static_cast<float*>(ep.C)[(int64_t)b * args.N + row] += v[k];
+      float* dst = static_cast<float*>(ep.C) + (int64_t)b * args.N + row;
+      if (ep.norm_role == 1)
+        norm_produce(ep, args.N, b, row, *dst + v[k], dst);
+      else
+        *dst += v[k];
     } else if constexpr (MODE == (int)Epi::kStoreF32) {
       static_cast<float*>(ep.C)[(int64_t)b * args.N + row] = v[k];
     } else if constexpr (MODE == (int)Epi::kSwiGLU) {
@@ -396,7 +445,15 @@ __global__ void __launch_bounds__(256) skinny_rope_fixup_kernel(const __grid_con
       sb.x += pb[k].x; sb.y += pb[k].y; sb.z += pb[k].z; sb.w += pb[k].w;
     }
   }
-  const float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
+  float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
+  if (ep.norm_role == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sc = q4 * 4 + k < args.M ? ep.row_scale[q4 * 4 + k] : 0.f;
+      va[k] *= sc;
+      vb[k] *= sc;
+    }
+  }
   const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
   const int hs = col_a / hd;  // head slot in [0, H + 2KV)
   const bool is_v = hs >= ep.heads + kv.kv_heads, is_k = !is_v && hs >= ep.heads;
@@ -503,11 +560,17 @@ bool gemm_skinny_enabled() {
   return g_skinny_mode == 1;
 }
 
+bool gemm_skinny_supported(int M, int N, int K, Epi mode) {
+  return gemm_skinny_enabled() && M >= 1 && M <= 128 && K >= kBox && K % kBox == 0 &&
+         N % (kRows * (mode == Epi::kSwiGLU ? 2 : 1)) == 0;
+}
+
 bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st) {
-  if (!gemm_skinny_enabled() || M < 1 || M > 128 || K < kBox || K % kBox) return false;
+  if (!gemm_skinny_supported(M, N, K, e.mode)) return false;
   if (e.mode == Epi::kRopeKV && e.kv.head_dim != 64 && e.kv.head_dim != 128) return false;  // heads tile 128 rows
+  if (e.norm_role == 1 && e.mode != Epi::kAddF32) return false;
+  if (e.norm_role == 2 && (e.mode == Epi::kAddF32 || e.mode == Epi::kStoreF32)) return false;
   const int NB = e.mode == Epi::kSwiGLU ? 2 : 1;
-  if (N % (kRows * NB)) return false;
   // Widest iteration (up to 4 boxes = 512 contiguous bytes of each weight row
   // per TMA issue) that divides K and still leaves a 3-stage ring: the weight
   // stream then reaches HBM as long runs instead of 128 B pieces of 128 rows
@@ -527,7 +590,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   a.stage_bytes = sub * (NB * kW_BYTES + a.Mp * kBox * 2);
   a.stages = std::max(2, std::min(12, kSmemBudget / a.stage_bytes));
   a.total_iters = units * kbs;
-  const int smem = a.stages * a.stage_bytes + 1024 + 256;
+  const int smem = a.stages * a.stage_bytes + 1024 + 1024;  // align slack + barriers + TMEM slot + [128] row scales
   // one CTA per SM, >= 2 k-blocks each
   int grid = std::max(1, std::min(kNumSMs, a.total_iters / 2));
   // Enough units to occupy most SMs (gate/up: 112): one whole unit per CTA.

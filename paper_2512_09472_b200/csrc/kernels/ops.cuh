@@ -76,6 +76,19 @@ struct TcEpilogue {
   int layer = 0, heads = 0, seq0 = 0, pos0 = 0;
   const int32_t* seq_arr = nullptr;
   const int32_t* pos_arr = nullptr;
+  // Decode RMSNorm folded across a residual GEMM and the next projection
+  // (skinny path only). norm_role 1 (kAddF32 producer): besides x += A.W^T,
+  // write norm_out = bf16(x_new * norm_g) and per-(row, 32-column group)
+  // sums of squares row_ss[M][norm_d / 32]. norm_role 2 (consumer): A is
+  // norm_out, and every output row is scaled by rsqrt(sum(row_ss) / norm_d +
+  // norm_eps) before bias / RoPE / SwiGLU — exact by linearity; row_scale[M]
+  // carries the scales from the GEMM to its fix-up kernels.
+  int norm_role = 0, norm_d = 0;
+  float norm_eps = 0.f;
+  const bf16* norm_g = nullptr;
+  bf16* norm_out = nullptr;
+  float* row_ss = nullptr;
+  float* row_scale = nullptr;
 };
 bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim);
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
@@ -96,6 +109,9 @@ bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, 
 // HBM bound. Returns false (nothing launched) outside that envelope or when
 // disabled with WS_SKINNY=0.
 bool gemm_skinny_enabled();
+// launch_gemm_skinny's shape envelope (kRopeKV aside, which may also decline
+// when the weight has more units than the grid has CTAs)
+bool gemm_skinny_supported(int M, int N, int K, Epi mode);
 bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st);
 // Legacy CUDA-core GEMV for M <= 16 (fallback when the skinny kernel does not apply).
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,

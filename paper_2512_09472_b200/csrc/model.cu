@@ -72,7 +72,7 @@ Layout make_layout(const ws_model_config& c) {
 }
 
 struct Workspace {
-  int64_t x, h, qkv, attn, gu, act, hl, seqs, scratch, partial, shard_logits, gathered, total;
+  int64_t x, h, qkv, attn, gu, act, hl, seqs, scratch, partial, shard_logits, gathered, norm_ss, norm_scale, total;
 };
 
 int head_rows(const ws_model_config& c) { return c.lm_head_rows > 0 ? c.lm_head_rows : c.vocab; }
@@ -103,6 +103,11 @@ Workspace make_ws(const ws_model_config& c, int T) {
   w.partial = take(tp ? (int64_t)T * d * 4 : 0);
   w.shard_logits = take(tp ? (int64_t)decode_cap(T) * head_rows(c) * 4 : 0);
   w.gathered = take(tp ? (int64_t)decode_cap(T) * c.vocab * 4 : 0);
+  // decode RMSNorm folded into the skinny GEMMs (<= 128 rows): per-(row,
+  // 32-column group) sums of squares and the per-row scales
+  const int64_t fold_rows = T < 128 ? T : 128;
+  w.norm_ss = take(fold_rows * (d / 32) * 4);
+  w.norm_scale = take(fold_rows * 4);
   w.total = off;
   return w;
 }
@@ -132,14 +137,14 @@ void gemm(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N,
 
 // QKV projection + RoPE + paged KV append. One tcgen05 launch with the fused
 // epilogue when the shape allows it, else GEMM then the rope_kv kernel.
-void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws::bf16* b, int rows,
+bool qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws::bf16* b, int rows,
               const ws::KvGeom& kv, int layer, int seq0, int pos0, const int32_t* seqs, const int32_t* pos,
-              ws::bf16* qkv, cudaStream_t st) {
+              ws::bf16* qkv, cudaStream_t st, const ws::TcEpilogue* norm = nullptr) {
   using namespace ws;
   const ws_model_config& c = m->cfg;
   const int q = (c.heads + 2 * c.kv_heads) * c.head_dim;
   if (!(m->gemm_impl & 1)) {
-    TcEpilogue e;
+    TcEpilogue e = norm ? *norm : TcEpilogue{};
     e.mode = Epi::kRopeKV;
     e.C = qkv;
     e.bias = b;
@@ -154,28 +159,40 @@ void qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
     // a few decode rows: skinny split-K GEMM with RoPE/KV-append in its fix-up
     // (one launch less; for more rows the plain fix-up + rope kernel is faster)
     static const bool fuse = !(getenv("WS_FUSE_ROPE") && getenv("WS_FUSE_ROPE")[0] == '0');
-    if (fuse && rows <= 8 && launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return;
+    if (fuse && rows <= 8 && launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return true;
+    if (norm) {  // folded RMSNorm: the skinny GEMM applies the row scales, then RoPE / KV append
+      e.mode = b ? Epi::kBiasBf16 : Epi::kStoreBf16;
+      e.C = qkv;
+      if (!launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return false;  // no unscaled fallback
+      launch_rope_kv(qkv, m->rope, kv, layer, rows, c.heads, seqs, pos, seq0, pos0, st);
+      return true;
+    }
     if (rows >= 16 && !(rows <= 128 && gemm_skinny_enabled()) && launch_gemm_tc_epi(h, w, rows, q, c.hidden, e, st))
-      return;
+      return true;
   }
+  if (norm) return false;
   gemm(m, h, w, rows, q, c.hidden, b ? Epi::kBiasBf16 : Epi::kStoreBf16, qkv, b, st);
   launch_rope_kv(qkv, m->rope, kv, layer, rows, c.heads, seqs, pos, seq0, pos0, st);
+  return true;
 }
 
 // gate/up projection + SwiGLU (fused epilogue on the tcgen05 path).
-void gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int rows, ws::bf16* gu,
-                    ws::bf16* act, cudaStream_t st) {
+bool gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int rows, ws::bf16* gu,
+                    ws::bf16* act, cudaStream_t st, const ws::TcEpilogue* norm = nullptr) {
   using namespace ws;
   const ws_model_config& c = m->cfg;
   if (!(m->gemm_impl & 1)) {
-    TcEpilogue e;
+    TcEpilogue e = norm ? *norm : TcEpilogue{};
     e.mode = Epi::kSwiGLU;
     e.C = act;
-    if (rows <= 128 && launch_gemm_skinny(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;  // decode
-    if (rows >= 16 && launch_gemm_tc_epi(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return;
+    if (rows <= 128 && launch_gemm_skinny(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return true;  // decode
+    if (norm) return false;  // folded RMSNorm: no unscaled fallback
+    if (rows >= 16 && launch_gemm_tc_epi(h, w, rows, 2 * c.ffn, c.hidden, e, st)) return true;
   }
+  if (norm) return false;
   gemm(m, h, w, rows, 2 * c.ffn, c.hidden, Epi::kStoreBf16, gu, nullptr, st);
   launch_silu_mul(gu, act, rows, c.ffn, st);
+  return true;
 }
 
 // Row-parallel projection + residual add: x += A.B^T, summed over the TP group
@@ -401,19 +418,65 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   const float scale = 1.0f / std::sqrt((float)c.head_dim);
   const Layout& L = m->layout;
 
+  // Fold the per-layer RMSNorms into the skinny GEMMs: each residual GEMM
+  // (O, down) also writes bf16(x * g) and row sums of squares, the next
+  // projection (gate/up, next layer's QKV) scales its rows by rsqrt(mean +
+  // eps) — two launches fewer per layer. Graph-replayed 8B steps, ctx 1024:
+  // B = 1 / 4 / 16 3.96 / 4.12 / 4.31 -> 3.79 / 4.05 / 4.23 ms; at B = 64 the
+  // per-CTA scale reduction and the load-add-store residual cost more than
+  // the launches (5.77 -> 5.86 ms), so only up to 16 rows. Off for TP (the
+  // residual is summed across ranks first), the legacy GEMMs, shapes outside
+  // the skinny kernel, and WS_FOLD_NORM=0 (A/B).
+  static const bool fold_env = !(getenv("WS_FOLD_NORM") && getenv("WS_FOLD_NORM")[0] == '0');
+  const bool fold = fold_env && n <= 16 && !m->comm && !(m->gemm_impl & 1) &&
+                    gemm_skinny_supported(n, d, o, Epi::kAddF32) &&
+                    gemm_skinny_supported(n, d, c.ffn, Epi::kAddF32) &&
+                    gemm_skinny_supported(n, q, d, Epi::kStoreBf16) &&
+                    gemm_skinny_supported(n, 2 * c.ffn, d, Epi::kSwiGLU);
+  TcEpilogue np, nc;  // producer / consumer halves of a folded norm
+  if (fold) {
+    np.mode = Epi::kAddF32;
+    np.C = x;
+    np.norm_role = 1;
+    np.norm_out = h;
+    np.row_ss = reinterpret_cast<float*>(wsb + w.norm_ss);
+    nc.norm_role = 2;
+    nc.norm_d = d;
+    nc.norm_eps = c.rms_eps;
+    nc.row_ss = np.row_ss;
+    nc.row_scale = reinterpret_cast<float*>(wsb + w.norm_scale);
+  }
   launch_embed(tokens, W<bf16>(wts, L.embed), x, n, d, st);
   launch_rmsnorm(x, W<bf16>(wts, L.layers[0].attn_norm), h, n, d, c.rms_eps, st);
   for (int l = 0; l < c.layers; ++l) {
     const auto& Ly = L.layers[l];
-    qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
-             pos, qkv, st);
+    if (!qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
+                  pos, qkv, st, fold && l > 0 ? &nc : nullptr))
+      WS_FAIL(WS_ERR_CUDA, "folded-norm QKV GEMM declined");
     launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
+    const bool last = l + 1 == c.layers;
+    if (fold) {
+      np.norm_g = W<bf16>(wts, Ly.ffn_norm);
+      if (!launch_gemm_skinny(attn, W<bf16>(wts, Ly.wo), n, d, o, np, st)) WS_FAIL(WS_ERR_CUDA, "folded O GEMM");
+      if (!gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st, &nc))
+        WS_FAIL(WS_ERR_CUDA, "folded-norm gate/up GEMM declined");
+      if (!last) {
+        np.norm_g = W<bf16>(wts, L.layers[l + 1].attn_norm);
+        if (!launch_gemm_skinny(act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, np, st))
+          WS_FAIL(WS_ERR_CUDA, "folded down GEMM");
+        continue;
+      }
+      // last layer: plain residual + the final norm kernel for the lm_head rows
+      if (int e = row_parallel_norm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial,
+                                    W<bf16>(wts, L.final_norm), hl, st))
+        return e;
+      continue;
+    }
     if (int e = row_parallel_norm(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x, partial, W<bf16>(wts, Ly.ffn_norm), h,
                                   st))
       return e;
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);
     // the residual after the FFN feeds the next layer's attn_norm (or the final norm)
-    const bool last = l + 1 == c.layers;
     if (int e = row_parallel_norm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial,
                                   W<bf16>(wts, last ? L.final_norm : L.layers[l + 1].attn_norm), last ? hl : h, st))
       return e;
