@@ -65,12 +65,22 @@ __device__ __forceinline__ void norm_produce(const TcEpilogue& ep, int N, int b,
 }
 
 // Consumer of a folded RMSNorm (norm_role 2): rsqrt(mean(x^2) + eps) of batch
-// row b from the producer's partials, one warp per row, fixed summation order.
+// row b from the producer's partials; one thread per row, every load issued
+// before the (fixed-order) adds.
 __device__ __forceinline__ float norm_row_scale(const TcEpilogue& ep, int b) {
   const int n = ep.norm_d / 32;
+  const float* p = ep.row_ss + (int64_t)b * n;
   float a = 0.f;
-  for (int k = threadIdx.x & 31; k < n; k += 32) a += __ldcg(ep.row_ss + (int64_t)b * n + k);
-  return rsqrtf(warp_sum(a) / (float)ep.norm_d + ep.norm_eps);
+  int k = 0;
+  for (; k + 16 <= n; k += 16) {
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(p + k) + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+  }
+  for (; k < n; ++k) a += __ldcg(p + k);
+  return rsqrtf(a / (float)ep.norm_d + ep.norm_eps);
 }
 
 template <int MODE>
@@ -251,12 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t slot_floats = (int64_t)NB * kRows * Mp;
     float* s_row = reinterpret_cast<float*>(smem_raw + (bars + 8 * (2 * S + 6) - raw));  // [128] row scales
     if (ep.norm_role == 2) {
-      for (int b = warp - 4; b < args.M; b += 4) {
-        const float sc = norm_row_scale(ep, b);
-        if (lane == 0) {
-          s_row[b] = sc;
-          if (blockIdx.x == 0) ep.row_scale[b] = sc;  // for the fix-up kernels
-        }
+      if (i < args.M) {
+        const float sc = norm_row_scale(ep, i);
+        s_row[i] = sc;
+        if (blockIdx.x == 0) ep.row_scale[i] = sc;  // for the fix-up kernels
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the 4 epilogue warps
     }

@@ -422,9 +422,9 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   // (O, down) also writes bf16(x * g) and row sums of squares, the next
   // projection (gate/up, next layer's QKV) scales its rows by rsqrt(mean +
   // eps) — two launches fewer per layer. Graph-replayed 8B steps, ctx 1024:
-  // B = 1 / 4 / 16 3.96 / 4.12 / 4.31 -> 3.79 / 4.05 / 4.23 ms; at B = 64 the
-  // per-CTA scale reduction and the load-add-store residual cost more than
-  // the launches (5.77 -> 5.86 ms), so only up to 16 rows. Off for TP (the
+  // B = 1 / 4 / 16 3.96 / 4.12 / 4.31 -> 3.79 / 4.05 / 4.23 ms; no gain at
+  // B = 32 and 0.6% slower at B = 64 (the load-add-store residual and the
+  // wider fix-up epilogues cost what the launches saved), so up to 16 rows. Off for TP (the
   // residual is summed across ranks first), the legacy GEMMs, shapes outside
   // the skinny kernel, and WS_FOLD_NORM=0 (A/B).
   static const bool fold_env = !(getenv("WS_FOLD_NORM") && getenv("WS_FOLD_NORM")[0] == '0');
