@@ -233,6 +233,27 @@ int ws_nccl_unique_id(uint8_t* out, int32_t n);  /* n >= 128 */
 int ws_comm_create(const uint8_t* unique_id, int32_t rank, int32_t nranks, int32_t device, ws_comm** out);
 int ws_comm_destroy(ws_comm* comm);
 
+/* Allreduce (fp32 sum) over peer memory: every rank exports one buffer
+ * (cudaIpcMemHandle_t, 64 bytes) and maps every peer's; a call copies the
+ * local partial into the rank's own buffer and one kernel signals the peers,
+ * waits for theirs, and sums all ranks' partials in rank order (bit-identical
+ * on every rank). Replaces ncclAllReduce for the row-parallel O / down
+ * partials (TP, config 4; reference: the NCCL-free cost model of
+ * PAPER.md:686-689 / SURVEY §8e). Every rank must issue the same sequence of
+ * calls. */
+typedef struct ws_peer ws_peer;
+int ws_peer_buffer_bytes(int64_t max_count, int64_t* out);
+int ws_peer_buffer_alloc(int64_t max_count, void** ptr, uint8_t* handle, int32_t handle_bytes);
+int ws_peer_buffer_free(void* ptr);
+int ws_peer_buffer_open(const uint8_t* handle, void** ptr);
+int ws_peer_buffer_close(void* ptr);
+int ws_peer_create(int32_t rank, int32_t world, void* const* bufs, int64_t max_count, ws_peer** out);
+int ws_peer_destroy(ws_peer* p);
+int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream);
+/* Route a TP communicator's allreduces of <= max_count floats through `peer`
+ * (NULL restores ncclAllReduce); the lm_head allgather stays on NCCL. */
+int ws_comm_set_peer(ws_comm* comm, ws_peer* peer, int64_t max_count);
+
 /* Weight layout of one (TP-partition of a) model inside its slot: byte
  * offsets, every tensor 256-byte aligned. offsets_out receives
  * [embed, final_norm, lm_head, total] then per layer

@@ -111,6 +111,15 @@ SIGNATURES: dict[str, list] = {
     "ws_streamer_start_packed": [vp, vp, vp, P(i64), i32, vp, i64, vp, vp],
     "ws_streamer_wait": [vp, i32, vp],
     "ws_streamer_times": [vp, P(f32), i32],
+    "ws_peer_buffer_bytes": [i64, P(i64)],
+    "ws_peer_buffer_alloc": [i64, P(vp), P(C.c_uint8), i32],
+    "ws_peer_buffer_free": [vp],
+    "ws_peer_buffer_open": [P(C.c_uint8), P(vp)],
+    "ws_peer_buffer_close": [vp],
+    "ws_peer_create": [i32, i32, P(vp), i64, P(vp)],
+    "ws_peer_destroy": [vp],
+    "ws_peer_allreduce_f32": [vp, vp, i64, vp],
+    "ws_comm_set_peer": [vp, vp, i64],
 }
 
 lib.ws_last_error.restype = C.c_char_p

@@ -1,0 +1,175 @@
+// Allreduce (sum, fp32) over peer memory for the TP row-parallel partials
+// — the NVSwitch replacement for ncclAllReduce on
+// the O / down outputs.
+//
+// Every rank owns one IPC-exported buffer: a flag row (one epoch word per
+// source rank) and two data slots. A call copies the rank's partial into slot
+// (epoch & 1) of its own buffer, then one kernel
+//   1. block 0 publishes `epoch` into every peer's flag row (system-scope
+//      release after a system fence),
+//   2. every CTA waits until all peers' words in its own flag row reached
+//      `epoch` (system-scope acquire),
+//   3. sums the W slots in rank order over peer loads (NVLink reads on a
+//      multi-GPU node), grid-stride with 16 B accesses.
+// The sum order is the same on every rank, so all ranks hold bit-identical
+// results. Two slots make a reused buffer safe: a rank can only run one
+// epoch ahead of the slowest peer (it needs that peer's flag for the next
+// epoch, which the peer writes only after finishing its previous reduce), so
+// slot (epoch & 1) is never overwritten while a peer still reads it.
+// The grid never exceeds the resident CTA count (the waits would otherwise
+// starve block 0).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+
+namespace {
+
+constexpr int kMaxPeers = 8;
+constexpr int64_t kFlagBytes = 4096;  // flag row + padding; data slots follow
+
+int64_t slot_bytes(int64_t max_count) { return (max_count * 4 + 255) / 256 * 256; }
+
+struct PeerArgs {
+  const float* data[kMaxPeers];  // slot (epoch & 1) of every rank's buffer
+  uint32_t* flags[kMaxPeers];    // every rank's flag row
+  int rank, world;
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
+                                                             int64_t n, uint32_t epoch) {
+  if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
+    __threadfence_system();
+    st_release_sys(a.flags[threadIdx.x] + a.rank, epoch);
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t* mine = a.flags[a.rank];
+    for (int p = 0; p < a.world; ++p) {
+      if (p == a.rank) continue;
+      while ((int32_t)(ld_acquire_sys(mine + p) - epoch) < 0) __nanosleep(128);
+    }
+  }
+  __syncthreads();
+  const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 s = __ldcv(reinterpret_cast<const float4*>(a.data[0]) + i);
+    for (int p = 1; p < a.world; ++p) {
+      const float4 v = __ldcv(reinterpret_cast<const float4*>(a.data[p]) + i);
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[i] = s;
+  }
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float s = __ldcv(a.data[0] + i);
+    for (int p = 1; p < a.world; ++p) s += __ldcv(a.data[p] + i);
+    out[i] = s;
+  }
+}
+
+}  // namespace
+
+struct ws_peer {
+  int rank = 0, world = 1, device = 0;
+  int64_t max_count = 0;
+  uint32_t epoch = 0;
+  std::vector<char*> bufs;  // every rank's buffer base (own + IPC-opened)
+};
+
+extern "C" {
+
+int ws_peer_buffer_bytes(int64_t max_count, int64_t* out) {
+  if (max_count < 1 || !out) WS_FAIL(WS_ERR_INVALID, "bad peer buffer size");
+  *out = kFlagBytes + 2 * slot_bytes(max_count);
+  return WS_OK;
+}
+
+int ws_peer_buffer_alloc(int64_t max_count, void** ptr, uint8_t* handle, int32_t handle_bytes) {
+  if (!ptr || !handle || handle_bytes < (int32_t)sizeof(cudaIpcMemHandle_t))
+    WS_FAIL(WS_ERR_INVALID, "peer buffer: need a %d-byte handle", (int)sizeof(cudaIpcMemHandle_t));
+  int64_t bytes = 0;
+  if (int e = ws_peer_buffer_bytes(max_count, &bytes)) return e;
+  void* p = nullptr;
+  WS_CUDA(cudaMalloc(&p, (size_t)bytes));
+  WS_CUDA(cudaMemset(p, 0, kFlagBytes));
+  cudaIpcMemHandle_t h;
+  WS_CUDA(cudaIpcGetMemHandle(&h, p));
+  memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return WS_OK;
+}
+
+int ws_peer_buffer_free(void* ptr) {
+  if (ptr) WS_CUDA(cudaFree(ptr));
+  return WS_OK;
+}
+
+int ws_peer_buffer_open(const uint8_t* handle, void** ptr) {
+  if (!handle || !ptr) WS_FAIL(WS_ERR_INVALID, "bad peer handle");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  WS_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return WS_OK;
+}
+
+int ws_peer_buffer_close(void* ptr) {
+  if (ptr) WS_CUDA(cudaIpcCloseMemHandle(ptr));
+  return WS_OK;
+}
+
+int ws_peer_create(int32_t rank, int32_t world, void* const* bufs, int64_t max_count, ws_peer** out) {
+  if (!out || !bufs || world < 1 || world > kMaxPeers || rank < 0 || rank >= world || max_count < 1)
+    WS_FAIL(WS_ERR_INVALID, "bad peer group (rank %d of %d, at most %d)", rank, world, kMaxPeers);
+  auto* p = new ws_peer;
+  p->rank = rank;
+  p->world = world;
+  p->max_count = max_count;
+  cudaGetDevice(&p->device);
+  for (int r = 0; r < world; ++r) p->bufs.push_back(static_cast<char*>(bufs[r]));
+  *out = p;
+  return WS_OK;
+}
+
+int ws_peer_destroy(ws_peer* p) {
+  delete p;
+  return WS_OK;
+}
+
+int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
+  if (!p || !buf || count < 0 || count > p->max_count || reinterpret_cast<uintptr_t>(buf) % 16)
+    WS_FAIL(WS_ERR_INVALID, "bad peer allreduce (count <= max_count, 16-byte aligned buffer)");
+  if (count == 0) return WS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint32_t epoch = ++p->epoch;
+  const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * slot_bytes(p->max_count);
+  PeerArgs a{};
+  a.rank = p->rank;
+  a.world = p->world;
+  for (int r = 0; r < p->world; ++r) {
+    a.data[r] = reinterpret_cast<const float*>(p->bufs[r] + slot);
+    a.flags[r] = reinterpret_cast<uint32_t*>(p->bufs[r]);
+  }
+  WS_CUDA(cudaMemcpyAsync(p->bufs[p->rank] + slot, buf, (size_t)count * 4, cudaMemcpyDeviceToDevice, st));
+  const int64_t want = (count / 4 + 255) / 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ws::kNumSMs, want));
+  ws::count_launch();
+  peer_allreduce_kernel<<<grid, 256, 0, st>>>(a, buf, count, epoch);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+}  // extern "C"

@@ -70,11 +70,14 @@ const Nccl* nccl() {
 struct ws_comm {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1, device = 0;
+  ws_peer* peer = nullptr;  // peer-memory allreduce (csrc/peer.cu); null = ncclAllReduce
+  int64_t peer_max = 0;
 };
 
 namespace ws {
 
 int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st) {
+  if (c->peer && count <= c->peer_max) return ws_peer_allreduce_f32(c->peer, buf, count, st);
   const Nccl* n = nccl();
   if (!n) return WS_ERR_INVALID;
   ncclResult_t r = n->allReduce(buf, buf, (size_t)count, ncclFloat32, ncclSum, c->comm, st);
@@ -96,6 +99,13 @@ int comm_size(const ws_comm* c) { return c->nranks; }
 }  // namespace ws
 
 extern "C" {
+
+int ws_comm_set_peer(ws_comm* comm, ws_peer* peer, int64_t max_count) {
+  if (!comm) WS_FAIL(WS_ERR_INVALID, "null communicator");
+  comm->peer = peer;
+  comm->peer_max = peer ? max_count : 0;
+  return WS_OK;
+}
 
 int ws_nccl_unique_id(uint8_t* out, int32_t n) {
   if (n < 128) WS_FAIL(WS_ERR_INVALID, "unique id buffer needs 128 bytes");

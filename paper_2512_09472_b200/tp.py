@@ -134,7 +134,19 @@ class TpGroup:
         dist.broadcast_object_list(obj, src=0)
         return cls(dist.get_rank(), dist.get_world_size(), device, obj[0])
 
+    def attach_peer(self, max_count: int, group=None) -> None:
+        """Route the row-parallel allreduces (<= max_count floats) through the
+        peer-memory allreduce (csrc/peer.cu) instead of NCCL."""
+        from .peer import PeerAllreduce
+
+        self.peer = PeerAllreduce(max_count, group)
+        N.call("ws_comm_set_peer", self.handle, self.peer._h, self.peer.max_count)
+
     def close(self):
+        if getattr(self, "peer", None) is not None:
+            N.call("ws_comm_set_peer", self.handle, None, 0)
+            self.peer.close()
+            self.peer = None
         if self.handle:
             N.fns["ws_comm_destroy"](self.handle)
             self.handle = None

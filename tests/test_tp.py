@@ -100,7 +100,8 @@ def test_tp2_gloo_shards_reproduce_full_model():
 @pytest.mark.gpu
 def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     """The NCCL TP path (fp32 partials + allreduce + residual add, lm_head
-    allgather + reorder) on a 1-rank communicator == the fused single-GPU path."""
+    allgather + reorder) on a 1-rank communicator == the fused single-GPU path,
+    and == the same path with the allreduces on the peer-memory kernel."""
     from paper_2512_09472_b200.weights import pinned_host_copy
     from paper_2512_09472_b200.worker import UniversalWorker
 
@@ -108,9 +109,11 @@ def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     host = pinned_host_copy(synth_flat(cfg, seed=2, device="cuda"))
     prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(1), dtype=torch.int32)
     outs = []
-    for use_tp in (False, True):
+    for use_tp in (False, True, "peer"):
         w = UniversalWorker(cuda_device, pool_pages=64, max_tokens=512)
         grp = TP.TpGroup(0, 1, cuda_device, TP.TpGroup.unique_id()) if use_tp else None
+        if use_tp == "peer":  # row-parallel allreduces through the peer-memory kernel
+            grp.attach_peer(512 * cfg.hidden)
         w.register(cfg, host, tp=grp)
         w.prewarm(cfg.name, layers=cfg.layers)
         r = w.activate_instance(cfg.name, prompt.pin_memory())
@@ -119,6 +122,7 @@ def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
         w.close()
         if grp:
             grp.close()
-    assert outs[0][0] == outs[1][0]
+    assert outs[0][0] == outs[1][0] == outs[2][0]
     rel = ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item()
     assert rel < 1e-3, rel
+    assert torch.equal(outs[1][1], outs[2][1])  # one rank: both allreduces are the identity
