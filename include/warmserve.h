@@ -250,6 +250,12 @@ int ws_peer_buffer_close(void* ptr);
 int ws_peer_create(int32_t rank, int32_t world, void* const* bufs, int64_t max_count, ws_peer** out);
 int ws_peer_destroy(ws_peer* p);
 int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream);
+/* Fused form for a row-parallel projection: the GEMM writes its fp32 partial
+ * straight into the rank's next exported slot (ws_peer_next_slot), then
+ * ws_peer_reduce_add_f32 does x += sum over ranks in one kernel — no staging
+ * copy and no separate residual-add launch. */
+int ws_peer_next_slot(ws_peer* p, float** slot);
+int ws_peer_reduce_add_f32(ws_peer* p, float* x, int64_t count, void* stream);
 /* Route a TP communicator's allreduces of <= max_count floats through `peer`
  * (NULL restores ncclAllReduce); the lm_head allgather stays on NCCL. */
 int ws_comm_set_peer(ws_comm* comm, ws_peer* peer, int64_t max_count);

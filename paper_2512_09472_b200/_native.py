@@ -120,6 +120,8 @@ SIGNATURES: dict[str, list] = {
     "ws_peer_destroy": [vp],
     "ws_peer_allreduce_f32": [vp, vp, i64, vp],
     "ws_comm_set_peer": [vp, vp, i64],
+    "ws_peer_next_slot": [vp, P(vp)],
+    "ws_peer_reduce_add_f32": [vp, vp, i64, vp],
 }
 
 lib.ws_last_error.restype = C.c_char_p

@@ -204,6 +204,14 @@ int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M,
     gemm(m, A, B, M, N, K, Epi::kAddF32, x, nullptr, st);
     return WS_OK;
   }
+  if (ws_peer* peer = comm_peer(m->comm, (int64_t)M * N)) {
+    // peer memory: the GEMM writes its partial straight into this rank's
+    // exported slot, one kernel sums all ranks' slots into the residual
+    float* slot = nullptr;
+    if (int e = ws_peer_next_slot(peer, &slot)) return e;
+    gemm(m, A, B, M, N, K, Epi::kStoreF32, slot, nullptr, st);
+    return ws_peer_reduce_add_f32(peer, x, (int64_t)M * N, st);
+  }
   gemm(m, A, B, M, N, K, Epi::kStoreF32, partial, nullptr, st);
   if (int e = comm_allreduce_f32(m->comm, partial, (int64_t)M * N, st)) return e;
   launch_add_f32(x, partial, (int64_t)M * N, st);

@@ -48,6 +48,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+template <bool ACC>
 __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
                                                              int64_t n, uint32_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
@@ -72,12 +73,16 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
       s.z += v.z;
       s.w += v.w;
     }
+    if constexpr (ACC) {  // out += sum (the residual add of a row-parallel projection)
+      const float4 o = reinterpret_cast<const float4*>(out)[i];
+      s = make_float4(o.x + s.x, o.y + s.y, o.z + s.z, o.w + s.w);
+    }
     reinterpret_cast<float4*>(out)[i] = s;
   }
   for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float s = __ldcv(a.data[0] + i);
     for (int p = 1; p < a.world; ++p) s += __ldcv(a.data[p] + i);
-    out[i] = s;
+    out[i] = ACC ? out[i] + s : s;
   }
 }
 
@@ -149,11 +154,9 @@ int ws_peer_destroy(ws_peer* p) {
   return WS_OK;
 }
 
-int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
-  if (!p || !buf || count < 0 || count > p->max_count || reinterpret_cast<uintptr_t>(buf) % 16)
-    WS_FAIL(WS_ERR_INVALID, "bad peer allreduce (count <= max_count, 16-byte aligned buffer)");
-  if (count == 0) return WS_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+// One epoch: out = (ACC ? out : 0) + sum of every rank's slot (epoch & 1);
+// the caller's partial must already sit in its own slot.
+static int run_epoch(ws_peer* p, float* out, int64_t count, bool acc, cudaStream_t st) {
   const uint32_t epoch = ++p->epoch;
   const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * slot_bytes(p->max_count);
   PeerArgs a{};
@@ -163,13 +166,44 @@ int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
     a.data[r] = reinterpret_cast<const float*>(p->bufs[r] + slot);
     a.flags[r] = reinterpret_cast<uint32_t*>(p->bufs[r]);
   }
-  WS_CUDA(cudaMemcpyAsync(p->bufs[p->rank] + slot, buf, (size_t)count * 4, cudaMemcpyDeviceToDevice, st));
   const int64_t want = (count / 4 + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ws::kNumSMs, want));
   ws::count_launch();
-  peer_allreduce_kernel<<<grid, 256, 0, st>>>(a, buf, count, epoch);
+  if (acc)
+    peer_allreduce_kernel<true><<<grid, 256, 0, st>>>(a, out, count, epoch);
+  else
+    peer_allreduce_kernel<false><<<grid, 256, 0, st>>>(a, out, count, epoch);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
+}
+
+static bool bad_args(const ws_peer* p, const float* buf, int64_t count) {
+  return !p || !buf || count < 0 || count > p->max_count || reinterpret_cast<uintptr_t>(buf) % 16;
+}
+
+int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
+  if (bad_args(p, buf, count))
+    WS_FAIL(WS_ERR_INVALID, "bad peer allreduce (count <= max_count, 16-byte aligned buffer)");
+  if (count == 0) return WS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* slot = nullptr;
+  if (int e = ws_peer_next_slot(p, &slot)) return e;
+  WS_CUDA(cudaMemcpyAsync(slot, buf, (size_t)count * 4, cudaMemcpyDeviceToDevice, st));
+  return run_epoch(p, buf, count, false, st);
+}
+
+int ws_peer_next_slot(ws_peer* p, float** slot) {
+  if (!p || !slot) WS_FAIL(WS_ERR_INVALID, "bad peer slot query");
+  const uint32_t next = p->epoch + 1;
+  *slot = reinterpret_cast<float*>(p->bufs[p->rank] + kFlagBytes + (int64_t)(next & 1) * slot_bytes(p->max_count));
+  return WS_OK;
+}
+
+int ws_peer_reduce_add_f32(ws_peer* p, float* x, int64_t count, void* stream) {
+  if (bad_args(p, x, count))
+    WS_FAIL(WS_ERR_INVALID, "bad peer reduce-add (count <= max_count, 16-byte aligned buffer)");
+  if (count == 0) return WS_OK;
+  return run_epoch(p, x, count, true, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

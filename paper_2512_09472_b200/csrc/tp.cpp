@@ -85,6 +85,8 @@ int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st) {
   return WS_OK;
 }
 
+ws_peer* comm_peer(const ws_comm* c, int64_t count) { return c->peer && count <= c->peer_max ? c->peer : nullptr; }
+
 int comm_allgather_f32(ws_comm* c, const float* send, float* recv, int64_t count, cudaStream_t st) {
   const Nccl* n = nccl();
   if (!n) return WS_ERR_INVALID;

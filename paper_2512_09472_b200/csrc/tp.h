@@ -8,6 +8,9 @@
 namespace ws {
 int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st);
 int comm_allgather_f32(ws_comm* c, const float* send, float* recv, int64_t count, cudaStream_t st);
+// the communicator's peer-memory allreduce if one is attached and covers
+// `count` floats, else null (NCCL path)
+ws_peer* comm_peer(const ws_comm* c, int64_t count);
 int comm_rank(const ws_comm* c);
 int comm_size(const ws_comm* c);
 }  // namespace ws

@@ -56,6 +56,23 @@ class PeerAllreduce:
         N.call("ws_peer_allreduce_f32", self._h, C.c_void_p(t.data_ptr()), t.numel(), C.c_void_p(st.cuda_stream))
         return t
 
+    def next_slot(self, count: int, device: int | None = None) -> torch.Tensor:
+        """fp32 view of this rank's exported slot for the next call: write the
+        partial here, then reduce_add_ (no staging copy)."""
+        from .devmem import view
+
+        p = C.c_void_p()
+        N.call("ws_peer_next_slot", self._h, C.byref(p))
+        return view(p.value, (count,), torch.float32, torch.cuda.current_device() if device is None else device)
+
+    def reduce_add_(self, x: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """x += sum over ranks of the partials each rank wrote into next_slot()."""
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise ValueError("reduce_add_ takes a contiguous fp32 CUDA tensor")
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        N.call("ws_peer_reduce_add_f32", self._h, C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(st.cuda_stream))
+        return x
+
     def close(self) -> None:
         if self._h:
             torch.cuda.synchronize()

@@ -48,6 +48,17 @@ def _worker(rank, world, port, q):
             got = t.cpu()
             if not torch.equal(got, want):
                 bad.append((step, n, (got - want).abs().max().item()))
+        # fused form: partial written straight into the exported slot, x += sum
+        for step, n in enumerate([4096 * 8 + 5, 1 << 20, 3]):
+            x = _inputs(9, n, 50 + step).cuda()
+            pa.next_slot(n).copy_(_inputs(rank, n, 100 + step).cuda())
+            pa.reduce_add_(x)
+            s = _inputs(0, n, 100 + step)
+            for r in range(1, world):
+                s = s + _inputs(r, n, 100 + step)
+            want = _inputs(9, n, 50 + step) + s
+            if not torch.equal(x.cpu(), want):
+                bad.append(("fused", n, (x.cpu() - want).abs().max().item()))
         with pytest.raises(Exception):
             pa.allreduce_(torch.zeros(8, device="cuda", dtype=torch.float64))
         pa.close()
