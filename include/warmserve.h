@@ -256,6 +256,12 @@ int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream);
  * copy and no separate residual-add launch. */
 int ws_peer_next_slot(ws_peer* p, float** slot);
 int ws_peer_reduce_add_f32(ws_peer* p, float* x, int64_t count, void* stream);
+/* recv[r * count + i] = rank r's send[i] (the vocab-parallel lm_head shards). */
+int ws_peer_allgather_f32(ws_peer* p, const float* send, float* recv, int64_t count, void* stream);
+/* A TP communicator with no NCCL behind it: every collective on `peer`
+ * (calls above max_count floats fail). */
+int ws_comm_create_peer(int32_t rank, int32_t nranks, int32_t device, ws_peer* peer, int64_t max_count,
+                        ws_comm** out);
 /* Route a TP communicator's allreduces of <= max_count floats through `peer`
  * (NULL restores ncclAllReduce); the lm_head allgather stays on NCCL. */
 int ws_comm_set_peer(ws_comm* comm, ws_peer* peer, int64_t max_count);

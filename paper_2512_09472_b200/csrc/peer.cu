@@ -48,7 +48,8 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-template <bool ACC>
+// MODE 0: out = sum, 1: out += sum, 2: allgather (out[r * n + i] = slot_r[i])
+template <int MODE>
 __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
                                                              int64_t n, uint32_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
@@ -64,6 +65,17 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
   }
   __syncthreads();
   const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  if constexpr (MODE == 2) {
+    for (int p = 0; p < a.world; ++p) {
+      float* dst = out + (int64_t)p * n;
+      const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (vec ? n4 : 0); i += stride)
+        reinterpret_cast<float4*>(dst)[i] = __ldcv(reinterpret_cast<const float4*>(a.data[p]) + i);
+      for (int64_t i = (vec ? n4 * 4 : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = __ldcv(a.data[p] + i);
+    }
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     float4 s = __ldcv(reinterpret_cast<const float4*>(a.data[0]) + i);
     for (int p = 1; p < a.world; ++p) {
@@ -73,7 +85,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
       s.z += v.z;
       s.w += v.w;
     }
-    if constexpr (ACC) {  // out += sum (the residual add of a row-parallel projection)
+    if constexpr (MODE == 1) {  // out += sum (the residual add of a row-parallel projection)
       const float4 o = reinterpret_cast<const float4*>(out)[i];
       s = make_float4(o.x + s.x, o.y + s.y, o.z + s.z, o.w + s.w);
     }
@@ -82,7 +94,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
   for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float s = __ldcv(a.data[0] + i);
     for (int p = 1; p < a.world; ++p) s += __ldcv(a.data[p] + i);
-    out[i] = ACC ? out[i] + s : s;
+    out[i] = MODE == 1 ? out[i] + s : s;
   }
 }
 
@@ -156,7 +168,7 @@ int ws_peer_destroy(ws_peer* p) {
 
 // One epoch: out = (ACC ? out : 0) + sum of every rank's slot (epoch & 1);
 // the caller's partial must already sit in its own slot.
-static int run_epoch(ws_peer* p, float* out, int64_t count, bool acc, cudaStream_t st) {
+static int run_epoch(ws_peer* p, float* out, int64_t count, int mode, cudaStream_t st) {
   const uint32_t epoch = ++p->epoch;
   const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * slot_bytes(p->max_count);
   PeerArgs a{};
@@ -169,10 +181,12 @@ static int run_epoch(ws_peer* p, float* out, int64_t count, bool acc, cudaStream
   const int64_t want = (count / 4 + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ws::kNumSMs, want));
   ws::count_launch();
-  if (acc)
-    peer_allreduce_kernel<true><<<grid, 256, 0, st>>>(a, out, count, epoch);
+  if (mode == 1)
+    peer_allreduce_kernel<1><<<grid, 256, 0, st>>>(a, out, count, epoch);
+  else if (mode == 2)
+    peer_allreduce_kernel<2><<<grid, 256, 0, st>>>(a, out, count, epoch);
   else
-    peer_allreduce_kernel<false><<<grid, 256, 0, st>>>(a, out, count, epoch);
+    peer_allreduce_kernel<0><<<grid, 256, 0, st>>>(a, out, count, epoch);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
@@ -189,7 +203,18 @@ int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
   float* slot = nullptr;
   if (int e = ws_peer_next_slot(p, &slot)) return e;
   WS_CUDA(cudaMemcpyAsync(slot, buf, (size_t)count * 4, cudaMemcpyDeviceToDevice, st));
-  return run_epoch(p, buf, count, false, st);
+  return run_epoch(p, buf, count, 0, st);
+}
+
+int ws_peer_allgather_f32(ws_peer* p, const float* send, float* recv, int64_t count, void* stream) {
+  if (bad_args(p, send, count) || !recv)
+    WS_FAIL(WS_ERR_INVALID, "bad peer allgather (count <= max_count, 16-byte aligned send buffer)");
+  if (count == 0) return WS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* slot = nullptr;
+  if (int e = ws_peer_next_slot(p, &slot)) return e;
+  WS_CUDA(cudaMemcpyAsync(slot, send, (size_t)count * 4, cudaMemcpyDeviceToDevice, st));
+  return run_epoch(p, recv, count, 2, st);
 }
 
 int ws_peer_next_slot(ws_peer* p, float** slot) {
@@ -203,7 +228,7 @@ int ws_peer_reduce_add_f32(ws_peer* p, float* x, int64_t count, void* stream) {
   if (bad_args(p, x, count))
     WS_FAIL(WS_ERR_INVALID, "bad peer reduce-add (count <= max_count, 16-byte aligned buffer)");
   if (count == 0) return WS_OK;
-  return run_epoch(p, x, count, true, static_cast<cudaStream_t>(stream));
+  return run_epoch(p, x, count, 1, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -78,6 +78,7 @@ namespace ws {
 
 int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st) {
   if (c->peer && count <= c->peer_max) return ws_peer_allreduce_f32(c->peer, buf, count, st);
+  if (!c->comm) WS_FAIL(WS_ERR_INVALID, "allreduce of %lld floats above the peer buffer", (long long)count);
   const Nccl* n = nccl();
   if (!n) return WS_ERR_INVALID;
   ncclResult_t r = n->allReduce(buf, buf, (size_t)count, ncclFloat32, ncclSum, c->comm, st);
@@ -88,6 +89,8 @@ int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st) {
 ws_peer* comm_peer(const ws_comm* c, int64_t count) { return c->peer && count <= c->peer_max ? c->peer : nullptr; }
 
 int comm_allgather_f32(ws_comm* c, const float* send, float* recv, int64_t count, cudaStream_t st) {
+  if (c->peer && count <= c->peer_max) return ws_peer_allgather_f32(c->peer, send, recv, count, st);
+  if (!c->comm) WS_FAIL(WS_ERR_INVALID, "allgather of %lld floats above the peer buffer", (long long)count);
   const Nccl* n = nccl();
   if (!n) return WS_ERR_INVALID;
   ncclResult_t r = n->allGather(send, recv, (size_t)count, ncclFloat32, c->comm, st);
@@ -106,6 +109,19 @@ int ws_comm_set_peer(ws_comm* comm, ws_peer* peer, int64_t max_count) {
   if (!comm) WS_FAIL(WS_ERR_INVALID, "null communicator");
   comm->peer = peer;
   comm->peer_max = peer ? max_count : 0;
+  return WS_OK;
+}
+
+int ws_comm_create_peer(int32_t rank, int32_t nranks, int32_t device, ws_peer* peer, int64_t max_count,
+                        ws_comm** out) {
+  if (!peer || !out || rank < 0 || nranks < 1 || rank >= nranks) WS_FAIL(WS_ERR_INVALID, "bad communicator arguments");
+  ws_comm* c = new ws_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  c->peer = peer;
+  c->peer_max = max_count;
+  *out = c;
   return WS_OK;
 }
 

@@ -134,6 +134,23 @@ class TpGroup:
         dist.broadcast_object_list(obj, src=0)
         return cls(dist.get_rank(), dist.get_world_size(), device, obj[0])
 
+    @classmethod
+    def peer_only(cls, device: int, max_count: int, group=None) -> "TpGroup":
+        """A TP group whose allreduces and allgathers all run on the
+        peer-memory kernels (csrc/peer.cu) — no NCCL communicator. Collectives
+        above max_count floats fail."""
+        import torch.distributed as dist
+
+        from .peer import PeerAllreduce
+
+        self = cls.__new__(cls)
+        self.rank, self.size, self.device = dist.get_rank(group), dist.get_world_size(group), device
+        self.peer = PeerAllreduce(max_count, group)
+        h = C.c_void_p()
+        N.call("ws_comm_create_peer", self.rank, self.size, device, self.peer._h, self.peer.max_count, C.byref(h))
+        self.handle = h
+        return self
+
     def attach_peer(self, max_count: int, group=None) -> None:
         """Route the row-parallel allreduces (<= max_count floats) through the
         peer-memory allreduce (csrc/peer.cu) instead of NCCL."""

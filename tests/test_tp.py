@@ -126,3 +126,66 @@ def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     rel = ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item()
     assert rel < 1e-3, rel
     assert torch.equal(outs[1][1], outs[2][1])  # one rank: both allreduces are the identity
+
+
+def _tp_peer_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_09472_b200.weights import pinned_host_copy
+        from paper_2512_09472_b200.worker import UniversalWorker
+
+        torch.cuda.set_device(0)
+        cfg = TINY_TP
+        scfg = TP.shard_config(cfg, world)
+        host = pinned_host_copy(TP.shard_flat(cfg, synth_flat(cfg, seed=6, device="cpu"), world, rank))
+        grp = TP.TpGroup.peer_only(0, max(512 * cfg.hidden, cfg.vocab))
+        w = UniversalWorker(0, pool_pages=64, max_tokens=512)
+        w.register(scfg, host, tp=grp)
+        w.prewarm(scfg.name, layers=scfg.layers)
+        prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
+        r = w.activate_instance(scfg.name, prompt.pin_memory())
+        q.put((rank, r.token, w.logits[: cfg.vocab].cpu().numpy()))  # by value: the process exits next
+        w.release()
+        w.close()
+        grp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_tp2_peer_collectives_two_processes_match_oracle(cuda_device):
+    """Config 4 end to end without NCCL: two ranks (two processes sharing one
+    B200) run their Megatron shards of the prefill through the native path,
+    the row-parallel partials reduced and the lm_head shards gathered over
+    peer memory (CUDA IPC); both ranks produce the same logits, which match
+    the fp32 oracle of the full model."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tp_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    for p in procs:
+        if p.exitcode is None:
+            p.kill()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = {}
+    for _ in range(2):
+        rank, tok, logits = q.get(timeout=10)
+        res[rank] = (tok, torch.from_numpy(logits))
+    assert res[0][0] == res[1][0]
+    assert torch.equal(res[0][1], res[1][1])
+    cfg = TINY_TP
+    prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
+    ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), synth_flat(cfg, seed=6, device="cpu")), prompt.long())
+    got = res[0][1].double()
+    rel = ((got - ref[-1].double()).norm() / ref[-1].double().norm()).item()
+    assert rel < 2e-2, rel
+    assert res[0][0] == int(ref[-1].argmax())
