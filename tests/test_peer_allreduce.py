@@ -77,11 +77,12 @@ def test_peer_allreduce_two_processes_one_gpu(cuda_device):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    for p in procs:
-        p.join(240)
-    for p in procs:
-        if p.exitcode is None:
-            p.kill()
+    try:
+        res = dict(q.get(timeout=240) for _ in range(2))  # read before joining
+    finally:
+        for p in procs:
+            p.join(60)
+            if p.exitcode is None:
+                p.kill()
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: [], 1: []}, res

@@ -147,7 +147,21 @@ def _tp_peer_worker(rank, world, port, q):
         w.prewarm(scfg.name, layers=scfg.layers)
         prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
         r = w.activate_instance(scfg.name, prompt.pin_memory())
-        q.put((rank, r.token, w.logits[: cfg.vocab].cpu().numpy()))  # by value: the process exits next
+        first = w.logits[: cfg.vocab].cpu().numpy()  # by value: the process exits before the reader
+        w.release()
+        # two decode steps on the same shards (row-parallel reduce-adds + lm_head gather per step)
+        w.switch_memory(scfg.name)
+        sq = w.open_seq(310)
+        w.prefill(sq, prompt.cuda())
+        tok, steps = r.token, []
+        for i in range(2):
+            logits, nxt = w.decode(torch.tensor([sq], dtype=torch.int32, device="cuda"),
+                                   torch.tensor([300 + i], dtype=torch.int32, device="cuda"),
+                                   torch.tensor([tok], dtype=torch.int32, device="cuda"), 301 + i)
+            steps.append((tok, logits[0].float().cpu().numpy()))
+            tok = int(nxt[0])
+        w.close_seq(sq)
+        q.put((rank, r.token, first, steps))
         w.release()
         w.close()
         grp.close()
@@ -160,8 +174,8 @@ def test_tp2_peer_collectives_two_processes_match_oracle(cuda_device):
     """Config 4 end to end without NCCL: two ranks (two processes sharing one
     B200) run their Megatron shards of the prefill through the native path,
     the row-parallel partials reduced and the lm_head shards gathered over
-    peer memory (CUDA IPC); both ranks produce the same logits, which match
-    the fp32 oracle of the full model."""
+    peer memory (CUDA IPC), then two decode steps; both ranks produce the
+    same logits, which match the fp32 oracle of the full model."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -170,22 +184,30 @@ def test_tp2_peer_collectives_two_processes_match_oracle(cuda_device):
     procs = [ctx.Process(target=_tp_peer_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    for p in procs:
-        p.join(300)
-    for p in procs:
-        if p.exitcode is None:
-            p.kill()
-    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     res = {}
-    for _ in range(2):
-        rank, tok, logits = q.get(timeout=10)
-        res[rank] = (tok, torch.from_numpy(logits))
+    try:
+        for _ in range(2):  # drain the queue before joining (a child exits only once its data is read)
+            rank, tok, logits, steps = q.get(timeout=300)
+            res[rank] = (tok, torch.from_numpy(logits), [(t, torch.from_numpy(x)) for t, x in steps])
+    finally:
+        for p in procs:
+            p.join(60)
+            if p.exitcode is None:
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert res[0][0] == res[1][0]
     assert torch.equal(res[0][1], res[1][1])
     cfg = TINY_TP
+    weights = O.unpack(cfg, cfg.layout(), synth_flat(cfg, seed=6, device="cpu"))
     prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
-    ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), synth_flat(cfg, seed=6, device="cpu")), prompt.long())
-    got = res[0][1].double()
-    rel = ((got - ref[-1].double()).norm() / ref[-1].double().norm()).item()
-    assert rel < 2e-2, rel
+    ref, past = O.forward(cfg, weights, prompt.long())
+
+    def rel(a, b):
+        return ((a.double() - b.double()).norm() / b.double().norm()).item()
+
+    assert rel(res[0][1], ref[-1]) < 2e-2
     assert res[0][0] == int(ref[-1].argmax())
+    for i, ((t0, l0), (t1, l1)) in enumerate(zip(res[0][2], res[1][2])):
+        assert t0 == t1 and torch.equal(l0, l1)
+        ref, past = O.forward(cfg, weights, [t0], pos0=300 + i, past=past)
+        assert rel(l0, ref[0]) < 2e-2, (i, rel(l0, ref[0]))
