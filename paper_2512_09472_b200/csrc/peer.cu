@@ -17,7 +17,7 @@
 // epoch, which the peer writes only after finishing its previous reduce), so
 // slot (epoch & 1) is never overwritten while a peer still reads it.
 // The grid never exceeds the resident CTA count (the waits would otherwise
-// starve block 0).
+// starve block 0). One rank: allreduce is the identity and returns at once.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -178,8 +178,10 @@ static int run_epoch(ws_peer* p, float* out, int64_t count, int mode, cudaStream
     a.data[r] = reinterpret_cast<const float*>(p->bufs[r] + slot);
     a.flags[r] = reinterpret_cast<uint32_t*>(p->bufs[r]);
   }
+  // up to 4 CTAs of 256 threads per SM: all resident (no smem, the next
+  // kernel waits for this grid), more peer loads in flight than one per SM
   const int64_t want = (count / 4 + 255) / 256;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ws::kNumSMs, want));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * ws::kNumSMs, want));
   ws::count_launch();
   if (mode == 1)
     peer_allreduce_kernel<1><<<grid, 256, 0, st>>>(a, out, count, epoch);
@@ -198,7 +200,7 @@ static bool bad_args(const ws_peer* p, const float* buf, int64_t count) {
 int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream) {
   if (bad_args(p, buf, count))
     WS_FAIL(WS_ERR_INVALID, "bad peer allreduce (count <= max_count, 16-byte aligned buffer)");
-  if (count == 0) return WS_OK;
+  if (count == 0 || p->world == 1) return WS_OK;  // one rank: the sum is the input
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* slot = nullptr;
   if (int e = ws_peer_next_slot(p, &slot)) return e;
