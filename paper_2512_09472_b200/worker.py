@@ -236,6 +236,8 @@ class UniversalWorker:
         """Prefill on the paged pool; returns (logits view [vocab], next-token device scalar)."""
         e = self.models[self.active_model]
         rows = tokens_dev.numel()
+        if rows > self.max_tokens:  # the workspace is sized for max_tokens rows
+            raise ValueError(f"prefill of {rows} tokens exceeds this worker's max_tokens={self.max_tokens}")
         st = self.streamer if stream_from is not None else None
         caller = torch.cuda.current_stream(self.dev)
         if caller != self.compute:
@@ -251,6 +253,8 @@ class UniversalWorker:
     def decode(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor, max_ctx: int):
         e = self.models[self.active_model]
         n = seqs_dev.numel()
+        if n > self.max_tokens:
+            raise ValueError(f"decode batch {n} exceeds this worker's max_tokens={self.max_tokens}")
         caller = torch.cuda.current_stream(self.dev)
         if caller != self.compute:
             self.compute.wait_stream(caller)
@@ -307,6 +311,8 @@ class UniversalWorker:
         on the copy engine, prefill the prompt with per-layer waits, return
         the first token on the host. prompt_host: pinned int32 tokens."""
         e = self.models[name]
+        if not 1 <= prompt_host.numel() <= self.max_tokens:  # checked before any state changes
+            raise ValueError(f"prompt of {prompt_host.numel()} tokens: need 1..max_tokens={self.max_tokens}")
         L = e.cfg.layers
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)

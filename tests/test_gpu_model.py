@@ -333,7 +333,7 @@ def test_decode_gqa_shapes_match_oracle(lib, shape, lens):
     from paper_2512_09472_b200 import models as M
 
     cfg = M.TINY.with_(name="d" + shape[:2], **_DECODE_SHAPES[shape])
-    w, host = _worker(cfg, pool_pages=256)
+    w, host = _worker(cfg, pool_pages=256, max_tokens=2048)
     try:
         weights = O.unpack(cfg, cfg.layout(), host.clone())
         w.prewarm(cfg.name, layers=cfg.layers)
@@ -464,4 +464,25 @@ def test_decode_graphed_matches_eager(tiny):
     assert len(w._graphs) == 1
     for s in seqs:
         w.close_seq(s)
+    w.release()
+
+
+def test_worker_rejects_oversized_and_empty_inputs(tiny):
+    """Inputs the workspace was not sized for fail loudly before any state
+    changes (no out-of-bounds writes): empty / over-long prompts, too many
+    prefill rows, a decode batch above max_tokens."""
+    cfg, w, weights = tiny
+    too_many = w.max_tokens + 1
+    with pytest.raises(ValueError):
+        w.activate_instance(cfg.name, torch.zeros(0, dtype=torch.int32).pin_memory())
+    with pytest.raises(ValueError):
+        w.activate_instance(cfg.name, torch.zeros(too_many, dtype=torch.int32).pin_memory())
+    if w.slot(cfg.name) is None:
+        w.prewarm(cfg.name, layers=cfg.layers)
+    w.switch_memory(cfg.name)
+    with pytest.raises(ValueError):
+        w.prefill(0, torch.zeros(too_many, dtype=torch.int32, device="cuda"))
+    z = torch.zeros(too_many, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        w.decode(z, z, z, 8)
     w.release()
