@@ -1,5 +1,5 @@
-"""Peer-memory allreduce (csrc/peer.cu): two processes sharing cuda:0 map each
-other's IPC buffers (the one-GPU stand-in for two NVLink peers) and sum fp32
+"""Peer-memory allreduce (csrc/peer.cu): two or three processes sharing cuda:0
+map each other's IPC buffers (the one-GPU stand-in for NVLink peers) and sum fp32
 partials; the result must equal the rank-ordered sum bit for bit on both
 ranks, across repeated calls (both data slots, epoch flags) and ragged
 sizes."""
@@ -68,21 +68,22 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_peer_allreduce_two_processes_one_gpu(cuda_device):
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_allreduce_processes_share_one_gpu(cuda_device, world):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     try:
-        res = dict(q.get(timeout=240) for _ in range(2))  # read before joining
+        res = dict(q.get(timeout=240) for _ in range(world))  # read before joining
     finally:
         for p in procs:
             p.join(60)
             if p.exitcode is None:
                 p.kill()
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    assert res == {0: [], 1: []}, res
+    assert res == {r: [] for r in range(world)}, res
