@@ -269,7 +269,7 @@ class UniversalWorker:
 
     def decode_graphed(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor,
                        max_ctx: int, ctx_bucket: int = 256):
-        """decode() replayed from a CUDA graph: the step's ~13 kernels per layer
+        """decode() replayed from a CUDA graph: the step's 8-11 kernels per layer
         (PDL edges included) go out as one launch, so a small batch is not
         bound by host launch issue. One graph per (model, batch, context
         bucket): the attention grid is sized for the bucket and every CTA
