@@ -1,6 +1,9 @@
 // Allreduce (sum, fp32) over peer memory for the TP row-parallel partials
 // — the NVSwitch replacement for ncclAllReduce on
-// the O / down outputs.
+// the O / down outputs. Below 1 MiB one-shot (one kernel, every rank reads
+// all peers: latency-bound decode messages); from 1 MiB two-shot (reduce
+// this rank's 1/W chunk, then gather the reduced chunks: 2(W-1)/W of the
+// bytes per rank instead of W-1, for prefill partials).
 //
 // Every rank owns one IPC-exported buffer: a flag row (one epoch word per
 // source rank) and two data slots. A call copies the rank's partial into slot
@@ -35,9 +38,29 @@ int64_t slot_bytes(int64_t max_count) { return (max_count * 4 + 255) / 256 * 256
 
 struct PeerArgs {
   const float* data[kMaxPeers];  // slot (epoch & 1) of every rank's buffer
-  uint32_t* flags[kMaxPeers];    // every rank's flag row
+  float* res[kMaxPeers];         // two-shot: reduced-chunk region (epoch & 1) of every rank
+  uint32_t* flags[kMaxPeers];    // every rank's flag row: [0, 64) phase A (data ready), [64, 128) phase B
   int rank, world;
 };
+
+// Publish `epoch` to every peer's flag word (row offset `phase`), then wait
+// for every peer's word in this rank's own row. Block 0 signals; every CTA waits.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v);
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p);
+__device__ __forceinline__ void peer_barrier(const PeerArgs& a, int phase, uint32_t epoch) {
+  if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
+    __threadfence_system();
+    st_release_sys(a.flags[threadIdx.x] + phase + a.rank, epoch);
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t* mine = a.flags[a.rank] + phase;
+    for (int p = 0; p < a.world; ++p) {
+      if (p == a.rank) continue;
+      while ((int32_t)(ld_acquire_sys(mine + p) - epoch) < 0) __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
@@ -52,18 +75,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 template <int MODE>
 __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
                                                              int64_t n, uint32_t epoch) {
-  if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
-    __threadfence_system();
-    st_release_sys(a.flags[threadIdx.x] + a.rank, epoch);
-  }
-  if (threadIdx.x == 0) {
-    const uint32_t* mine = a.flags[a.rank];
-    for (int p = 0; p < a.world; ++p) {
-      if (p == a.rank) continue;
-      while ((int32_t)(ld_acquire_sys(mine + p) - epoch) < 0) __nanosleep(128);
-    }
-  }
-  __syncthreads();
+  peer_barrier(a, 0, epoch);
   const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
   if constexpr (MODE == 2) {
     for (int p = 0; p < a.world; ++p) {
@@ -98,6 +110,54 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
   }
 }
 
+// Two-shot (large messages: every rank reads 2(W-1)/W of the data over the
+// links instead of (W-1)x). Phase 1: rank r sums chunk r of every rank's
+// slot (rank order) into its own res region. Phase 2 (next kernel, so all of
+// phase 1 is complete before the signal): gather every rank's reduced chunk.
+__global__ void __launch_bounds__(256) peer_reduce_chunk_kernel(const __grid_constant__ PeerArgs a, int64_t n,
+                                                                int64_t chunk, uint32_t epoch) {
+  peer_barrier(a, 0, epoch);
+  const int64_t lo = (int64_t)a.rank * chunk, hi = min(n, lo + chunk);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float* dst = a.res[a.rank];
+  for (int64_t i = lo / 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi / 4; i += stride) {
+    float4 s = __ldcv(reinterpret_cast<const float4*>(a.data[0]) + i);
+    for (int p = 1; p < a.world; ++p) {
+      const float4 v = __ldcv(reinterpret_cast<const float4*>(a.data[p]) + i);
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    reinterpret_cast<float4*>(dst)[i] = s;
+  }
+  for (int64_t i = max(lo, hi / 4 * 4) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    float s = __ldcv(a.data[0] + i);
+    for (int p = 1; p < a.world; ++p) s += __ldcv(a.data[p] + i);
+    dst[i] = s;
+  }
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(256) peer_gather_chunks_kernel(const __grid_constant__ PeerArgs a, float* out,
+                                                                 int64_t n, int64_t chunk, uint32_t epoch) {
+  peer_barrier(a, 64, epoch);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += stride) {
+    const float4 v = __ldcv(reinterpret_cast<const float4*>(a.res[(i * 4) / chunk]) + i);
+    float4 o = v;
+    if constexpr (ACC) {
+      const float4 x = reinterpret_cast<const float4*>(out)[i];
+      o = make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
+    }
+    reinterpret_cast<float4*>(out)[i] = o;
+  }
+  for (int64_t i = n / 4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = __ldcv(a.res[i / chunk] + i);
+    out[i] = ACC ? out[i] + v : v;
+  }
+}
+
 }  // namespace
 
 struct ws_peer {
@@ -111,7 +171,7 @@ extern "C" {
 
 int ws_peer_buffer_bytes(int64_t max_count, int64_t* out) {
   if (max_count < 1 || !out) WS_FAIL(WS_ERR_INVALID, "bad peer buffer size");
-  *out = kFlagBytes + 2 * slot_bytes(max_count);
+  *out = kFlagBytes + 4 * slot_bytes(max_count);  // 2 data slots + 2 reduced-chunk regions
   return WS_OK;
 }
 
@@ -168,15 +228,33 @@ int ws_peer_destroy(ws_peer* p) {
 
 // One epoch: out = (ACC ? out : 0) + sum of every rank's slot (epoch & 1);
 // the caller's partial must already sit in its own slot.
+// Messages of at least this many bytes (per rank) take the two-shot path.
+constexpr int64_t kTwoShotBytes = 1 << 20;
+
 static int run_epoch(ws_peer* p, float* out, int64_t count, int mode, cudaStream_t st) {
   const uint32_t epoch = ++p->epoch;
-  const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * slot_bytes(p->max_count);
+  const int64_t sb = slot_bytes(p->max_count);
+  const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * sb, res = kFlagBytes + (2 + (int64_t)(epoch & 1)) * sb;
   PeerArgs a{};
   a.rank = p->rank;
   a.world = p->world;
   for (int r = 0; r < p->world; ++r) {
     a.data[r] = reinterpret_cast<const float*>(p->bufs[r] + slot);
+    a.res[r] = reinterpret_cast<float*>(p->bufs[r] + res);
     a.flags[r] = reinterpret_cast<uint32_t*>(p->bufs[r]);
+  }
+  if (mode != 2 && p->world > 1 && count * 4 >= kTwoShotBytes) {
+    const int64_t chunk = ((count + p->world - 1) / p->world + 3) / 4 * 4;  // float4-aligned chunks
+    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * ws::kNumSMs, (chunk / 4 + 255) / 256));
+    const int grid2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * ws::kNumSMs, (count / 4 + 255) / 256));
+    ws::count_launch(2);
+    peer_reduce_chunk_kernel<<<grid1, 256, 0, st>>>(a, count, chunk, epoch);
+    if (mode == 1)
+      peer_gather_chunks_kernel<true><<<grid2, 256, 0, st>>>(a, out, count, chunk, epoch);
+    else
+      peer_gather_chunks_kernel<false><<<grid2, 256, 0, st>>>(a, out, count, chunk, epoch);
+    WS_CUDA(cudaGetLastError());
+    return WS_OK;
   }
   // up to 4 CTAs of 256 threads per SM: all resident (no smem, the next
   // kernel waits for this grid), more peer loads in flight than one per SM
