@@ -43,10 +43,17 @@ struct PeerArgs {
   int rank, world;
 };
 
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Publish `epoch` to every peer's flag word (row offset `phase`), then wait
 // for every peer's word in this rank's own row. Block 0 signals; every CTA waits.
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v);
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p);
 __device__ __forceinline__ void peer_barrier(const PeerArgs& a, int phase, uint32_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < a.world && (int)threadIdx.x != a.rank) {
     __threadfence_system();
@@ -60,15 +67,6 @@ __device__ __forceinline__ void peer_barrier(const PeerArgs& a, int phase, uint3
     }
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 
 // MODE 0: out = sum, 1: out += sum, 2: allgather (out[r * n + i] = slot_r[i])
