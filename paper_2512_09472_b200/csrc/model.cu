@@ -383,12 +383,20 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, rows, kv, l, seq,
              pos0, nullptr, nullptr, qkv, st);
-    if ((m->gemm_impl & 2) || !launch_attn_prefill_tc(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st))
-      launch_attn_prefill(qkv, attn, kv, l, seq, rows, pos0, c.heads, scale, st);
-    if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), rows, d, o, x, partial, st)) return e;
-    launch_rmsnorm(x, W<bf16>(wts, Ly.ffn_norm), h, rows, d, c.rms_eps, st);
-    gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), rows, gu, act, st);
-    if (int e = row_parallel(m, act, W<bf16>(wts, Ly.wdown), rows, d, c.ffn, x, partial, st)) return e;
+    // Last layer: every row's K/V is now in the cache; past this point only
+    // the last row feeds anything (the final norm + lm_head), so attention,
+    // O and the FFN run for that row alone. WS_PRUNE_LAST=0 computes all rows.
+    static const bool prune = !(getenv("WS_PRUNE_LAST") && getenv("WS_PRUNE_LAST")[0] == '0');
+    const int r0 = prune && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
+    const bf16* q_rows = qkv + (int64_t)r0 * q;
+    float* x_rows = x + (int64_t)r0 * d;
+    if ((m->gemm_impl & 2) ||
+        !launch_attn_prefill_tc(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st))
+      launch_attn_prefill(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st);
+    if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x_rows, partial, st)) return e;
+    launch_rmsnorm(x_rows, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
+    gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);
+    if (int e = row_parallel(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x_rows, partial, st)) return e;
   }
   if (streamer && c.layers >= first_streamed)
     if (int e = ws_streamer_wait(streamer, c.layers - first_streamed, stream)) return e;
