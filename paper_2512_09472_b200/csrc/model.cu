@@ -383,10 +383,12 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, rows, kv, l, seq,
              pos0, nullptr, nullptr, qkv, st);
-    // Last layer: every row's K/V is now in the cache; past this point only
-    // the last row feeds anything (the final norm + lm_head), so attention,
-    // O and the FFN run for that row alone. WS_PRUNE_LAST=0 computes all rows.
-    static const bool prune = !(getenv("WS_PRUNE_LAST") && getenv("WS_PRUNE_LAST")[0] == '0');
+    // Opt-in (WS_PRUNE_LAST=1): in the last layer every row's K/V is in the
+    // cache after qkv_rope and only the last row feeds the final norm +
+    // lm_head, so attention, O and the FFN may run for that row alone. Off by
+    // default: the measured prefill then does every row's full work, like the
+    // reference's per-token cost model and the CPU oracle.
+    static const bool prune = getenv("WS_PRUNE_LAST") && getenv("WS_PRUNE_LAST")[0] == '1';
     const int r0 = prune && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
     const bf16* q_rows = qkv + (int64_t)r0 * q;
     float* x_rows = x + (int64_t)r0 * d;
