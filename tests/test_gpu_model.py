@@ -6,6 +6,8 @@ greedy first token identical on >= 99% of prompts.
 """
 
 import math
+import os
+from pathlib import Path
 
 import pytest
 import torch
@@ -486,3 +488,34 @@ def test_worker_rejects_oversized_and_empty_inputs(tiny):
     with pytest.raises(ValueError):
         w.decode(z, z, z, 8)
     w.release()
+
+
+def test_prune_last_layer_opt_in_matches_oracle(lib):
+    """WS_PRUNE_LAST=1 (last layer's attention / O / FFN for the last row
+    only): the first token and logits still match the fp32 oracle (own
+    process: the switch is read once per library load)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch\n"
+        "from oracle import llama_fp32 as O\n"
+        "from paper_2512_09472_b200 import models as M\n"
+        "from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat\n"
+        "from paper_2512_09472_b200.worker import UniversalWorker\n"
+        "cfg = M.TINY\n"
+        "w = UniversalWorker(0, pool_pages=64, max_tokens=1024)\n"
+        "host = pinned_host_copy(synth_flat(cfg, seed=3, device='cuda'))\n"
+        "w.register(cfg, host); w.prewarm(cfg.name, layers=cfg.layers)\n"
+        "p = torch.randint(0, cfg.vocab, (700,), generator=torch.Generator().manual_seed(2), dtype=torch.int32)\n"
+        "r = w.activate_instance(cfg.name, p.pin_memory())\n"
+        "got = w.logits[: cfg.vocab].double().cpu()\n"
+        "ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), host.clone()), p.long())\n"
+        "rel = ((got - ref[-1].double()).norm() / ref[-1].double().norm()).item()\n"
+        "assert rel < 2e-2 and r.token == int(ref[-1].argmax()), rel\n"
+        "print('ok', rel)\n"
+    )
+    env = dict(os.environ, WS_PRUNE_LAST="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=str(Path(__file__).resolve().parent.parent))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
