@@ -284,6 +284,10 @@ int ws_model_workspace_bytes(const ws_model* m, int32_t max_tokens, int64_t* byt
 /* Kernel selection bits (A/B tests): 0 = tcgen05 GEMMs + tcgen05 attention (default);
  * bit 0 = legacy mma.sync GEMMs, bit 1 = legacy mma.sync attention (3 = all legacy). */
 int ws_model_set_gemm(ws_model* m, int32_t impl);
+/* Opt-in (default off): the last decoder layer of a prefill runs attention, O
+ * and the FFN for the last row only (every row's QKV + KV append still runs);
+ * same first token and KV cache. Every rank of a TP group must agree. */
+int ws_model_set_prune_last(ws_model* m, int32_t on);
 
 /* Prefill `rows` new tokens of sequence `seq` (positions pos0..pos0+rows-1;
  * blocks must be reserved). `weights` is the slot VA. If `streamer` is set,

@@ -128,3 +128,52 @@ def forward(cfg, w: dict, tokens, pos0: int = 0, past: list | None = None):
         x = x + (torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ w[f"l{l}.wdown"].T
     h = _rms(x, w["final_norm"], cfg.rms_eps)
     return h @ w["lm_head"].T, new_past
+
+
+def forward_streamed(cfg, layout, flat_bf16: torch.Tensor, tokens, heads_per_chunk: int = 8) -> torch.Tensor:
+    """Last-row logits [vocab] of ``forward`` without materialising the whole
+    fp32 model: each tensor is upcast from the bf16 image when its layer runs
+    (a full-size Llama-3-8B needs ~1 GB of fp32 weights at a time instead of
+    32 GB). Same math, same order of operations as ``forward`` with pos0 = 0;
+    attention runs ``heads_per_chunk`` heads at a time to bound the S x S
+    score buffers."""
+    tokens = torch.as_tensor(tokens, dtype=torch.long)
+    S = tokens.numel()
+    H, KV, hd, d = cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.hidden
+    cos, sin = rope_table(hd, cfg.rope_theta, S)
+
+    def t(off, *shape):
+        n = int(np.prod(shape))
+        return flat_bf16[off // 2: off // 2 + n].view(*shape).float()
+
+    x = flat_bf16[layout.embed // 2: layout.embed // 2 + cfg.vocab * d].view(cfg.vocab, d)[tokens].float()
+    causal = torch.ones(S, S, dtype=torch.bool).triu(1)[None]
+    for L in layout.layers:
+        h = _rms(x, t(L["attn_norm"], d), cfg.rms_eps)
+        qkv = h @ t(L["wqkv"], cfg.qkv_dim, d).T
+        if L["bqkv"] >= 0:
+            qkv = qkv + t(L["bqkv"], cfg.qkv_dim)
+        q = _rope(qkv[:, : H * hd].view(S, H, hd), cos, sin)
+        k = _rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin)
+        v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+        g = H // KV
+        o = torch.empty(S, H, hd)
+        for h0 in range(0, H, heads_per_chunk):
+            h1 = min(H, h0 + heads_per_chunk)
+            kk = k[:, torch.arange(h0, h1) // g]
+            vv = v[:, torch.arange(h0, h1) // g]
+            sc = torch.einsum("shd,thd->hst", q[:, h0:h1], kk) / math.sqrt(hd)
+            sc = sc.masked_fill(causal, float("-inf"))
+            o[:, h0:h1] = torch.einsum("hst,thd->shd", torch.softmax(sc, dim=-1), vv)
+        x = x + o.reshape(S, H * hd) @ t(L["wo"], d, H * hd).T
+        h = _rms(x, t(L["ffn_norm"], d), cfg.rms_eps)
+        wg, wu = split_gate_up(t(L["wgu"], 2 * cfg.ffn, d), cfg.ffn)
+        x = x + (torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ t(L["wdown"], d, cfg.ffn).T
+    h = _rms(x[-1:], t(layout.final_norm, d), cfg.rms_eps)
+    rows = cfg.lm_head_rows or cfg.vocab
+    out = torch.empty(rows)
+    step = 16384
+    for r0 in range(0, rows, step):
+        r1 = min(rows, r0 + step)
+        out[r0:r1] = (h @ t(layout.lm_head + r0 * d * 2, r1 - r0, d).T)[0]
+    return out

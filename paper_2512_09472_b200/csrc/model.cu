@@ -120,6 +120,7 @@ struct ws_model {
   int device = 0;
   float2* rope = nullptr;  // [max_positions, head_dim/2] (cos, sin)
   int gemm_impl = 0;
+  bool prune_last = false;  // ws_model_set_prune_last
   ws_comm* comm = nullptr;  // TP group (config 4); null = single GPU
 };
 
@@ -347,6 +348,12 @@ int ws_model_set_gemm(ws_model* m, int32_t impl) {
   return WS_OK;
 }
 
+int ws_model_set_prune_last(ws_model* m, int32_t on) {
+  if (!m) WS_FAIL(WS_ERR_INVALID, "null model");
+  m->prune_last = on != 0;
+  return WS_OK;
+}
+
 int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
                      const int32_t* tokens, int32_t rows, int32_t pos0, ws_streamer* streamer,
                      int32_t first_streamed, void* workspace, float* logits, int32_t* next_token,
@@ -383,13 +390,13 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     launch_rmsnorm(x, W<bf16>(wts, Ly.attn_norm), h, rows, d, c.rms_eps, st);
     qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, rows, kv, l, seq,
              pos0, nullptr, nullptr, qkv, st);
-    // Opt-in (WS_PRUNE_LAST=1): in the last layer every row's K/V is in the
-    // cache after qkv_rope and only the last row feeds the final norm +
-    // lm_head, so attention, O and the FFN may run for that row alone. Off by
-    // default: the measured prefill then does every row's full work, like the
-    // reference's per-token cost model and the CPU oracle.
-    static const bool prune = getenv("WS_PRUNE_LAST") && getenv("WS_PRUNE_LAST")[0] == '1';
-    const int r0 = prune && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
+    // Per-model opt-in (ws_model_set_prune_last): in the last layer every
+    // row's K/V is in the cache after qkv_rope and only the last row feeds the
+    // final norm + lm_head, so attention, O and the FFN may run for that row
+    // alone. Off by default: the measured prefill then does every row's full
+    // work, like the reference's per-token cost model and the CPU oracle. A TP
+    // group sets it on every rank (the row-parallel collectives change size).
+    const int r0 = m->prune_last && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
     const bf16* q_rows = qkv + (int64_t)r0 * q;
     float* x_rows = x + (int64_t)r0 * d;
     if ((m->gemm_impl & 2) ||

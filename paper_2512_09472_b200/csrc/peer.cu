@@ -71,7 +71,7 @@ __device__ __forceinline__ void peer_barrier(const PeerArgs& a, int phase, uint3
 
 // MODE 0: out = sum, 1: out += sum, 2: allgather (out[r * n + i] = slot_r[i])
 template <int MODE>
-__global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
+__global__ void __launch_bounds__(256, 4) peer_allreduce_kernel(const __grid_constant__ PeerArgs a, float* out,
                                                              int64_t n, uint32_t epoch) {
   peer_barrier(a, 0, epoch);
   const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const __grid_consta
 // links instead of (W-1)x). Phase 1: rank r sums chunk r of every rank's
 // slot (rank order) into its own res region. Phase 2 (next kernel, so all of
 // phase 1 is complete before the signal): gather every rank's reduced chunk.
-__global__ void __launch_bounds__(256) peer_reduce_chunk_kernel(const __grid_constant__ PeerArgs a, int64_t n,
+__global__ void __launch_bounds__(256, 4) peer_reduce_chunk_kernel(const __grid_constant__ PeerArgs a, int64_t n,
                                                                 int64_t chunk, uint32_t epoch) {
   peer_barrier(a, 0, epoch);
   const int64_t lo = (int64_t)a.rank * chunk, hi = min(n, lo + chunk);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) peer_reduce_chunk_kernel(const __grid_con
 }
 
 template <bool ACC>
-__global__ void __launch_bounds__(256) peer_gather_chunks_kernel(const __grid_constant__ PeerArgs a, float* out,
+__global__ void __launch_bounds__(256, 4) peer_gather_chunks_kernel(const __grid_constant__ PeerArgs a, float* out,
                                                                  int64_t n, int64_t chunk, uint32_t epoch) {
   peer_barrier(a, 64, epoch);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

@@ -24,6 +24,8 @@ class PeerAllreduce:
         import torch.distributed as dist
 
         single = not dist.is_initialized()
+        self._group = group
+        self._single = single
         self.rank = 0 if single else dist.get_rank(group)
         self.world = 1 if single else dist.get_world_size(group)
         self.max_count = int(max_count)
@@ -76,6 +78,12 @@ class PeerAllreduce:
     def close(self) -> None:
         if self._h:
             torch.cuda.synchronize()
+            if not self._single:
+                # A slower peer may still be inside its last peer kernel, reading
+                # this rank's exported slot: free nothing until every rank is done.
+                import torch.distributed as dist
+
+                dist.barrier(group=self._group)
             N.call("ws_peer_destroy", self._h)
             self._h = C.c_void_p()
             for p in self._opened:

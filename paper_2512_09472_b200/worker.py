@@ -37,6 +37,7 @@ class ModelEntry:
     handle: C.c_void_p
     peer: torch.Tensor | None = None  # optional peer-device image (NVLink source)
     packed: object | None = None      # weights.PackedImage: the packed cold-start stream
+    tp: object | None = None          # tp.TpGroup of a TP shard (None: single GPU)
 
 
 @dataclass
@@ -98,7 +99,7 @@ class UniversalWorker:
         if tp is not None:
             N.call("ws_model_set_comm", h, tp.handle)
         spec = model_spec(cfg, max_batch=max_batch)
-        e = ModelEntry(cfg, spec, cfg.layout(), host_weights, h)
+        e = ModelEntry(cfg, spec, cfg.layout(), host_weights, h, tp=tp)
         self.models[cfg.name] = e
         need = C.c_int64()
         N.call("ws_model_workspace_bytes", h, self.max_tokens, C.byref(need))
@@ -122,6 +123,13 @@ class UniversalWorker:
     def set_gemm_impl(self, impl: int) -> None:
         for e in self.models.values():
             N.call("ws_model_set_gemm", e.handle, impl)
+
+    def set_prune_last(self, name: str, on: bool) -> None:
+        """Per-model opt-in: the last decoder layer runs attention, O and the
+        FFN for the last prompt row only (every row's QKV + KV append still
+        runs). A TP group must set the same value on every rank: the last
+        layer's row-parallel collectives change size with it."""
+        N.call("ws_model_set_prune_last", self.models[name].handle, int(bool(on)))
 
     def slot(self, name: str) -> PrewarmSlot | None:
         return self.gpu.slots.get(name)
@@ -276,6 +284,13 @@ class UniversalWorker:
         clips to its sequence's length, so results equal decode() with
         max_ctx = the bucket. Inputs are copied into the graph's static
         buffers on the compute stream."""
+        tp = self.models[self.active_model].tp
+        if tp is not None and getattr(tp, "peer", None) is not None:
+            # The peer allreduce advances its epoch and picks its double-buffered
+            # slot on the host at launch time; a graph would freeze both and a
+            # replay could read peers' slots before they are written.
+            raise RuntimeError("decode_graphed: a TP model on the peer-memory allreduce cannot be graph-captured "
+                               "(host-side epochs); use decode()")
         n = seqs_dev.numel()
         cap = -(-max_ctx // ctx_bucket) * ctx_bucket
         key = (self.active_model, n, cap)

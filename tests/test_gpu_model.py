@@ -5,6 +5,7 @@ bf16 weights and activations against fp32 math on the same bf16 weights);
 greedy first token identical on >= 99% of prompts.
 """
 
+import json
 import math
 import os
 from pathlib import Path
@@ -171,20 +172,26 @@ def test_tiny_greedy_agreement_256_prompts(tiny):
         hits.append(hit)
         agree += hit
     w.release()
-    # Random-init models have flat next-token distributions: a few prompts have
-    # an fp32 top1-top2 margin below the bf16 logit noise floor, where the
-    # greedy token is a coin flip for ANY bf16 implementation. The 99% bar is
-    # applied to prompts whose margin exceeds 2x the worst observed |logit err|
-    # (SURVEY §7 hard parts: report agreement with its margin distribution).
-    floor = 2 * max(noise)
-    decisive = [h for h, m in zip(hits, margins) if m > floor]
-    print(f"\ngreedy agreement {agree}/{n} overall, {sum(decisive)}/{len(decisive)} with margin > "
-          f"{floor:.2e} (2x max |logit err|); logits rel err max {max(rels):.2e} mean {sum(rels)/n:.2e}; "
-          f"ref margin min {min(margins):.2e} median {sorted(margins)[n//2]:.2e}; "
-          f"disagreements at margins {sorted(m for h, m in zip(hits, margins) if not h)}")
+    # Random-init models have flat next-token distributions: the report keeps
+    # the margin distribution next to the agreement (SURVEY §7 hard parts), so
+    # a disagreement can be read against its fp32 top1-top2 margin.
+    report = {"config": "tiny (2 layers, d=256, vocab 4096), 512-token prompts, seeds 1000..1255",
+              "agree": agree, "n": n, "logit_rel_max": max(rels), "logit_rel_mean": sum(rels) / n,
+              "max_abs_logit_err": max(noise), "ref_margin_min": min(margins),
+              "ref_margin_median": sorted(margins)[n // 2],
+              "disagreements": [{"seed": 1000 + i, "ref_margin": m} for i, (h, m) in enumerate(zip(hits, margins))
+                                if not h]}
+    out = os.environ.get("WS_REPORT_DIR", "gpurun_out")
+    try:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "r2_tiny_greedy_report.json"), "w") as f:
+            json.dump(report, f, indent=1)
+    except OSError:
+        pass
+    print(f"\ngreedy agreement {agree}/{n}; logits rel err max {max(rels):.2e} mean {sum(rels)/n:.2e}; "
+          f"disagreements at margins {[d['ref_margin'] for d in report['disagreements']]}")
     assert max(rels) < LOGIT_RTOL
-    assert sum(decisive) >= math.ceil(0.99 * len(decisive)) and len(decisive) >= 0.75 * n
-    assert agree >= math.ceil(0.97 * n)
+    assert agree >= math.ceil(0.99 * n)
 
 
 @pytest.mark.parametrize("impl", [0, 1, 2, 3])
@@ -490,32 +497,27 @@ def test_worker_rejects_oversized_and_empty_inputs(tiny):
     w.release()
 
 
-def test_prune_last_layer_opt_in_matches_oracle(lib):
-    """WS_PRUNE_LAST=1 (last layer's attention / O / FFN for the last row
-    only): the first token and logits still match the fp32 oracle (own
-    process: the switch is read once per library load)."""
-    import subprocess
-    import sys
-
-    code = (
-        "import torch\n"
-        "from oracle import llama_fp32 as O\n"
-        "from paper_2512_09472_b200 import models as M\n"
-        "from paper_2512_09472_b200.weights import pinned_host_copy, synth_flat\n"
-        "from paper_2512_09472_b200.worker import UniversalWorker\n"
-        "cfg = M.TINY\n"
-        "w = UniversalWorker(0, pool_pages=64, max_tokens=1024)\n"
-        "host = pinned_host_copy(synth_flat(cfg, seed=3, device='cuda'))\n"
-        "w.register(cfg, host); w.prewarm(cfg.name, layers=cfg.layers)\n"
-        "p = torch.randint(0, cfg.vocab, (700,), generator=torch.Generator().manual_seed(2), dtype=torch.int32)\n"
-        "r = w.activate_instance(cfg.name, p.pin_memory())\n"
-        "got = w.logits[: cfg.vocab].double().cpu()\n"
-        "ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), host.clone()), p.long())\n"
-        "rel = ((got - ref[-1].double()).norm() / ref[-1].double().norm()).item()\n"
-        "assert rel < 2e-2 and r.token == int(ref[-1].argmax()), rel\n"
-        "print('ok', rel)\n"
-    )
-    env = dict(os.environ, WS_PRUNE_LAST="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
-                         cwd=str(Path(__file__).resolve().parent.parent))
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+def test_prune_last_layer_opt_in_matches_oracle(tiny):
+    """ws_model_set_prune_last (last layer's attention / O / FFN for the last
+    row only): the first token and logits still match the fp32 oracle, and
+    the KV cache the prefill leaves is the unpruned one (a decode step over
+    it matches too)."""
+    cfg, w, weights = tiny
+    if w.slot(cfg.name) is None:
+        w.prewarm(cfg.name, layers=cfg.layers)
+    w.set_prune_last(cfg.name, True)
+    try:
+        p = _prompt(cfg, 2, 700)
+        r = w.activate_instance(cfg.name, p.pin_memory(), keep_seq=True)
+        got = w.logits[: cfg.vocab].float().cpu()
+        ref, past = O.forward(cfg, weights, p.long())
+        assert _rel(got, ref[-1]) < LOGIT_RTOL and r.token == int(ref[-1].argmax())
+        tok = int(ref[-1].argmax())
+        logits, _ = w.decode(torch.tensor([r.seq], dtype=torch.int32, device="cuda"),
+                             torch.tensor([700], dtype=torch.int32, device="cuda"),
+                             torch.tensor([tok], dtype=torch.int32, device="cuda"), 701)
+        ref2, _ = O.forward(cfg, weights, [tok], pos0=700, past=past)
+        assert _rel(logits[0].float().cpu(), ref2[0]) < LOGIT_RTOL
+        w.release()
+    finally:
+        w.set_prune_last(cfg.name, False)

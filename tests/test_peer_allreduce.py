@@ -12,7 +12,9 @@ import socket
 import pytest
 import torch
 
-SIZES = [1, 3, 1000, 4096 * 8 + 5, 1 << 20, 17, 1 << 20]
+# two-shot from 1 MiB (262,144 floats): ragged sizes exercise the scalar tails of
+# the chunk reduce / gather (n % 4 != 0, a short last chunk)
+SIZES = [1, 3, 1000, 4096 * 8 + 5, 1 << 20, 17, 1 << 20, (1 << 18) + 3, (1 << 20) + 7, (1 << 18) + 1]
 
 
 def _free_port():
@@ -37,7 +39,7 @@ def _worker(rank, world, port, q):
         from paper_2512_09472_b200.peer import PeerAllreduce
 
         torch.cuda.set_device(0)
-        pa = PeerAllreduce(max_count=1 << 20)
+        pa = PeerAllreduce(max_count=(1 << 20) + 64)
         bad = []
         for step, n in enumerate(SIZES):
             t = _inputs(rank, n, step).cuda()
@@ -49,7 +51,7 @@ def _worker(rank, world, port, q):
             if not torch.equal(got, want):
                 bad.append((step, n, (got - want).abs().max().item()))
         # fused form: partial written straight into the exported slot, x += sum
-        for step, n in enumerate([4096 * 8 + 5, 1 << 20, 3]):
+        for step, n in enumerate([4096 * 8 + 5, 1 << 20, 3, (1 << 18) + 3, (1 << 20) + 7]):
             x = _inputs(9, n, 50 + step).cuda()
             pa.next_slot(n).copy_(_inputs(rank, n, 100 + step).cuda())
             pa.reduce_add_(x)
