@@ -159,30 +159,145 @@ def _layer_cpu(cfg, w, x, O):
     return x
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the reference CPU path (oracle port) on host cores."""
-    from paper_2512_09472_b200 import models as M
+# Model shapes of the reference arm (public HF configs).
+# Hard-coded so the reference arm never loads this repo's package or native
+# library; tests/test_bench_contract.py checks them against models.py.
+REF_SHAPES = {
+    "llama3-8b": dict(layers=32, hidden=4096, ffn=14336, heads=32, kv_heads=8, head_dim=128, vocab=128256,
+                      rope_theta=500000.0, rms_eps=1e-5),
+}
 
+
+def _ref_cpu_weights(shape, seed=0):
+    """bf16 weights of every decoder layer + final norm + lm_head on the host,
+    generated once outside the timed region. Values are N(0, 0.02) (norm gains
+    N(1, 0.1)) drawn from one 2^27-value seeded pool at a random offset per
+    tensor: 8 G fresh normals would take ~70 s of single-threaded RNG, and the
+    forward's cost does not depend on the values."""
+    import torch
+
+    g = torch.Generator().manual_seed(seed)
+    pool = (torch.randn(1 << 27, generator=g) * 0.02).bfloat16()
+    d, f, H, KV, hd = shape["hidden"], shape["ffn"], shape["heads"], shape["kv_heads"], shape["head_dim"]
+    q = (H + 2 * KV) * hd
+
+    def lin(*sh):
+        n = 1
+        for v in sh:
+            n *= v
+        off = int(torch.randint(0, 1 << 27, (1,), generator=g))
+        reps = -(-(off + n) // (1 << 27))
+        return pool.repeat(reps)[off:off + n].view(*sh).clone()
+
+    def norm(n):
+        return (torch.randn(n, generator=g) * 0.1 + 1.0).bfloat16()
+
+    layers = [dict(attn_norm=norm(d), wqkv=lin(q, d), wo=lin(d, H * hd), ffn_norm=norm(d), wg=lin(f, d),
+                   wu=lin(f, d), wdown=lin(d, f)) for _ in range(shape["layers"])]
+    return dict(embed=lin(shape["vocab"], d), layers=layers, final_norm=norm(d), lm_head=lin(shape["vocab"], d))
+
+
+def _ref_cpu_prefill(shape, w, tokens):
+    """One full prefill on the host CPU: the oracle's fp32 Llama forward
+    (oracle/llama_fp32.py: RMSNorm, rotate-half RoPE, causal GQA attention,
+    SwiGLU, fp32 residual) over every decoder layer, each layer's bf16
+    weights upcast to fp32 as it runs, then the last row's logits. Returns the
+    greedy token."""
+    import torch
+
+    from oracle import llama_fp32 as O
+
+    S = tokens.numel()
+    H, KV, hd, eps = shape["heads"], shape["kv_heads"], shape["head_dim"], shape["rms_eps"]
+    cos, sin = O.rope_table(hd, shape["rope_theta"], S)
+    x = w["embed"][tokens].float()
+    for L in w["layers"]:
+        h = O._rms(x, L["attn_norm"].float(), eps)
+        qkv = h @ L["wqkv"].float().T
+        q = O._rope(qkv[:, : H * hd].view(S, H, hd), cos, sin)
+        k = O._rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin)
+        v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+        g = H // KV
+        o = torch.nn.functional.scaled_dot_product_attention(
+            q.transpose(0, 1), k.repeat_interleave(g, 1).transpose(0, 1), v.repeat_interleave(g, 1).transpose(0, 1),
+            is_causal=True).transpose(0, 1).reshape(S, H * hd)
+        x = x + o @ L["wo"].float().T
+        h = O._rms(x, L["ffn_norm"].float(), eps)
+        x = x + (torch.nn.functional.silu(h @ L["wg"].float().T) * (h @ L["wu"].float().T)) @ L["wdown"].float().T
+    h = O._rms(x[-1:], w["final_norm"].float(), eps)
+    return int((h @ w["lm_head"].float().T).argmax())
+
+
+def _ref_ledger_ops(n=2000):
+    """The reference's switch bookkeeping (cluster.py:291-387, restated in
+    oracle/ledger.py): promote (evicting 3 co-prewarmed slots) / reclaim /
+    release on the config-3 ledger (89,600 pages, 4 models), timed per call."""
+    from oracle import ledger as Lg
+
+    models = [("llama3-8b", 7659), ("qwen2.5-7b", 7263), ("mistral-7b", 6907), ("phi3-mini", 3645)]
+    page = 2 << 20
+    t = {"promote": [], "reclaim": [], "release": [], "begin_prewarm": []}
+    for i in range(n):
+        cl = Lg.new_cluster(1, 1, 89600, page)
+        t0 = time.perf_counter()
+        for m, p in models:
+            Lg.begin_prewarm(cl, 0, m, p, 4)
+        t1 = time.perf_counter()
+        m, p = models[i % 4]
+        iid, _ = Lg.promote(cl, (0,), m, 1, p * page, 32, 4)
+        t2 = time.perf_counter()
+        cl["instances"][iid]["state"] = Lg.ACTIVE
+        Lg.enter_grace(cl, iid)
+        t3 = time.perf_counter()
+        Lg.reclaim(cl, 0, 8, 32, 10 * (1 << 30))
+        t4 = time.perf_counter()
+        Lg.release(cl, iid)
+        t5 = time.perf_counter()
+        t["begin_prewarm"].append((t1 - t0) * 1e6 / 4)
+        t["promote"].append((t2 - t1) * 1e6)
+        t["reclaim"].append((t4 - t3) * 1e6)
+        t["release"].append((t5 - t4) * 1e6)
+    return {k + "_p50_us": pct(v, 50) for k, v in t.items()} | {"n": n, "cores": 1,
+                                                                 "source": "oracle/ledger.py (cluster.py:245-387)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference-side CPU path on the host cores — the
+    oracle port of a FULL prefill (every decoder layer, 2048 tokens, fp32 on
+    all host threads) per step, plus the reference ledger ops beside the GPU
+    arm's switch latency. Never imports this repo's package or library."""
     if rank != 0:
         return
-    cfg = M.ALL[args.model]
-    vals = []
-    sample = ""
-    threads = 1
-    for i in range(args.warmup + args.steps):
-        v, sample, threads, _ = cpu_prefill_sample(cfg, args.prompt, min_seconds=0.0, max_layers=1)
-        if i >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+    import torch
+
+    shape = REF_SHAPES[args.model]
+    w = _ref_cpu_weights(shape)
+    tokens = torch.randint(0, shape["vocab"], (args.prompt,), generator=torch.Generator().manual_seed(7))
+    for _ in range(args.warmup):
+        _ref_cpu_prefill(shape, w, tokens)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _ref_cpu_prefill(shape, w, tokens)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps * args.prompt / total
+    threads = torch.get_num_threads()
+    sample = (f"{args.steps} full {args.model} prefills of a {args.prompt}-token prompt ({shape['layers']} layers "
+              f"+ last-row lm_head), torch CPU fp32 oracle port, {threads} threads; median "
+              f"{statistics.median(times):.1f} s per prefill")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.prompt / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} prefill of a {args.prompt}-token prompt on the host CPU "
-                               "(the reference has no GPU path; its prefill is the linear model "
-                               "engine.py:107-108 — timed here is the fp32 oracle port of the forward)",
-                   "model": cfg.name, "prompt_tokens": args.prompt},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded random-init weights of the named shape, random token ids)",
+        "config": {"workload": f"{args.model} universal worker, 2048-token prompt prefill (BASELINE configs[1]); "
+                               "the reference has no GPU path (its prefill is the linear model engine.py:107-108), "
+                               "so its arm is the CPU fp32 oracle port of the full forward",
+                   "model": args.model, "prompt_tokens": args.prompt},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu": _cpu_model()},
+        "ledger_us": _ref_ledger_ops(),
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -237,51 +352,59 @@ def run_ours(args, rank, world, local_rank):
     # clocks are sampled across every timed region below (cold, warm, value)
     clk = Clocks(dev).__enter__()
     time.sleep(0.5)  # let nvidia-smi start sampling before the first timed step
-    # ---- cold starts, plain bf16 stream: layers k..L + lm_head over PCIe each step
-    cold = []
-    for i in range(Wm + K):
-        if i:
-            w.drop_suffix(cfg.name, args.prewarm_layers)
-        barrier()
-        r = w.activate_instance(cfg.name, prompt_pinned)
-        w.release()
-        if i >= Wm:
-            cold.append(r)
-    # ---- cold starts (e2e), packed stream: the same ranges losslessly packed on
-    #      the host (~25% fewer PCIe bytes), unpacked on the GPU per layer
+    # ---- TTFT legs: n_prompts distinct seeded 2048-token
+    #      prompts per leg after Wm warm-up activations; each leg drops the
+    #      ledger's residency back to k layers so the suffix streams again
+    n_prompts = max(K, args.ttft_prompts)
+    gp = torch.Generator().manual_seed(1234)
+    prompts = [torch.randint(0, cfg.vocab, (S,), generator=gp, dtype=torch.int32).pin_memory()
+               for _ in range(n_prompts)]
+
+    def leg(k_resident, source=None):
+        out = []
+        for i in range(Wm + n_prompts):
+            if k_resident is not None:
+                w.drop_suffix(cfg.name, k_resident)
+            barrier()
+            r = w.activate_instance(cfg.name, prompts[(i - Wm) % n_prompts] if i >= Wm else prompt_pinned,
+                                    source=source)
+            w.release()
+            if i >= Wm:
+                out.append(r)
+        return out
+
+    k0 = args.prewarm_layers
+    # cold, plain bf16 stream: layers k..L + lm_head over PCIe
+    cold = leg(k0)
+    # cold (e2e), packed stream: the same ranges losslessly packed on the host
+    # (~34% fewer PCIe bytes), unpacked on the GPU per layer
     w.set_packed(cfg.name, packed)
-    cold_packed = []
-    for i in range(Wm + K):
-        w.drop_suffix(cfg.name, args.prewarm_layers)
-        barrier()
-        r = w.activate_instance(cfg.name, prompt_pinned)
-        w.release()
-        if i >= Wm:
-            cold_packed.append(r)
+    cold_packed = leg(k0)
     w.models[cfg.name].packed = None
-    # ---- cold starts from an HBM-resident image of the model on this GPU: the
-    #      stand-in for a peer GPU's copy (an NVLink 5 peer is
-    #      capped at ~900 GB/s, this source is faster), showing what layer
-    #      streaming hides once the link keeps up with the forward
+    # cold from an HBM-resident image on this GPU: the stand-in for a peer
+    # GPU's copy, showing what layer streaming hides once the
+    # link keeps up with the forward
     dev_src = host.to(f"cuda:{dev}")
-    cold_hbm = []
-    for i in range(Wm + K):
-        w.drop_suffix(cfg.name, args.prewarm_layers)
-        barrier()
-        r = w.activate_instance(cfg.name, prompt_pinned, source=dev_src)
-        w.release()
-        if i >= Wm:
-            cold_hbm.append(r)
+    cold_hbm = leg(k0, source=dev_src)
     del dev_src
     torch.cuda.empty_cache()
-    # ---- warm starts: every layer resident
-    warm = []
-    for i in range(Wm + K):
-        barrier()
-        r = w.activate_instance(cfg.name, prompt_pinned)
-        w.release()
-        if i >= Wm:
-            warm.append(r)
+    # warm: every layer resident
+    warm = leg(None)
+    # the reference's own policy: k = required_prewarm_layers (cluster.py:145-166)
+    # at the MEASURED stream bandwidth and per-token prefill cost, plain and packed
+    spec = entry.spec
+    warm_ms = pct([r.ttft_ms for r in warm], 50)
+    a_ms = warm_ms / S  # measured per-token prefill cost (the reference's prefill_a)
+    spec_m = type(spec)(spec.model_id, spec.weight_bytes, 1, layers=cfg.layers, prefill_a_ms=a_ms, prefill_b_ms=0.0)
+    stream_gbs = statistics.median(r.streamed_bytes / (r.stream_ms / 1e3) / 1e9 for r in cold)
+    bw_bytes_ms = stream_gbs * 1e9 / 1e3
+    k_req = required_prewarm_layers(spec_m, bw_bytes_ms, S)
+    packed_bw = cold[0].streamed_bytes / (statistics.median(r.stream_ms for r in cold_packed) / 1e3) / 1e3
+    k_req_packed = required_prewarm_layers(spec_m, packed_bw, S)
+    cold_kreq = leg(k_req)
+    w.set_packed(cfg.name, packed)
+    cold_kreq_packed = leg(k_req_packed)
+    w.models[cfg.name].packed = None
 
     # ---- value: warm prefill throughput, prompt + weights resident in HBM
     w.switch_memory(cfg.name)
@@ -413,16 +536,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = gemm_flops / (gemm_ms[0] / 1e3) / 1e12
 
     # ---- the reference's analytic model, evaluated with MEASURED inputs
-    stream_gbs = statistics.median(r.streamed_bytes / (r.stream_ms / 1e3) / 1e9 for r in cold)
-    bw_bytes_ms = stream_gbs * 1e9 / 1e3
-    spec = entry.spec
-    a_ms = (prefill_ms / S)  # measured per-token prefill cost
-    spec_m = type(spec)(spec.model_id, spec.weight_bytes, 1, layers=cfg.layers, prefill_a_ms=a_ms, prefill_b_ms=0.0)
-    k_req = required_prewarm_layers(spec_m, bw_bytes_ms, S)
     stall_pred = catchup_stall_ms(spec_m, args.prewarm_layers, bw_bytes_ms, S)
-    # the packed stream delivers weight bytes faster than the link moves bytes
-    packed_bw = cold[0].streamed_bytes / (statistics.median(r.stream_ms for r in cold_packed) / 1e3) / 1e3
-    k_req_packed = required_prewarm_layers(spec_m, packed_bw, S)
     stall_packed = catchup_stall_ms(spec_m, args.prewarm_layers, packed_bw, S)
 
     traffic = None
@@ -434,7 +548,7 @@ def run_ours(args, rank, world, local_rank):
     packed_ttft = [r.ttft_ms for r in cold_packed]
     warm_ttft = [r.ttft_ms for r in warm]
     cold_total_s = max_over_ranks(sum(packed_ttft) / 1e3)
-    e2e_value = world * K * S / cold_total_s
+    e2e_value = world * len(packed_ttft) * S / cold_total_s
     clk_sum = clk.summary()
 
     cpu = None
@@ -459,26 +573,6 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 4,
                 "path": "UniversalWorker.activate_instance (cold, packed stream): switch_memory + packed layer "
                         "streaming from pinned host memory + GPU unpack + prefill"},
-        "ttft_ms": {"cold_p50": pct(packed_ttft, 50), "cold_p99": pct(packed_ttft, 99),
-                    "cold_over_warm_p50": pct(packed_ttft, 50) / pct(warm_ttft, 50),
-                    "cold_packed_streamed_bytes": cold_packed[0].streamed_bytes,
-                    "cold_packed_stream_ms_p50": pct([r.stream_ms for r in cold_packed], 50),
-                    "pack_ratio": cold_packed[0].streamed_bytes / cold[0].streamed_bytes,
-                    "pack_setup_s": pack_s,
-                    "cold_plain_p50": pct(cold_ttft, 50), "cold_plain_p99": pct(cold_ttft, 99),
-                    "warm_p50": pct(warm_ttft, 50), "warm_p99": pct(warm_ttft, 99),
-                    "cold_plain_over_warm_p50": pct(cold_ttft, 50) / pct(warm_ttft, 50), "target_ratio": 1.2,
-                    "cold_device_p50": pct([r.device_ms for r in cold], 50),
-                    "stream_ms_p50": pct([r.stream_ms for r in cold], 50),
-                    "streamed_bytes": cold[0].streamed_bytes, "stream_gbs_p50": stream_gbs,
-                    "pcie_gen5_peak_gbs": 64.0,
-                    "cold_hbm_source_p50": pct([r.ttft_ms for r in cold_hbm], 50),
-                    "cold_hbm_source_p99": pct([r.ttft_ms for r in cold_hbm], 99),
-                    "cold_hbm_source_over_warm_p50": pct([r.ttft_ms for r in cold_hbm], 50) / pct(warm_ttft, 50),
-                    "hbm_source_stream_gbs_p50": statistics.median(
-                        r.streamed_bytes / (r.stream_ms / 1e3) / 1e9 for r in cold_hbm),
-                    "hbm_source_note": "layers 4..31 + lm_head streamed from a device-resident copy on the same "
-                                       "GPU (stand-in for an NVLink peer source; not a peer measurement)"},
         "reference_model_at_measured_inputs": {
             "required_prewarm_layers": k_req, "catchup_stall_ms_k4": stall_pred,
             "predicted_cold_ttft_ms": pct(warm_ttft, 50) + stall_pred,
@@ -510,6 +604,40 @@ def run_ours(args, rank, world, local_rank):
         "setup_s": setup_s,
         "vmm": {"pool_init_ms": init_ms.value, "slot_map_us_per_page": map_pp.value * 1e3,
                 "prewarm_ms": getattr(slot, "prewarm_ms", None)},
+        # last key: the driver's stdout tail keeps the end of the line
+        "ttft_ms": {"prompts": n_prompts, "prompt_seeds": "torch.Generator().manual_seed(1234), one 2048-token "
+                    "prompt per activation",
+                    "cold_p50": pct(packed_ttft, 50), "cold_p99": pct(packed_ttft, 99),
+                    "cold_over_warm_p50": pct(packed_ttft, 50) / pct(warm_ttft, 50),
+                    "cold_packed_streamed_bytes": cold_packed[0].streamed_bytes,
+                    "cold_packed_stream_ms_p50": pct([r.stream_ms for r in cold_packed], 50),
+                    "pack_ratio": cold_packed[0].streamed_bytes / cold[0].streamed_bytes,
+                    "pack_setup_s": pack_s,
+                    "cold_plain_p50": pct(cold_ttft, 50), "cold_plain_p99": pct(cold_ttft, 99),
+                    "warm_p50": pct(warm_ttft, 50), "warm_p99": pct(warm_ttft, 99),
+                    "cold_plain_over_warm_p50": pct(cold_ttft, 50) / pct(warm_ttft, 50), "target_ratio": 1.2,
+                    "cold_device_p50": pct([r.device_ms for r in cold], 50),
+                    "stream_ms_p50": pct([r.stream_ms for r in cold], 50),
+                    "streamed_bytes": cold[0].streamed_bytes, "stream_gbs_p50": stream_gbs,
+                    "pcie_gen5_peak_gbs": 64.0,
+                    "cold_hbm_source_p50": pct([r.ttft_ms for r in cold_hbm], 50),
+                    "cold_hbm_source_p99": pct([r.ttft_ms for r in cold_hbm], 99),
+                    "cold_hbm_source_over_warm_p50": pct([r.ttft_ms for r in cold_hbm], 50) / pct(warm_ttft, 50),
+                    "hbm_source_stream_gbs_p50": statistics.median(
+                        r.streamed_bytes / (r.stream_ms / 1e3) / 1e9 for r in cold_hbm),
+                    "hbm_source_note": "layers 4..31 + lm_head streamed from a device-resident copy on the same "
+                                       "GPU (stand-in for an NVLink peer source; not a peer measurement)",
+                    "k_required": k_req, "cold_k_required_p50": pct([r.ttft_ms for r in cold_kreq], 50),
+                    "cold_k_required_p99": pct([r.ttft_ms for r in cold_kreq], 99),
+                    "cold_k_required_over_warm_p50": pct([r.ttft_ms for r in cold_kreq], 50) / pct(warm_ttft, 50),
+                    "k_required_packed": k_req_packed,
+                    "cold_k_required_packed_p50": pct([r.ttft_ms for r in cold_kreq_packed], 50),
+                    "cold_k_required_packed_p99": pct([r.ttft_ms for r in cold_kreq_packed], 99),
+                    "cold_k_required_packed_over_warm_p50":
+                        pct([r.ttft_ms for r in cold_kreq_packed], 50) / pct(warm_ttft, 50),
+                    "k_required_note": "k = required_prewarm_layers (cluster.py:145-166) at the measured PCIe "
+                                       "stream bandwidth (plain / packed) and the measured per-token prefill cost"},
+
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -539,6 +667,7 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=12288)
     ap.add_argument("--switch-iters", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ttft-prompts", type=int, default=100)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--decode-ctx", type=int, default=1024)
     ap.add_argument("--decode-batches", type=lambda v: [int(x) for x in v.split(",") if x], default=[1, 16, 64])

@@ -130,17 +130,30 @@ def forward(cfg, w: dict, tokens, pos0: int = 0, past: list | None = None):
     return h @ w["lm_head"].T, new_past
 
 
-def forward_streamed(cfg, layout, flat_bf16: torch.Tensor, tokens, heads_per_chunk: int = 8) -> torch.Tensor:
+def forward_streamed(cfg, layout, flat_bf16: torch.Tensor, tokens, heads_per_chunk: int = 8,
+                     emulate_bf16: bool = False) -> torch.Tensor:
     """Last-row logits [vocab] of ``forward`` without materialising the whole
     fp32 model: each tensor is upcast from the bf16 image when its layer runs
     (a full-size Llama-3-8B needs ~1 GB of fp32 weights at a time instead of
     32 GB). Same math, same order of operations as ``forward`` with pos0 = 0;
     attention runs ``heads_per_chunk`` heads at a time to bound the S x S
-    score buffers."""
+    score buffers.
+
+    ``emulate_bf16=True`` is the *bf16 floor*: the same fp32 math with every
+    tensor a bf16 kernel path must hold in bf16 rounded to bf16 — the
+    normalised activations fed to the QKV and gate/up GEMMs, q/k/v after
+    RoPE (the KV cache), the unnormalised softmax numerators exp(s - max)
+    fed to the PV product (normalised in fp32 afterwards), the attention
+    output fed to O, the SwiGLU output fed to down, and the final normalised
+    row fed to the lm_head; the residual stream and every accumulation stay
+    fp32. Any bf16 implementation carries at least this rounding; its
+    distance to the fp32 logits is the accuracy a bf16 forward can reach on
+    these weights."""
     tokens = torch.as_tensor(tokens, dtype=torch.long)
     S = tokens.numel()
     H, KV, hd, d = cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.hidden
     cos, sin = rope_table(hd, cfg.rope_theta, S)
+    R = (lambda v: v.bfloat16().float()) if emulate_bf16 else (lambda v: v)
 
     def t(off, *shape):
         n = int(np.prod(shape))
@@ -149,13 +162,13 @@ def forward_streamed(cfg, layout, flat_bf16: torch.Tensor, tokens, heads_per_chu
     x = flat_bf16[layout.embed // 2: layout.embed // 2 + cfg.vocab * d].view(cfg.vocab, d)[tokens].float()
     causal = torch.ones(S, S, dtype=torch.bool).triu(1)[None]
     for L in layout.layers:
-        h = _rms(x, t(L["attn_norm"], d), cfg.rms_eps)
+        h = R(_rms(x, t(L["attn_norm"], d), cfg.rms_eps))
         qkv = h @ t(L["wqkv"], cfg.qkv_dim, d).T
         if L["bqkv"] >= 0:
             qkv = qkv + t(L["bqkv"], cfg.qkv_dim)
-        q = _rope(qkv[:, : H * hd].view(S, H, hd), cos, sin)
-        k = _rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin)
-        v = qkv[:, (H + KV) * hd:].view(S, KV, hd)
+        q = R(_rope(qkv[:, : H * hd].view(S, H, hd), cos, sin))
+        k = R(_rope(qkv[:, H * hd: (H + KV) * hd].view(S, KV, hd), cos, sin))
+        v = R(qkv[:, (H + KV) * hd:].view(S, KV, hd))
         g = H // KV
         o = torch.empty(S, H, hd)
         for h0 in range(0, H, heads_per_chunk):
@@ -164,12 +177,16 @@ def forward_streamed(cfg, layout, flat_bf16: torch.Tensor, tokens, heads_per_chu
             vv = v[:, torch.arange(h0, h1) // g]
             sc = torch.einsum("shd,thd->hst", q[:, h0:h1], kk) / math.sqrt(hd)
             sc = sc.masked_fill(causal, float("-inf"))
-            o[:, h0:h1] = torch.einsum("hst,thd->shd", torch.softmax(sc, dim=-1), vv)
-        x = x + o.reshape(S, H * hd) @ t(L["wo"], d, H * hd).T
-        h = _rms(x, t(L["ffn_norm"], d), cfg.rms_eps)
+            if emulate_bf16:
+                e = torch.exp(sc - sc.amax(-1, keepdim=True))
+                o[:, h0:h1] = (torch.einsum("hst,thd->hsd", R(e), vv) / e.sum(-1, keepdim=True)).transpose(0, 1)
+            else:
+                o[:, h0:h1] = torch.einsum("hst,thd->shd", torch.softmax(sc, dim=-1), vv)
+        x = x + R(o.reshape(S, H * hd)) @ t(L["wo"], d, H * hd).T
+        h = R(_rms(x, t(L["ffn_norm"], d), cfg.rms_eps))
         wg, wu = split_gate_up(t(L["wgu"], 2 * cfg.ffn, d), cfg.ffn)
-        x = x + (torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ t(L["wdown"], d, cfg.ffn).T
-    h = _rms(x[-1:], t(layout.final_norm, d), cfg.rms_eps)
+        x = x + R(torch.nn.functional.silu(h @ wg.T) * (h @ wu.T)) @ t(L["wdown"], d, cfg.ffn).T
+    h = R(_rms(x[-1:], t(layout.final_norm, d), cfg.rms_eps))
     rows = cfg.lm_head_rows or cfg.vocab
     out = torch.empty(rows)
     step = 16384

@@ -155,6 +155,8 @@ def test_tiny_greedy_agreement_256_prompts(tiny):
         w.prewarm(cfg.name, layers=cfg.layers)
     inst, *_ = w.switch_memory(cfg.name)
     agree, rels, margins, hits, noise = 0, [], [], [], []
+    emu_rels, emu_hits = [], 0
+    flat_img = w.models[cfg.name].host  # the pinned bf16 image the worker streams from
     n = 256
     for s in range(n):
         prompt = _prompt(cfg, 1000 + s)
@@ -164,6 +166,9 @@ def test_tiny_greedy_agreement_256_prompts(tiny):
         w.close_seq(seq)
         ref, _ = O.forward(cfg, weights, prompt.long())
         r = ref[-1]
+        emu = O.forward_streamed(cfg, cfg.layout(), flat_img, prompt.long(), emulate_bf16=True)
+        emu_rels.append(_rel(emu, r))
+        emu_hits += int(int(emu.argmax()) == int(r.argmax()))
         rels.append(_rel(got, r))
         top2 = r.topk(2).values
         margins.append((top2[0] - top2[1]).item())
@@ -177,6 +182,8 @@ def test_tiny_greedy_agreement_256_prompts(tiny):
     # a disagreement can be read against its fp32 top1-top2 margin.
     report = {"config": "tiny (2 layers, d=256, vocab 4096), 512-token prompts, seeds 1000..1255",
               "agree": agree, "n": n, "logit_rel_max": max(rels), "logit_rel_mean": sum(rels) / n,
+              "bf16_floor": {"agree": emu_hits, "logit_rel_max": max(emu_rels), "logit_rel_mean": sum(emu_rels) / n,
+                             "what": "oracle with every bf16-held tensor rounded (forward_streamed emulate_bf16)"},
               "max_abs_logit_err": max(noise), "ref_margin_min": min(margins),
               "ref_margin_median": sorted(margins)[n // 2],
               "disagreements": [{"seed": 1000 + i, "ref_margin": m} for i, (h, m) in enumerate(zip(hits, margins))
