@@ -34,6 +34,8 @@ extern "C" {
 #define WS_ERR_CUDA 6             /* CUDA runtime / driver failure              */
 #define WS_ERR_NO_DEVICE 7        /* device op on a ledger-only pool            */
 #define WS_ERR_KV_BUSY 8          /* KV shrink would drop live blocks           */
+#define WS_ERR_FRAGMENTED 9       /* device pool: no slot placement exists at   *
+                                   * the physical handle granularity            */
 
 const char* ws_last_error(void);
 int ws_version(int* major, int* minor);
@@ -89,20 +91,26 @@ int ws_background_kv_mapping(int64_t pages, double map_ms_per_page, double consu
  * operations that touch it. device < 0 gives a ledger-only pool (host
  * bookkeeping, identical page identities, no CUDA calls).
  *
- * Device pools pre-create every physical 2 MiB page with cuMemCreate and
- * alias all of them into one "page window" VA at init, so converting pages
- * between weight slots and the KV cache never calls the driver on the
- * critical path; slot VAs (one reservation per prewarm slot, weights at its
- * start — PAPER.md:420-453) are mapped at prewarm time and unmapped by a
- * background worker (engine.py:615-632 async-unmap contract).
+ * Device pools back the ledger's pages with physical handles of
+ * `handle_pages` pages each (cuMemCreate; default 16 x 2 MiB = 32 MiB — the
+ * driver's cost is per handle, so a full-HBM pool builds in about a second),
+ * all mapped once, in page order, into one "page window" VA at init (page p
+ * at window + p*page_size). KV blocks address pages through the window, so
+ * converting pages between weight slots and the KV cache never calls the
+ * driver (PAPER.md:420-453 slots, engine.py:615-632 async unmap).
  *
  * Page identity rules (documented, deterministic; the reference pins only
- * counts): a new slot takes the lowest-id free pages (a keyed slot on a device
- * pool first reclaims, at the same slot index, the still-free pages its cached
- * VA maps, so a re-prewarm needs no driver calls for them); promotion turns every
- * free page into KV; a KV shrink returns the highest-id KV pages, migrating
- * any live KV block that sits on one of them to the lowest-id unallocated
- * KV page that stays.
+ * counts): a new slot takes (1) for a keyed slot, the run of pages it held
+ * last time if that run is free; else (2) the lowest contiguous run of free
+ * pages — a WINDOWED slot whose VA is window + first*page_size, created and
+ * evicted with zero driver calls; else (3) a COMPOSITE placement: the longest
+ * free suffix of one handle, then whole free handles (lowest first), then
+ * the shortest sufficient free prefix of one more handle, each handle mapped
+ * whole into a private VA reservation (unmapped asynchronously on evict);
+ * else a device pool fails with WS_ERR_FRAGMENTED and a ledger-only pool
+ * takes the lowest free pages. Promotion turns every free page into KV; a
+ * KV shrink returns the highest-id KV pages, migrating any live KV block that
+ * sits on one of them to the lowest-id unallocated KV page that stays.
  * ==================================================================== */
 typedef struct ws_pool ws_pool;
 
@@ -119,6 +127,10 @@ typedef struct ws_pool_counts {
 } ws_pool_counts;
 
 int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out);
+/* Same with an explicit physical handle size in pages (ws_pool_create: 16). */
+int ws_pool_create_ex(int32_t device, int64_t total_pages, int64_t page_size, int64_t handle_pages,
+                      ws_pool** out);
+int ws_pool_handle_pages(ws_pool* pool, int64_t* handle_pages_out);
 int ws_pool_destroy(ws_pool* pool);
 int ws_pool_counts_get(ws_pool* pool, ws_pool_counts* out);
 /* Host copy of the page-ownership map: -1 free, -2 KV, >=0 owning slot id. */
@@ -127,8 +139,10 @@ int ws_pool_owner_map(ws_pool* pool, int32_t* out, int64_t n);
 int ws_pool_device_owner_map(ws_pool* pool, int32_t* host_out, int64_t n);
 /* Base of the page window (page p lives at base + p*page_size). */
 int ws_pool_window(ws_pool* pool, void** base_out);
-/* Measured driver cost of the last slot map / init (ms), for the μ report. */
-int ws_pool_timing(ws_pool* pool, double* init_ms, double* last_map_ms_per_page,
+/* Measured driver cost (ms) of the pool init, of slot mapping per slot page
+ * placed on the device so far (windowed slots count as 0 — the memswitch.py
+ * μ this hardware achieves), and of the last async unmap per page. */
+int ws_pool_timing(ws_pool* pool, double* init_ms, double* map_ms_per_slot_page,
                    double* last_unmap_ms_per_page);
 /* Wait for the background unmap worker to drain. */
 int ws_pool_sync_unmaps(ws_pool* pool);
@@ -137,12 +151,12 @@ int ws_pool_sync_unmaps(ws_pool* pool);
  * map_now=1 maps all of them before returning (device pools); map_now=0 lets
  * the caller drive ws_slot_map_chunk() from the pipelined loader. */
 int ws_slot_create(ws_pool* pool, int64_t slot_id, int64_t pages, int32_t map_now, void** va_out);
-/* Same, with a per-model key (nonzero): the slot VA is cached across
- * evictions, so a later slot of the same model only remaps the pages whose
- * physical identity changed (evicted keyed slots keep their mappings). */
+/* Same, with a per-model key (nonzero): the model's next slot takes back the
+ * page run its last windowed slot held if that run is free (rule 1 above). */
 int ws_slot_create_keyed(ws_pool* pool, int64_t slot_id, int64_t pages, int32_t map_now, uint64_t key,
                          void** va_out);
-/* Slot pages mapped by the driver vs served from the VA cache, since create. */
+/* Slot pages mapped by the driver (composite) vs addressed through the page
+ * window with no driver call (windowed), since create. */
 int ws_pool_map_stats(ws_pool* pool, int64_t* remapped_pages, int64_t* reused_pages);
 /* Map pages [first, first+count) of the slot into its VA (memswitch.py:78-88
  * per-chunk map step). */
@@ -152,6 +166,9 @@ int ws_slot_map_chunk(ws_pool* pool, int64_t slot_id, int64_t first, int64_t cou
 int ws_slot_evict(ws_pool* pool, int64_t slot_id, void* fence_stream);
 int ws_slot_info(ws_pool* pool, int64_t slot_id, int64_t* pages_out, int64_t* mapped_out, void** va_out);
 int ws_slot_pages(ws_pool* pool, int64_t slot_id, int32_t* ids_out, int64_t cap, int64_t* n_out);
+/* Placement of a slot: kind 0 windowed, 1 composite, 2 scattered (ledger-only
+ * pools); handles_out = physical handles a composite slot maps. */
+int ws_slot_placement(ws_pool* pool, int64_t slot_id, int32_t* kind_out, int64_t* handles_out);
 
 /* promote_to_dedicated KV step (cluster.py:332-338): every free page becomes
  * KV; capacity = mapped = the resulting KV page count. */

@@ -21,6 +21,7 @@ WS_ERR_STATE = 5
 WS_ERR_CUDA = 6
 WS_ERR_NO_DEVICE = 7
 WS_ERR_KV_BUSY = 8
+WS_ERR_FRAGMENTED = 9
 
 
 class NativeError(RuntimeError):
@@ -80,6 +81,8 @@ SIGNATURES: dict[str, list] = {
     "ws_pipelined_load": [i64, f64, f64, i64, i64, P(TransferPlanC)],
     "ws_background_kv_mapping": [i64, f64, f64, P(f64)],
     "ws_pool_create": [i32, i64, i64, P(vp)],
+    "ws_pool_create_ex": [i32, i64, i64, i64, P(vp)],
+    "ws_pool_handle_pages": [vp, P(i64)],
     "ws_pool_destroy": [vp],
     "ws_pool_counts_get": [vp, P(PoolCounts)],
     "ws_pool_owner_map": [vp, P(i32), i64],
@@ -94,6 +97,7 @@ SIGNATURES: dict[str, list] = {
     "ws_slot_evict": [vp, i64, vp],
     "ws_slot_info": [vp, i64, P(i64), P(i64), P(vp)],
     "ws_slot_pages": [vp, i64, P(i32), i64, P(i64)],
+    "ws_slot_placement": [vp, i64, P(i32), P(i64)],
     "ws_kv_map_all": [vp, vp, P(i64)],
     "ws_kv_reclaim": [vp, i32, i32, f64, vp, P(i64)],
     "ws_kv_resize": [vp, i64, vp],

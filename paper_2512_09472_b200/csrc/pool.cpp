@@ -1,15 +1,34 @@
 // Per-GPU page pool: the page ledger of a universal worker and the CUDA VMM
-// pages behind it.
+// memory behind it.
 //
 // Host ledger (single writer, mutated synchronously before device work is
 // enqueued — cluster.py:200-201) replaces GpuWorker's page counters
-// (cluster.py:110-129) and adds page identities. Device pools own every
-// physical 2 MiB page (cuMemCreate at init), alias them all into
-// one page-window VA so KV blocks address physical pages directly (weight<->KV
-// conversion needs no driver call), map each prewarm slot's pages into its own
-// VA reservation (weights at the slot start) and unmap
-// evicted slots on a background worker (async-unmap contract,
-// engine.py:615-632).
+// (cluster.py:110-129) and adds page identities.
+//
+// Physical memory: the ledger's 2 MiB pages are backed by physical handles of
+// `hpages` pages each (default 16 = 32 MiB; cuMemCreate), all mapped once,
+// in page order, into one "page window" VA at init — page p lives at
+// window + p * page. The driver's cost is per handle, not per byte (on this
+// B200: create + map + set-access ~0.3-1.8 ms per 2 MiB handle vs ~10 us per
+// 2 MiB with 32 MiB handles, profiles/r1_vmm_granularity.json), so large
+// handles make a full-HBM pool cheap to build.
+//
+// KV blocks address pages through the window: weight<->KV conversion is a
+// ledger update + the switch kernel, never a driver call.
+//
+// Prewarm slots: a slot is placed, by a deterministic rule
+// the host ledger and the device agree on, as
+//   * WINDOWED  — the lowest contiguous run of free pages: the slot's VA is
+//                 window + first * page, zero driver calls to create or evict;
+//   * COMPOSITE — when no run is long enough: [free suffix of one handle] +
+//                 whole free handles + [free prefix of one handle], each
+//                 handle mapped whole into a private VA reservation (with one
+//                 handle of slack either side) — driver cost per 32 MiB, and
+//                 evicted composite slots are unmapped by a background worker
+//                 (async-unmap contract, engine.py:615-632);
+//   * a ledger-only pool (no device) falls back to the lowest free pages when
+//     even a composite placement does not exist; a device pool refuses
+//     (WS_ERR_FRAGMENTED) before any state changes.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -35,22 +54,25 @@ double now_ms() {
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-struct Slot {
-  std::vector<int32_t> pages;  // slot page j -> physical page id
-  int64_t mapped = 0;          // pages [0, mapped) mapped into the slot VA
-  int va = -1;                 // index into ws_pool::vas
-  uint64_t key = 0;            // model key of a cached VA (0: unkeyed slot)
+enum SlotKind { kWindowed = 0, kComposite = 1, kScattered = 2 };
+
+// One whole physical handle mapped into a composite slot's VA, at slot page
+// offset `off` (negative for the head handle, whose first pages are not the
+// slot's).
+struct Seg {
+  int32_t handle;
+  int64_t off;
 };
 
-// Per-model VA cache: an evicted keyed slot keeps its VA mappings (nothing
-// reads them while the model is not active), so re-prewarming the same model
-// only remaps the slot pages whose physical page changed. Driver map/access
-// calls cost ~0.2-1.5 ms per 2 MiB handle on this B200, so this turns a
-// re-prewarm of an 8B slot from seconds into (usually) zero driver calls.
-struct CachedVa {
-  int va = -1;
-  std::vector<int32_t> phys;  // physical page mapped at slot page j, -1 if none
-  bool in_use = false;
+struct Slot {
+  std::vector<int32_t> pages;  // slot page j -> physical page id
+  int64_t mapped = 0;          // pages [0, mapped) addressable through the slot VA
+  int kind = kWindowed;
+  int va = -1;                 // composite: index into ws_pool::vas
+  CUdeviceptr base = 0;        // slot VA (device pools)
+  std::vector<Seg> segs;       // composite: handle mappings in slot-page order
+  size_t segs_mapped = 0;      // segments [0, segs_mapped) are mapped
+  uint64_t key = 0;
 };
 
 struct VaRange {
@@ -60,8 +82,7 @@ struct VaRange {
 
 struct UnmapJob {
   int va;
-  CUdeviceptr base;  // copied at enqueue: ws_pool::vas may grow concurrently
-  int64_t mapped;
+  std::vector<std::pair<CUdeviceptr, size_t>> maps;  // (address, bytes) of every mapped handle
   cudaEvent_t fence;
 };
 
@@ -101,7 +122,8 @@ struct ws_pool {
   int bt_next = 0;
   // ---- device ----
   const ws::Driver* drv = nullptr;
-  std::vector<CUmemGenericAllocationHandle> handles;
+  std::vector<CUmemGenericAllocationHandle> handles;  // handle h backs pages [h*hpages, ...)
+  int64_t hpages = 16;                                // ledger pages per physical handle
   CUdeviceptr window = 0;
   int32_t* owner_dev = nullptr;
   char* stage_host = nullptr;  // pinned staging for switch lists
@@ -110,9 +132,11 @@ struct ws_pool {
   cudaEvent_t stage_ev = nullptr, sw_start = nullptr, sw_stop = nullptr;
   bool sw_recorded = false;
   int64_t sw_entries = 0;
-  std::vector<VaRange> vas;
-  std::unordered_map<uint64_t, CachedVa> va_cache;
-  int64_t remapped_pages = 0, reused_pages = 0;
+  std::vector<VaRange> vas;                           // composite-slot VA reservations
+  std::unordered_map<uint64_t, int64_t> last_first;   // keyed windowed slot -> its last first page
+  int64_t remapped_pages = 0, reused_pages = 0;       // slot pages mapped by the driver / by the window
+  int64_t placed_pages = 0;                           // device slot pages placed (for the per-page cost)
+  double map_ms_total = 0;
   // ---- background unmap worker ----
   std::mutex mu;
   std::condition_variable cv, cv_done;
@@ -123,7 +147,9 @@ struct ws_pool {
   double init_ms = 0, map_ms_per_page = 0, unmap_ms_per_page = 0;
 
   bool on_device() const { return dev >= 0; }
-  CUdeviceptr va_base(int i) const { return vas[i].base; }
+  int64_t n_handles() const { return (n + hpages - 1) / hpages; }
+  int64_t handle_size(int64_t h) const { return std::min(hpages, n - h * hpages); }  // in pages
+  size_t va_bytes() const { return (size_t)((n + 2 * hpages) * page); }
 };
 
 namespace {
@@ -194,7 +220,7 @@ void unmap_worker(ws_pool* p) {
       std::unique_lock<std::mutex> lk(p->mu);
       p->cv.wait(lk, [&] { return p->stop || !p->jobs.empty(); });
       if (p->jobs.empty()) return;
-      job = p->jobs.front();
+      job = std::move(p->jobs.front());
       p->jobs.pop_front();
     }
     if (job.fence) {
@@ -202,10 +228,14 @@ void unmap_worker(ws_pool* p) {
       cudaEventDestroy(job.fence);
     }
     double t0 = now_ms();
-    for (int64_t j = 0; j < job.mapped; ++j) p->drv->cuMemUnmap(job.base + j * p->page, p->page);
+    int64_t pages = 0;
+    for (const auto& m : job.maps) {
+      p->drv->cuMemUnmap(m.first, m.second);
+      pages += (int64_t)(m.second / (size_t)p->page);
+    }
     double t1 = now_ms();
     std::lock_guard<std::mutex> lk(p->mu);
-    if (job.mapped) p->unmap_ms_per_page = (t1 - t0) / (double)job.mapped;
+    if (pages) p->unmap_ms_per_page = (t1 - t0) / (double)pages;
     p->vas[job.va].busy = false;
     p->pending -= 1;
     p->cv_done.notify_all();
@@ -221,50 +251,128 @@ int acquire_va(ws_pool* p, int* out) {
       return WS_OK;
     }
   VaRange r;
-  DRV(p->drv->cuMemAddressReserve(&r.base, (size_t)(p->n * p->page), (size_t)p->page, 0, 0));
+  DRV(p->drv->cuMemAddressReserve(&r.base, p->va_bytes(), (size_t)(p->hpages * p->page), 0, 0));
   r.busy = true;
   p->vas.push_back(r);
   *out = (int)p->vas.size() - 1;
   return WS_OK;
 }
 
+// Make slot pages [first, first + count) addressable through the slot VA
+// (memswitch.py:78-88 per-chunk map step). Windowed slots alias the page
+// window: nothing to do. Composite slots map every handle segment that
+// covers a page of the range and is not mapped yet, then grant access to the
+// newly mapped span in one call.
 int map_range(ws_pool* p, Slot& s, int64_t first, int64_t count) {
   if (first != s.mapped) WS_FAIL(WS_ERR_INVALID, "slot pages must be mapped in order");
   if (first + count > (int64_t)s.pages.size()) WS_FAIL(WS_ERR_INVALID, "map beyond slot");
-  if (!p->on_device() || count == 0) {
-    s.mapped += count;
+  s.mapped += count;
+  if (!p->on_device() || count == 0 || s.kind != kComposite) return WS_OK;
+  const double t0 = now_ms();
+  const size_t seg0 = s.segs_mapped;
+  int64_t lo = INT64_MAX, hi = INT64_MIN, pages = 0;
+  while (s.segs_mapped < s.segs.size() && s.segs[s.segs_mapped].off < s.mapped) {
+    const Seg& g = s.segs[s.segs_mapped];
+    const int64_t hs = p->handle_size(g.handle);
+    DRV(p->drv->cuMemMap(s.base + g.off * p->page, (size_t)(hs * p->page), 0, p->handles[g.handle], 0));
+    lo = std::min(lo, g.off);
+    hi = std::max(hi, g.off + hs);
+    pages += hs;
+    ++s.segs_mapped;
+  }
+  if (s.segs_mapped > seg0) {
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = p->dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    DRV(p->drv->cuMemSetAccess(s.base + lo * p->page, (size_t)((hi - lo) * p->page), &acc, 1));
+    p->remapped_pages += pages;
+  }
+  p->map_ms_total += now_ms() - t0;
+  return WS_OK;
+}
+
+// Slot placement (the identity rule; host ledger only, no side effects).
+// Returns WS_OK and fills `s.pages`, `s.kind`, `s.segs`, or
+// WS_ERR_FRAGMENTED when a device pool has no placement.
+int place_slot(const ws_pool* p, int64_t n, uint64_t key, Slot& s) {
+  s.pages.clear();
+  s.segs.clear();
+  const auto& own = p->owner;
+  auto run_free = [&](int64_t f) {
+    if (f < 0 || f + n > p->n) return false;
+    for (int64_t q = f; q < f + n; ++q)
+      if (own[q] != kOwnerFree) return false;
+    return true;
+  };
+  auto windowed = [&](int64_t f) {
+    s.kind = kWindowed;
+    for (int64_t q = f; q < f + n; ++q) s.pages.push_back((int32_t)q);
+    return WS_OK;
+  };
+  if (n == 0) return windowed(0);
+  // 1. a keyed slot takes back the run it held last time if it is free
+  if (key) {
+    auto it = p->last_first.find(key);
+    if (it != p->last_first.end() && run_free(it->second)) return windowed(it->second);
+  }
+  // 2. the lowest contiguous free run
+  for (int64_t q = 0, run = 0; q < p->n; ++q) {
+    run = own[q] == kOwnerFree ? run + 1 : 0;
+    if (run == n) return windowed(q - n + 1);
+  }
+  // 3. composite: [free suffix of one handle] + whole free handles + [free prefix of one handle]
+  const int64_t G = p->hpages, H = p->n_handles();
+  std::vector<int64_t> whole, fs(H), fp(H);
+  for (int64_t h = 0; h < H; ++h) {
+    const int64_t b = h * G, gs = p->handle_size(h);
+    int64_t nf = 0;
+    for (int64_t q = b; q < b + gs; ++q) nf += own[q] == kOwnerFree;
+    while (fp[h] < gs && own[b + fp[h]] == kOwnerFree) ++fp[h];
+    while (fs[h] < gs && own[b + gs - 1 - fs[h]] == kOwnerFree) ++fs[h];
+    if (nf == gs && gs == G) whole.push_back(h);
+  }
+  auto is_whole = [&](int64_t h) { return fp[h] == G; };
+  int64_t head = -1;  // the partial (or short last) handle with the longest free suffix
+  for (int64_t h = 0; h < H; ++h)
+    if (!is_whole(h) && fs[h] > 0 && (head < 0 || fs[h] > fs[head])) head = h;
+  int64_t got = head >= 0 ? fs[head] : 0;
+  if (got >= n) head = -1, got = 0;  // cannot happen (step 2 found no run) — defensive
+  const int64_t nw = std::min<int64_t>((n - got) / G, (int64_t)whole.size());
+  got += nw * G;
+  int64_t rem = n - got, tail = -1;
+  if (rem > 0) {
+    for (int64_t h = 0; h < H; ++h)  // best-fit partial prefix
+      if (h != head && !is_whole(h) && fp[h] >= rem && (tail < 0 || fp[h] < fp[tail])) tail = h;
+    if (tail < 0 && (int64_t)whole.size() > nw) tail = whole[nw];  // first rem pages of one more whole handle
+  }
+  if (rem > 0 && tail < 0) {
+    if (p->on_device())
+      WS_FAIL(WS_ERR_FRAGMENTED,
+              "slot of %lld pages cannot be placed: free pages are fragmented below the %lld-page physical "
+              "handle granularity", (long long)n, (long long)G);
+    s.kind = kScattered;  // ledger-only pool: identities only, lowest free pages
+    for (int64_t q = 0; q < p->n && (int64_t)s.pages.size() < n; ++q)
+      if (own[q] == kOwnerFree) s.pages.push_back((int32_t)q);
     return WS_OK;
   }
-  double t0 = now_ms();
-  CUdeviceptr base = p->va_base(s.va);
-  CUmemAccessDesc acc{};
-  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  acc.location.id = p->dev;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  std::vector<int32_t>* phys = nullptr;
-  if (s.key) {
-    phys = &p->va_cache[s.key].phys;
-    if ((int64_t)phys->size() < first + count) phys->resize(first + count, -1);
+  s.kind = kComposite;
+  int64_t off = 0;
+  if (head >= 0) {
+    const int64_t gs = p->handle_size(head), r = gs - fs[head];
+    s.segs.push_back({(int32_t)head, -r});
+    for (int64_t q = 0; q < fs[head]; ++q) s.pages.push_back((int32_t)(head * G + r + q));
+    off = fs[head];
   }
-  // map only pages whose cached physical page differs; coalesce SetAccess runs
-  int64_t run = -1, changed = 0;
-  for (int64_t j = first; j <= first + count; ++j) {
-    const bool need = j < first + count && (!phys || (*phys)[j] != s.pages[j]);
-    if (need) {
-      if (phys && (*phys)[j] >= 0) DRV(p->drv->cuMemUnmap(base + j * p->page, (size_t)p->page));
-      DRV(p->drv->cuMemMap(base + j * p->page, (size_t)p->page, 0, p->handles[s.pages[j]], 0));
-      if (phys) (*phys)[j] = s.pages[j];
-      if (run < 0) run = j;
-      ++changed;
-    } else if (run >= 0) {
-      DRV(p->drv->cuMemSetAccess(base + run * p->page, (size_t)((j - run) * p->page), &acc, 1));
-      run = -1;
-    }
+  for (int64_t i = 0; i < nw; ++i) {
+    s.segs.push_back({(int32_t)whole[i], off});
+    for (int64_t q = 0; q < G; ++q) s.pages.push_back((int32_t)(whole[i] * G + q));
+    off += G;
   }
-  if (changed) p->map_ms_per_page = (now_ms() - t0) / (double)changed;
-  p->remapped_pages += changed;
-  p->reused_pages += count - changed;
-  s.mapped += count;
+  if (rem > 0) {
+    s.segs.push_back({(int32_t)tail, off});
+    for (int64_t q = 0; q < rem; ++q) s.pages.push_back((int32_t)(tail * G + q));
+  }
   return WS_OK;
 }
 
@@ -324,12 +432,19 @@ int kv_grow(ws_pool* p, int64_t n, cudaStream_t stream) {
 extern "C" {
 
 int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out) {
+  return ws_pool_create_ex(device, total_pages, page_size, 16, out);
+}
+
+int ws_pool_create_ex(int32_t device, int64_t total_pages, int64_t page_size, int64_t handle_pages,
+                      ws_pool** out) {
   if (total_pages < 1 || page_size < 1) WS_FAIL(WS_ERR_INVALID, "pool needs pages and a page size");
   if (total_pages > (int64_t)INT32_MAX) WS_FAIL(WS_ERR_INVALID, "too many pages");
+  if (handle_pages < 1) WS_FAIL(WS_ERR_INVALID, "handle_pages must be >= 1");
   ws_pool* p = new ws_pool();
   p->dev = device;
   p->n = total_pages;
   p->page = page_size;
+  p->hpages = handle_pages;
   p->owner.assign(total_pages, kOwnerFree);
   p->kv_seq.assign(total_pages, -1);
   p->kv_blk.assign(total_pages, -1);
@@ -357,18 +472,27 @@ int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_po
       ws::set_error("page size is not a multiple of the VMM granularity");
       return fail(WS_ERR_INVALID);
     }
-    if (p->drv->cuMemAddressReserve(&p->window, (size_t)(total_pages * page_size), (size_t)page_size,
-                                    0, 0) != CUDA_SUCCESS) {
+    if (p->drv->cuMemAddressReserve(&p->window, (size_t)(total_pages * page_size),
+                                    (size_t)(handle_pages * page_size), 0, 0) != CUDA_SUCCESS) {
       ws::set_error("cuMemAddressReserve(window) failed");
       return fail(WS_ERR_CUDA);
     }
-    p->handles.resize(total_pages);
-    for (int64_t i = 0; i < total_pages; ++i) {
-      CUresult r = p->drv->cuMemCreate(&p->handles[i], (size_t)page_size, &prop, 0);
-      if (r == CUDA_SUCCESS) r = p->drv->cuMemMap(p->window + i * page_size, (size_t)page_size, 0,
-                                                  p->handles[i], 0);
+    const int64_t H = p->n_handles();
+    p->handles.reserve(H);
+    for (int64_t h = 0; h < H; ++h) {
+      const size_t bytes = (size_t)(p->handle_size(h) * page_size);
+      CUmemGenericAllocationHandle hd;
+      CUresult r = p->drv->cuMemCreate(&hd, bytes, &prop, 0);
+      if (r == CUDA_SUCCESS) {
+        p->handles.push_back(hd);
+        r = p->drv->cuMemMap(p->window + h * handle_pages * page_size, bytes, 0, hd, 0);
+      }
       if (r != CUDA_SUCCESS) {
-        p->handles.resize(i + (r == CUDA_SUCCESS ? 1 : 0));
+        // destroy unmaps and releases only the fully mapped handles
+        if ((int64_t)p->handles.size() == h + 1) {
+          p->drv->cuMemRelease(p->handles.back());
+          p->handles.pop_back();
+        }
         ws::set_error("cuMemCreate/cuMemMap of the page window failed (out of HBM?)");
         return fail(WS_ERR_CUDA);
       }
@@ -400,12 +524,23 @@ int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_po
       return fail(WS_ERR_CUDA);
     }
     cudaEventRecord(p->stage_ev, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      ws::set_error("pool init synchronize failed");
+      return fail(WS_ERR_CUDA);
+    }
     p->worker = std::thread(unmap_worker, p);
     p->init_ms = now_ms() - t0;
   }
   *out = p;
   return WS_OK;
 }
+
+namespace {
+void unmap_slot_now(ws_pool* p, const Slot& s) {
+  for (size_t i = 0; i < s.segs_mapped; ++i)
+    p->drv->cuMemUnmap(s.base + s.segs[i].off * p->page, (size_t)(p->handle_size(s.segs[i].handle) * p->page));
+}
+}  // namespace
 
 int ws_pool_destroy(ws_pool* p) {
   if (!p) return WS_OK;
@@ -421,14 +556,10 @@ int ws_pool_destroy(ws_pool* p) {
     cudaSetDevice(p->dev);
     cudaDeviceSynchronize();
     for (auto& kv : p->slots)
-      if (!kv.second.key)
-        for (int64_t j = 0; j < kv.second.mapped; ++j)
-          p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
-    for (auto& kv : p->va_cache)
-      for (size_t j = 0; j < kv.second.phys.size(); ++j)
-        if (kv.second.phys[j] >= 0) p->drv->cuMemUnmap(p->va_base(kv.second.va) + j * p->page, p->page);
-    for (auto& v : p->vas) p->drv->cuMemAddressFree(v.base, (size_t)(p->n * p->page));
-    for (size_t i = 0; i < p->handles.size(); ++i) p->drv->cuMemUnmap(p->window + i * p->page, p->page);
+      if (kv.second.kind == kComposite) unmap_slot_now(p, kv.second);
+    for (auto& v : p->vas) p->drv->cuMemAddressFree(v.base, p->va_bytes());
+    for (size_t h = 0; h < p->handles.size(); ++h)
+      p->drv->cuMemUnmap(p->window + h * p->hpages * p->page, (size_t)(p->handle_size(h) * p->page));
     for (auto h : p->handles) p->drv->cuMemRelease(h);
     if (p->window) p->drv->cuMemAddressFree(p->window, (size_t)(p->n * p->page));
     if (p->owner_dev) cudaFree(p->owner_dev);
@@ -489,7 +620,7 @@ int ws_pool_timing(ws_pool* p, double* init_ms, double* map_pp, double* unmap_pp
   if (int e = check_pool(p)) return e;
   std::lock_guard<std::mutex> lk(p->mu);
   *init_ms = p->init_ms;
-  *map_pp = p->map_ms_per_page;
+  *map_pp = p->placed_pages ? p->map_ms_total / (double)p->placed_pages : 0.0;
   *unmap_pp = p->unmap_ms_per_page;
   return WS_OK;
 }
@@ -498,6 +629,12 @@ int ws_pool_sync_unmaps(ws_pool* p) {
   if (int e = check_pool(p)) return e;
   std::unique_lock<std::mutex> lk(p->mu);
   p->cv_done.wait(lk, [&] { return p->pending == 0; });
+  return WS_OK;
+}
+
+int ws_pool_handle_pages(ws_pool* p, int64_t* handle_pages) {
+  if (int e = check_pool(p)) return e;
+  *handle_pages = p->hpages;
   return WS_OK;
 }
 
@@ -515,41 +652,20 @@ int ws_slot_create_keyed(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map
     WS_FAIL(WS_ERR_INSUFFICIENT, "insufficient pages (need %lld, free %lld)", (long long)pages,
             (long long)p->n_free);
   Slot s;
-  s.pages.assign(pages, -1);
-  // Identity rule: a keyed slot on a device pool first takes back, at the same
-  // slot index, every page its cached VA still maps that is free now (no
-  // driver call needed for those); every other index gets the lowest free
-  // page. Unkeyed / ledger-only slots: lowest free pages in order.
-  auto cached = (key && p->on_device()) ? p->va_cache.find(key) : p->va_cache.end();
-  if (cached != p->va_cache.end() && !cached->second.in_use) {
-    const auto& ph = cached->second.phys;
-    for (int64_t j = 0; j < pages && j < (int64_t)ph.size(); ++j)
-      if (ph[j] >= 0 && p->owner[ph[j]] == kOwnerFree) {
-        s.pages[j] = ph[j];
-        p->owner[ph[j]] = (int32_t)slot_id;  // claimed (final owner below)
-      }
-  }
-  {
-    int64_t q = 0;
-    for (int64_t j = 0; j < pages; ++j) {
-      if (s.pages[j] >= 0) continue;
-      while (p->owner[q] != kOwnerFree) ++q;
-      s.pages[j] = (int32_t)q++;
-    }
-  }
+  if (int e = place_slot(p, pages, key, s)) return e;
+  s.key = key;
   if (p->on_device()) {
     WS_CUDA(cudaSetDevice(p->dev));
-    auto hit = key ? p->va_cache.find(key) : p->va_cache.end();
-    if (hit != p->va_cache.end() && !hit->second.in_use) {
-      s.va = hit->second.va;  // mappings of the previous residency stay valid
-    } else {
-      if (hit != p->va_cache.end()) WS_FAIL(WS_ERR_DUPLICATE, "model key already has a live slot");
+    if (s.kind == kComposite) {
       if (int e = acquire_va(p, &s.va)) return e;
-      if (key) p->va_cache[key].va = s.va;
+      s.base = p->vas[s.va].base + (CUdeviceptr)(p->hpages * p->page);
+    } else {
+      s.base = p->window + (CUdeviceptr)(pages ? (int64_t)s.pages[0] * p->page : 0);
     }
-    if (key) p->va_cache[key].in_use = true;
-    s.key = key;
+    p->placed_pages += pages;
+    if (s.kind == kWindowed) p->reused_pages += pages;
   }
+  if (key && s.kind == kWindowed && pages) p->last_first[key] = s.pages[0];
   for (int32_t q : s.pages) p->owner[q] = (int32_t)slot_id;
   p->n_free -= pages;
   p->n_slot += pages;
@@ -558,7 +674,7 @@ int ws_slot_create_keyed(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map
   if (int e = device_switch(p, none, ref.pages, (int32_t)slot_id, {}, 0)) return e;
   if (map_now)
     if (int e = map_range(p, ref, 0, pages)) return e;
-  if (va_out) *va_out = p->on_device() ? reinterpret_cast<void*>(p->va_base(ref.va)) : nullptr;
+  if (va_out) *va_out = p->on_device() ? reinterpret_cast<void*>(ref.base) : nullptr;
   return WS_OK;
 }
 
@@ -581,16 +697,16 @@ int ws_slot_evict(ws_pool* p, int64_t slot_id, void* fence_stream) {
   if (!p->on_device()) return WS_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(fence_stream);
   if (int e = device_switch(p, one_rule((int32_t)slot_id, kOwnerFree), {}, 0, {}, st)) return e;
-  if (s.key) {  // keep the mappings for the next residency of this model
-    p->va_cache[s.key].in_use = false;
-    return WS_OK;
-  }
-  UnmapJob job{s.va, p->va_base(s.va), s.mapped, nullptr};
+  if (s.kind != kComposite) return WS_OK;  // windowed: the window mapping stays, nothing to undo
+  UnmapJob job;
+  job.va = s.va;
+  for (size_t i = 0; i < s.segs_mapped; ++i)
+    job.maps.emplace_back(s.base + s.segs[i].off * p->page, (size_t)(p->handle_size(s.segs[i].handle) * p->page));
   WS_CUDA(cudaEventCreateWithFlags(&job.fence, cudaEventDisableTiming));
   WS_CUDA(cudaEventRecord(job.fence, st));
   {
     std::lock_guard<std::mutex> lk(p->mu);
-    p->jobs.push_back(job);
+    p->jobs.push_back(std::move(job));
     p->pending += 1;
   }
   p->cv.notify_all();
@@ -603,7 +719,16 @@ int ws_slot_info(ws_pool* p, int64_t slot_id, int64_t* pages, int64_t* mapped, v
   if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
   if (pages) *pages = (int64_t)it->second.pages.size();
   if (mapped) *mapped = it->second.mapped;
-  if (va) *va = p->on_device() ? reinterpret_cast<void*>(p->va_base(it->second.va)) : nullptr;
+  if (va) *va = p->on_device() ? reinterpret_cast<void*>(it->second.base) : nullptr;
+  return WS_OK;
+}
+
+int ws_slot_placement(ws_pool* p, int64_t slot_id, int32_t* kind, int64_t* handles_mapped) {
+  if (int e = check_pool(p)) return e;
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  *kind = it->second.kind;
+  *handles_mapped = (int64_t)it->second.segs.size();
   return WS_OK;
 }
 

@@ -37,10 +37,39 @@ def _owner(h, n, device=True):
     return out
 
 
-def test_slot_va_aliases_page_window(torch_cuda):
-    torch = torch_cuda
+def _check_slot_data(torch, h, n, va, ids):
+    """Write through the slot VA, read through the page window: slot page j
+    must be physical page ids[j]."""
     from paper_2512_09472_b200 import _native as N
     from paper_2512_09472_b200.devmem import view
+
+    slot = view(va, (len(ids) * PAGE // 4,), torch.int32)
+    slot.copy_(torch.arange(slot.numel(), device="cuda", dtype=torch.int32))
+    base = C.c_void_p()
+    N.call("ws_pool_window", h, C.byref(base))
+    win = view(base.value, (n * PAGE // 4,), torch.int32)
+    torch.cuda.synchronize()
+    per = PAGE // 4
+    for j, p in enumerate(ids):
+        assert torch.equal(win[p * per:(p + 1) * per], slot[j * per:(j + 1) * per]), (j, p)
+
+
+def _placement(h, sid):
+    from paper_2512_09472_b200 import _native as N
+
+    kind, nh = C.c_int32(), C.c_int64()
+    N.call("ws_slot_placement", h, sid, C.byref(kind), C.byref(nh))
+    ids = (C.c_int32 * 4096)()
+    cnt = C.c_int64()
+    N.call("ws_slot_pages", h, sid, ids, 4096, C.byref(cnt))
+    return kind.value, nh.value, list(ids)[: cnt.value]
+
+
+def test_windowed_slots_alias_the_page_window(torch_cuda):
+    """A slot on a contiguous free run IS a range of the page window: its VA
+    is window + first*page, created and evicted with no driver call."""
+    torch = torch_cuda
+    from paper_2512_09472_b200 import _native as N
 
     n = 64
     h = _pool(n)
@@ -50,30 +79,65 @@ def test_slot_va_aliases_page_window(torch_cuda):
         N.call("ws_slot_create", h, 1, 7, 1, C.byref(va2))
         N.call("ws_slot_evict", h, 0, None)
         va3 = C.c_void_p()
-        N.call("ws_slot_create", h, 2, 9, 1, C.byref(va3))  # takes pages 0-4 then 12-15
-        ids = (C.c_int32 * 9)()
-        cnt = C.c_int64()
-        N.call("ws_slot_pages", h, 2, ids, 9, C.byref(cnt))
-        assert list(ids) == [0, 1, 2, 3, 4, 12, 13, 14, 15]
-        slot = view(va3.value, (9 * PAGE // 4,), torch.int32)
-        slot.copy_(torch.arange(slot.numel(), device="cuda", dtype=torch.int32))
+        N.call("ws_slot_create", h, 2, 9, 1, C.byref(va3))  # pages 0-4 are too short: run 12-20
+        kind, nh, ids = _placement(h, 2)
+        assert (kind, nh, ids) == (0, 0, list(range(12, 21)))
         base = C.c_void_p()
         N.call("ws_pool_window", h, C.byref(base))
-        win = view(base.value, (n * PAGE // 4,), torch.int32)
-        torch.cuda.synchronize()
-        per = PAGE // 4
-        for j, p in enumerate(ids):
-            assert torch.equal(win[p * per:(p + 1) * per], slot[j * per:(j + 1) * per])
+        assert va3.value == base.value + 12 * PAGE and va2.value == base.value + 5 * PAGE
+        _check_slot_data(torch, h, n, va3.value, ids)
         host = _owner(h, n, device=False)
-        dev = _owner(h, n, device=True)
-        assert np.array_equal(host, dev)
-        assert host[:5].tolist() == [2] * 5 and host[5:12].tolist() == [1] * 7
+        assert np.array_equal(host, _owner(h, n, device=True))
+        assert host[5:12].tolist() == [1] * 7 and host[12:21].tolist() == [2] * 9
+        init_ms, map_pp, unmap_pp = C.c_double(), C.c_double(), C.c_double()
+        N.call("ws_pool_timing", h, C.byref(init_ms), C.byref(map_pp), C.byref(unmap_pp))
+        assert map_pp.value == 0.0  # no driver call for windowed slots
+        rm, ru = C.c_int64(), C.c_int64()
+        N.call("ws_pool_map_stats", h, C.byref(rm), C.byref(ru))
+        assert (rm.value, ru.value) == (0, 21)
+    finally:
+        N.call("ws_pool_destroy", h)
+
+
+def test_composite_slot_maps_whole_handles(torch_cuda):
+    """No contiguous run is long enough: the slot is [free suffix of handle 1]
+    + whole free handle 2 + [free prefix of handle 0], each 16-page handle
+    mapped whole into the slot's own VA; eviction unmaps asynchronously.
+    A placement that needs sub-handle pieces beyond one head and one tail
+    fails on a device pool (WS_ERR_FRAGMENTED) and changes nothing."""
+    torch = torch_cuda
+    from paper_2512_09472_b200 import _native as N
+
+    n = 96
+    h = _pool(n)
+    try:
+        for sid, pages in ((0, 12), (1, 8), (2, 28), (3, 8), (4, 40)):
+            N.call("ws_slot_create", h, sid, pages, 1, C.byref(C.c_void_p()))
+        N.call("ws_slot_evict", h, 0, None)  # frees 0-11
+        N.call("ws_slot_evict", h, 2, None)  # frees 20-47 (longest run: 28)
+        va = C.c_void_p()
+        N.call("ws_slot_create", h, 5, 36, 0, C.byref(va))
+        kind, nh, ids = _placement(h, 5)
+        assert kind == 1 and nh == 3
+        assert ids == list(range(20, 48)) + list(range(0, 8))
+        for first in range(0, 36, 10):  # the pipelined loader's chunked map
+            N.call("ws_slot_map_chunk", h, 5, first, min(10, 36 - first))
+        _check_slot_data(torch, h, n, va.value, ids)
+        assert np.array_equal(_owner(h, n, False), _owner(h, n, True))
+        N.call("ws_slot_evict", h, 3, None)  # free: 8-11 (mid-handle) and 48-55 (prefix of handle 3)
+        free_before = _owner(h, n, False)
+        rc = N.fns["ws_slot_create"](h, 6, 9, 1, C.byref(C.c_void_p()))
+        assert rc == N.WS_ERR_FRAGMENTED, rc
+        assert np.array_equal(_owner(h, n, False), free_before)
+        N.call("ws_slot_evict", h, 5, None)
         N.call("ws_pool_sync_unmaps", h)
         init_ms, map_pp, unmap_pp = C.c_double(), C.c_double(), C.c_double()
         N.call("ws_pool_timing", h, C.byref(init_ms), C.byref(map_pp), C.byref(unmap_pp))
-        print(f"\nVMM: init {init_ms.value:.1f} ms for {n} pages, map {map_pp.value*1e3:.1f} us/page, "
-              f"unmap {unmap_pp.value*1e3:.1f} us/page")
-        assert map_pp.value > 0 and unmap_pp.value > 0
+        rm, ru = C.c_int64(), C.c_int64()
+        N.call("ws_pool_map_stats", h, C.byref(rm), C.byref(ru))
+        print(f"\nVMM: init {init_ms.value:.1f} ms for {n} pages, map {map_pp.value*1e3:.1f} us per slot page "
+              f"({rm.value} driver-mapped, {ru.value} windowed), unmap {unmap_pp.value*1e3:.1f} us/page")
+        assert rm.value == 48 and unmap_pp.value > 0
     finally:
         N.call("ws_pool_destroy", h)
 

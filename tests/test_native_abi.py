@@ -84,3 +84,45 @@ def test_kv_shrink_migrates_live_blocks():
         assert own.tolist() == [-2] * 5 + [-1] * 5
     finally:
         N.call("ws_pool_destroy", h)
+
+
+def test_ledger_only_pool_placement_rules():
+    """The slot placement rule (include/warmserve.h) on a ledger-only pool with
+    16-page handles: lowest contiguous run; composite head suffix + whole
+    handles + tail prefix; scattered lowest free pages where a device pool
+    would report WS_ERR_FRAGMENTED; a keyed slot takes its last run back."""
+    h = C.c_void_p()
+    N.call("ws_pool_create_ex", -1, 96, 1, 16, C.byref(h))
+
+    def place(sid):
+        kind, nh = C.c_int32(), C.c_int64()
+        N.call("ws_slot_placement", h, sid, C.byref(kind), C.byref(nh))
+        ids = (C.c_int32 * 96)()
+        cnt = C.c_int64()
+        N.call("ws_slot_pages", h, sid, ids, 96, C.byref(cnt))
+        return kind.value, nh.value, list(ids)[: cnt.value]
+
+    try:
+        for sid, pages in ((0, 12), (1, 8), (2, 28), (3, 8), (4, 40)):
+            N.call("ws_slot_create", h, sid, pages, 1, C.byref(C.c_void_p()))
+        assert place(2) == (0, 0, list(range(20, 48)))
+        N.call("ws_slot_evict", h, 0, None)
+        N.call("ws_slot_evict", h, 2, None)
+        N.call("ws_slot_create", h, 5, 36, 1, C.byref(C.c_void_p()))
+        assert place(5) == (1, 3, list(range(20, 48)) + list(range(8)))
+        N.call("ws_slot_evict", h, 3, None)
+        N.call("ws_slot_create", h, 6, 9, 1, C.byref(C.c_void_p()))
+        assert place(6) == (2, 0, [8, 9, 10, 11, 48, 49, 50, 51, 52])
+    finally:
+        N.call("ws_pool_destroy", h)
+    h = C.c_void_p()
+    N.call("ws_pool_create", -1, 64, 1, C.byref(h))
+    try:
+        N.call("ws_slot_create_keyed", h, 0, 4, 1, 0, C.byref(C.c_void_p()))
+        N.call("ws_slot_create_keyed", h, 1, 6, 1, 77, C.byref(C.c_void_p()))  # pages 4-9
+        N.call("ws_slot_evict", h, 0, None)
+        N.call("ws_slot_evict", h, 1, None)
+        N.call("ws_slot_create_keyed", h, 2, 6, 1, 77, C.byref(C.c_void_p()))
+        assert place(2)[2] == list(range(4, 10))  # not the lowest run 0-5: its own last run
+    finally:
+        N.call("ws_pool_destroy", h)
