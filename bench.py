@@ -340,7 +340,11 @@ def run_ours(args, rank, world, local_rank):
     pack_s = time.perf_counter() - t_pack
     del flat
     torch.cuda.empty_cache()
-    w = UniversalWorker(dev, pool_pages=args.pool_pages, max_tokens=max(S, 256))
+    pool_pages = args.pool_pages
+    if pool_pages <= 0:  # a full-HBM universal worker: every byte but the reserve is pool
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        pool_pages = int((free_b - args.reserve_gib * (1 << 30)) // M.PAGE)
+    w = UniversalWorker(dev, pool_pages=pool_pages, max_tokens=max(S, 256))
     entry = w.register(cfg, host)
     slot = w.prewarm(cfg.name, layers=args.prewarm_layers)
     init_ms, map_pp, _ = (lambda a, b, c: (N.call("ws_pool_timing", w.gpu.pool, a, b, c), a, b, c))(
@@ -567,7 +571,7 @@ def run_ours(args, rank, world, local_rank):
                    "weight_source": "pinned host memory (PCIe H2D on the copy engine)",
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "no flush needed: 16 GB of weights per step > 126 MB L2",
-                   "pool_pages": args.pool_pages},
+                   "pool_pages": pool_pages, "pool_gib": pool_pages * M.PAGE / (1 << 30)},
         "e2e": {"value": e2e_value, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(statistics.median(r.streamed_bytes for r in cold_packed)) + S * 4,
                 "d2h_bytes_per_step": 4,
@@ -602,8 +606,13 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk_sum,
         "gpu_launches": launches,
         "setup_s": setup_s,
-        "vmm": {"pool_init_ms": init_ms.value, "slot_map_us_per_page": map_pp.value * 1e3,
-                "prewarm_ms": getattr(slot, "prewarm_ms", None)},
+        "vmm": {"pool_init_ms": init_ms.value, "pool_pages": pool_pages,
+                "slot_map_us_per_page": map_pp.value * 1e3, "reference_mu_us_per_page": 39.0,
+                "slot_placement": ["windowed", "composite", "scattered"][_placement(w, slot)],
+                "prewarm_ms": getattr(slot, "prewarm_ms", None),
+                "note": "2 MiB ledger pages backed by 32 MiB physical handles mapped once into the page window; "
+                        "a windowed slot is a window range (no driver call to map, evict or re-prewarm); "
+                        "reference mu = config.py:38"},
         # last key: the driver's stdout tail keeps the end of the line
         "ttft_ms": {"prompts": n_prompts, "prompt_seeds": "torch.Generator().manual_seed(1234), one 2048-token "
                     "prompt per activation",
@@ -645,6 +654,16 @@ def run_ours(args, rank, world, local_rank):
     w.close()
 
 
+def _placement(w, slot):
+    import ctypes as C
+
+    from paper_2512_09472_b200 import _native as N
+
+    kind, nh = C.c_int32(), C.c_int64()
+    N.call("ws_slot_placement", w.gpu.pool, slot.slot_id, C.byref(kind), C.byref(nh))
+    return kind.value
+
+
 def _cpu_model():
     try:
         for l in open("/proc/cpuinfo"):
@@ -664,7 +683,9 @@ def main():
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--prompt", type=int, default=2048)
     ap.add_argument("--prewarm-layers", type=int, default=4)
-    ap.add_argument("--pool-pages", type=int, default=12288)
+    ap.add_argument("--pool-pages", type=int, default=0, help="0: all free HBM but --reserve-gib")
+    ap.add_argument("--reserve-gib", type=float, default=24.0,
+                    help="HBM left outside the pool: the 16 GB HBM-source stand-in, workspace, graphs")
     ap.add_argument("--switch-iters", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ttft-prompts", type=int, default=100)

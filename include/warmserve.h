@@ -92,7 +92,7 @@ int ws_background_kv_mapping(int64_t pages, double map_ms_per_page, double consu
  * bookkeeping, identical page identities, no CUDA calls).
  *
  * Device pools back the ledger's pages with physical handles of
- * `handle_pages` pages each (cuMemCreate; default 16 x 2 MiB = 32 MiB — the
+ * `handle_pages` pages each (cuMemCreate; default 64 x 2 MiB = 128 MiB — the
  * driver's cost is per handle, so a full-HBM pool builds in about a second),
  * all mapped once, in page order, into one "page window" VA at init (page p
  * at window + p*page_size). KV blocks address pages through the window, so
@@ -127,7 +127,7 @@ typedef struct ws_pool_counts {
 } ws_pool_counts;
 
 int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out);
-/* Same with an explicit physical handle size in pages (ws_pool_create: 16). */
+/* Same with an explicit physical handle size in pages (ws_pool_create: 64). */
 int ws_pool_create_ex(int32_t device, int64_t total_pages, int64_t page_size, int64_t handle_pages,
                       ws_pool** out);
 int ws_pool_handle_pages(ws_pool* pool, int64_t* handle_pages_out);

@@ -6,12 +6,14 @@
 // (cluster.py:110-129) and adds page identities.
 //
 // Physical memory: the ledger's 2 MiB pages are backed by physical handles of
-// `hpages` pages each (default 16 = 32 MiB; cuMemCreate), all mapped once,
+// `hpages` pages each (default 64 = 128 MiB; cuMemCreate), all mapped once,
 // in page order, into one "page window" VA at init — page p lives at
 // window + p * page. The driver's cost is per handle, not per byte (on this
-// B200: create + map + set-access ~0.3-1.8 ms per 2 MiB handle vs ~10 us per
-// 2 MiB with 32 MiB handles, profiles/r1_vmm_granularity.json), so large
-// handles make a full-HBM pool cheap to build.
+// B200: create + map + set-access ~0.3-1.8 ms per 2 MiB handle vs ~4 us per
+// 2 MiB with 128 MiB handles, profiles/r1_vmm_granularity.json), so large
+// handles make a full-HBM pool cheap to build: 86,906 pages (170 GiB) in
+// 0.2-1.5 s with 64-page handles vs 1.4-8 s with 16-page ones
+// (profiles/r2_pool_init.txt).
 //
 // KV blocks address pages through the window: weight<->KV conversion is a
 // ledger update + the switch kernel, never a driver call.
@@ -23,7 +25,7 @@
 //   * COMPOSITE — when no run is long enough: [free suffix of one handle] +
 //                 whole free handles + [free prefix of one handle], each
 //                 handle mapped whole into a private VA reservation (with one
-//                 handle of slack either side) — driver cost per 32 MiB, and
+//                 handle of slack either side) — driver cost per handle, and
 //                 evicted composite slots are unmapped by a background worker
 //                 (async-unmap contract, engine.py:615-632);
 //   * a ledger-only pool (no device) falls back to the lowest free pages when
@@ -123,7 +125,7 @@ struct ws_pool {
   // ---- device ----
   const ws::Driver* drv = nullptr;
   std::vector<CUmemGenericAllocationHandle> handles;  // handle h backs pages [h*hpages, ...)
-  int64_t hpages = 16;                                // ledger pages per physical handle
+  int64_t hpages = 64;                                // ledger pages per physical handle
   CUdeviceptr window = 0;
   int32_t* owner_dev = nullptr;
   char* stage_host = nullptr;  // pinned staging for switch lists
@@ -432,7 +434,7 @@ int kv_grow(ws_pool* p, int64_t n, cudaStream_t stream) {
 extern "C" {
 
 int ws_pool_create(int32_t device, int64_t total_pages, int64_t page_size, ws_pool** out) {
-  return ws_pool_create_ex(device, total_pages, page_size, 16, out);
+  return ws_pool_create_ex(device, total_pages, page_size, 64, out);
 }
 
 int ws_pool_create_ex(int32_t device, int64_t total_pages, int64_t page_size, int64_t handle_pages,
@@ -744,8 +746,9 @@ int ws_slot_pages(ws_pool* p, int64_t slot_id, int32_t* ids, int64_t cap, int64_
 
 int ws_kv_map_all(ws_pool* p, void* stream, int64_t* kv_out) {
   if (int e = check_pool(p)) return e;
-  for (int64_t q = 0; q < p->n; ++q)
-    if (p->owner[q] == kOwnerFree) p->owner[q] = kOwnerKV;
+  int32_t* own = p->owner.data();
+  for (int64_t q = 0; q < p->n; ++q)  // branch-free: vectorises (89k pages in a few us)
+    own[q] = own[q] == kOwnerFree ? kOwnerKV : own[q];
   p->n_kv += p->n_free;
   p->n_free = 0;
   p->kv_cap = p->n_kv;
@@ -789,8 +792,9 @@ int ws_kv_resize(ws_pool* p, int64_t kv_pages, void* stream) {
 int ws_kv_release(ws_pool* p, void* stream) {
   if (int e = check_pool(p)) return e;
   if (p->n_alloc) WS_FAIL(WS_ERR_KV_BUSY, "KV release with %lld live blocks", (long long)p->n_alloc);
+  int32_t* own = p->owner.data();
   for (int64_t q = 0; q < p->n; ++q)
-    if (p->owner[q] == kOwnerKV) p->owner[q] = kOwnerFree;
+    own[q] = own[q] == kOwnerKV ? kOwnerFree : own[q];
   p->n_free += p->n_kv;
   p->n_kv = p->kv_cap = p->kv_used = 0;
   return device_switch(p, one_rule(kOwnerKV, kOwnerFree), {}, 0, {},

@@ -20,11 +20,11 @@ def torch_cuda(cuda_device):
     return torch
 
 
-def _pool(n_pages):
+def _pool(n_pages, handle_pages=16):
     from paper_2512_09472_b200 import _native as N
 
     h = C.c_void_p()
-    N.call("ws_pool_create", 0, n_pages, PAGE, C.byref(h))
+    N.call("ws_pool_create_ex", 0, n_pages, PAGE, handle_pages, C.byref(h))
     return h
 
 
