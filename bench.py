@@ -346,7 +346,7 @@ def run_ours(args, rank, world, local_rank):
         pool_pages = int((free_b - args.reserve_gib * (1 << 30)) // M.PAGE)
     w = UniversalWorker(dev, pool_pages=pool_pages, max_tokens=max(S, 256))
     entry = w.register(cfg, host)
-    slot = w.prewarm(cfg.name, layers=args.prewarm_layers)
+    slot = w.prewarm(cfg.name, layers=args.prewarm_layers, full=False)  # exactly k layers resident
     init_ms, map_pp, _ = (lambda a, b, c: (N.call("ws_pool_timing", w.gpu.pool, a, b, c), a, b, c))(
         *(__import__("ctypes").c_double() for _ in range(3)))[1:]
     prompt = torch.randint(0, cfg.vocab, (S,), generator=torch.Generator().manual_seed(7), dtype=torch.int32)

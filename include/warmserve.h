@@ -222,6 +222,12 @@ int ws_streamer_start_packed(ws_streamer* s, void* dst_base, const void* packed_
                              void* unpack_stream);
 /* Make `stream` wait until range i has landed (no-op if i >= started). */
 int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream);
+/* Host-side residency: number of leading ranges already landed (event
+ * query, never blocks) — the per-layer "layers_loaded" progress of a
+ * background prewarm (engine.py:426-432, 658-686). */
+int ws_streamer_progress(ws_streamer* s, int32_t* done_out);
+/* Block the host until range i has landed (the "ready" / "full" stages). */
+int ws_streamer_sync(ws_streamer* s, int32_t i);
 /* ms from start to each range's completion (after sync). */
 int ws_streamer_times(ws_streamer* s, float* ms_out, int32_t n);
 

@@ -114,6 +114,8 @@ SIGNATURES: dict[str, list] = {
     "ws_streamer_start": [vp, vp, vp, P(i64), i32, vp],
     "ws_streamer_start_packed": [vp, vp, vp, P(i64), i32, vp, i64, vp, vp],
     "ws_streamer_wait": [vp, i32, vp],
+    "ws_streamer_progress": [vp, P(i32)],
+    "ws_streamer_sync": [vp, i32],
     "ws_streamer_times": [vp, P(f32), i32],
     "ws_peer_buffer_bytes": [i64, P(i64)],
     "ws_peer_buffer_alloc": [i64, P(vp), P(C.c_uint8), i32],

@@ -112,6 +112,26 @@ int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream) {
   return WS_OK;
 }
 
+int ws_streamer_progress(ws_streamer* s, int32_t* done_out) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  int32_t d = 0;
+  while (d < s->started) {  // ranges complete in order (one copy stream)
+    cudaError_t e = cudaEventQuery(s->done[d]);
+    if (e == cudaErrorNotReady) break;
+    if (e != cudaSuccess) WS_FAIL(WS_ERR_CUDA, "cudaEventQuery: %s", cudaGetErrorString(e));
+    ++d;
+  }
+  *done_out = d;
+  return WS_OK;
+}
+
+int ws_streamer_sync(ws_streamer* s, int32_t i) {
+  if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
+  if (i < 0 || i >= s->started) return WS_OK;
+  WS_CUDA(cudaEventSynchronize(s->done[i]));
+  return WS_OK;
+}
+
 int ws_streamer_times(ws_streamer* s, float* ms_out, int32_t n) {
   if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
   for (int32_t i = 0; i < n && i < s->started; ++i) {

@@ -41,6 +41,17 @@ class ModelEntry:
 
 
 @dataclass
+class _Loader:
+    """Background prewarm of one slot: a streamer whose ranges are the
+    embedding, layers 0..L-1 and the final norm + lm_head (or only the
+    first k + 1 of them when the prewarm stops at k)."""
+    streamer: C.c_void_p
+    n_ranges: int = 0   # ranges still tracked (0: settled / idle)
+    full: bool = True
+    k: int = 0
+
+
+@dataclass
 class ActivationResult:
     model: str
     token: int
@@ -85,6 +96,7 @@ class UniversalWorker:
         self._graphs: dict = {}  # (model, batch, ctx bucket) -> (CUDAGraph, static seqs, pos, tokens)
         self.unpack = torch.cuda.Stream(self.dev)  # packed stream: rebuilds bf16 ranges in the slot
         self._staging = None
+        self._loaders: dict[int, _Loader] = {}  # slot id -> background prewarm streamer
 
     # ------------------------------------------------------------ models
     def register(self, cfg: ModelConfig, host_weights: torch.Tensor | None, max_batch: int = 32,
@@ -142,44 +154,118 @@ class UniversalWorker:
         return view(self.slot(name).va, (e.layout.total // 2,), torch.bfloat16, self.device)
 
     # ------------------------------------------------------------ prewarm
-    def prewarm(self, name: str, layers: int | None = None, chunk_pages: int = 64,
-                source: torch.Tensor | None = None) -> PrewarmSlot:
-        """prewarm(model, layers): take a slot (cluster.py:245-274), map all
-        of its pages chunk by chunk while the copy engine loads the
-        embedding + first ``layers`` decoder layers (memswitch.py:59-98
-        pipeline, run for real). ``layers=None`` uses the reference's
-        stall-free prefix k (required_prewarm_layers)."""
+    def prewarm(self, name: str, layers: int | None = None, source: torch.Tensor | None = None,
+                full: bool = True, wait: str | None = "ready") -> PrewarmSlot:
+        """prewarm(model, layers): take a slot (cluster.py:245-274) and start
+        loading the model into it on the copy engine (engine.py:885-919).
+
+        ``layers`` is the slot's required prefix k (``None``: the reference's
+        stall-free k, required_prewarm_layers at the worker's bandwidth). With
+        ``full=True`` (the reference's prewarm) the whole partition streams in
+        the background, layer by layer — "ready" once k layers have landed,
+        "full" at L (engine.py:658-686) — and the slot's ``layers_loaded`` /
+        ``weight_bytes_loaded`` follow the per-layer copy events
+        (``residency()``); ``full=False`` stops after k layers (a worker
+        prewarmed to exactly k, BASELINE configs[1]). ``wait``: "ready"
+        (return once k layers are resident), "full", or None (return at once).
+
+        One copy range per unit: the embedding, each decoder layer, then the
+        final norm + lm_head; a windowed slot needs no driver call at all, a
+        composite one maps its handles before the copies are queued."""
         e = self.models[name]
         if layers is None:
             layers = required_prewarm_layers(e.spec, self.cluster.bandwidth)
-        layers = max(0, min(layers, e.cfg.layers))
+        L = e.cfg.layers
+        layers = max(0, min(layers, L))
         pages = e.spec.partition_pages(self.page_size)
         slot = self.cluster.begin_prewarm(self.gpu, e.spec, pages, max(layers, 1))
-        src = source if source is not None else e.host
-        prefix = e.layout.prefix_bytes(layers) if layers < e.cfg.layers else e.layout.total
         t0 = time.perf_counter()
-        mapped = 0
-        with torch.cuda.stream(self.copy):
-            while mapped < pages:
-                n = min(chunk_pages, pages - mapped)
-                # map chunk c on the host while the copy engine moves chunk c-1
-                N.call("ws_slot_map_chunk", self.gpu.pool, slot.slot_id, mapped, n)
-                lo, hi = mapped * self.page_size, min((mapped + n) * self.page_size, prefix)
-                if hi > lo and src is not None:
-                    d = view(slot.va + lo, ((hi - lo) // 2,), torch.bfloat16, self.device)
-                    d.copy_(src[lo // 2: hi // 2], non_blocking=True)
-                mapped += n
-        self.copy.synchronize()
-        slot.load_start = None
+        N.call("ws_slot_map_chunk", self.gpu.pool, slot.slot_id, 0, pages)
+        map_ms = (time.perf_counter() - t0) * 1e3
+        src = source if source is not None else e.host
+        lay = e.layout
+        units = [(0, 0, lay.layers[0]["begin"])] + [(x["begin"], x["begin"], x["end"] - x["begin"]) for x in lay.layers]
+        units.append((lay.final_norm, lay.final_norm, lay.total - lay.final_norm))
+        n = len(units) if full else layers + 1
+        slot.layers_loaded = 0
+        slot.weight_bytes_loaded = 0.0
+        slot.load_start = time.perf_counter() * 1e3
         slot.load_finish = None
-        slot.layers_loaded = layers
-        slot.weight_bytes_loaded = float(prefix)
+        slot.map_ms = map_ms
+        if src is None:  # ledger/layout only (no weight image registered): nothing to copy
+            slot.layers_loaded = layers if not full else L
+            slot.weight_bytes_loaded = float(lay.prefix_bytes(slot.layers_loaded) if not full else lay.total)
+            slot.prewarm_ms = map_ms
+            return slot
+        ld = self._loader_for(slot)
+        flat = (C.c_int64 * (3 * n))(*[v for u in units[:n] for v in u])
+        self.copy.wait_stream(self.compute)  # the slot's pages may have held KV a moment ago
+        N.call("ws_streamer_start", ld.streamer, C.c_void_p(slot.va), C.c_void_p(src.data_ptr()), flat, n,
+               C.c_void_p(self.copy.cuda_stream))
+        ld.n_ranges, ld.full, ld.k = n, full, layers
+        if wait == "ready":  # range k = embedding + layers [0, k); k = L: everything
+            N.call("ws_streamer_sync", ld.streamer, layers if layers < L else n - 1)
+        elif wait == "full":
+            N.call("ws_streamer_sync", ld.streamer, n - 1)
+        self.residency(name)
         slot.prewarm_ms = (time.perf_counter() - t0) * 1e3
         return slot
+
+    def _loader_for(self, slot) -> "_Loader":
+        ld = self._loaders.get(slot.slot_id)
+        if ld is None:
+            st = C.c_void_p()
+            N.call("ws_streamer_create", 512, C.byref(st))
+            ld = self._loaders[slot.slot_id] = _Loader(st)
+        return ld
+
+    def residency(self, name: str) -> int:
+        """Refresh the slot's layer residency from the copy events of its
+        background prewarm (never blocks) and return ``layers_loaded`` — the
+        measured counterpart of the reference's linear _slot_layers_at
+        (engine.py:426-432): a layer counts once its bytes have landed."""
+        slot = self.slot(name)
+        if slot is None:
+            return 0
+        ld = self._loaders.get(slot.slot_id)
+        if ld is None or ld.n_ranges == 0:
+            return slot.layers_loaded
+        d = C.c_int32()
+        N.call("ws_streamer_progress", ld.streamer, C.byref(d))
+        e = self.models[name]
+        L = e.cfg.layers
+        got = max(0, min(d.value - 1, L))
+        slot.layers_loaded = max(slot.layers_loaded, got)
+        slot.weight_bytes_loaded = float(e.layout.prefix_bytes(slot.layers_loaded)) if d.value else 0.0
+        if d.value == ld.n_ranges:  # every range landed: settle (engine.py:634-640)
+            if ld.full:
+                slot.layers_loaded = L
+                slot.weight_bytes_loaded = float(e.layout.total)
+            slot.load_finish = time.perf_counter() * 1e3
+            ld.n_ranges = 0
+        return slot.layers_loaded
+
+    def _fence_loader(self, name: str) -> None:
+        """A forward that does not ride the slot's background prewarm layer by
+        layer waits (on the device) for all of it."""
+        slot = self.slot(name)
+        ld = self._loaders.get(slot.slot_id) if slot else None
+        if ld is not None and ld.n_ranges:
+            N.call("ws_streamer_wait", ld.streamer, ld.n_ranges - 1, C.c_void_p(self.compute.cuda_stream))
+            self.residency(name)
+
+    def wait_resident(self, name: str, layers: int | None = None) -> int:
+        """Block until ``layers`` (default: everything the prewarm loads) are resident."""
+        slot = self.slot(name)
+        ld = self._loaders.get(slot.slot_id) if slot else None
+        if ld is not None and ld.n_ranges:
+            N.call("ws_streamer_sync", ld.streamer, ld.n_ranges - 1 if layers is None else min(layers, ld.n_ranges - 1))
+        return self.residency(name)
 
     def drop_suffix(self, name: str, layers: int) -> None:
         """Forget residency of layers >= ``layers`` (bytes stay, ledger says
         they are gone), so the next activation streams them again."""
+        self.wait_resident(name)
         s = self.slot(name)
         e = self.models[name]
         s.layers_loaded = layers
@@ -192,7 +278,14 @@ class UniversalWorker:
         switch kernel, no driver call on this path. Returns (inst, evicted,
         host_ms, kernel_ms)."""
         e = self.models[name]
-        self.compute.wait_stream(self.copy)  # in-flight prewarm copies must not race KV reuse
+        # In-flight prewarm copies into slots this promote evicts must land
+        # before those pages become KV; the promoted slot's own background
+        # load keeps streaming (activate_instance waits on it layer by layer).
+        for other, s_ in self.gpu.slots.items():
+            ld = self._loaders.get(s_.slot_id)
+            if other != name and ld is not None and ld.n_ranges:
+                N.call("ws_streamer_wait", ld.streamer, ld.n_ranges - 1, C.c_void_p(self.compute.cuda_stream))
+                ld.n_ranges = 0
         t0 = time.perf_counter()
         inst, evicted = self.cluster.promote_to_dedicated((0,), e.spec, self.slot(name).required_prewarm_layers
                                                           if self.slot(name) else 1)
@@ -203,11 +296,21 @@ class UniversalWorker:
         self.active_model = name
         return inst, evicted, host_ms, kms.value
 
-    def reclaim(self, inflight: int, kv_used_bytes: float) -> int:
-        """KV->weights switch on a draining worker (cluster.py:351-365)."""
+    def kv_used_bytes(self) -> int:
+        """Device truth for the reference's _kv_used_bytes (engine.py:391-404):
+        the bytes of the KV pages that hold live blocks of open sequences (the
+        reference counts tokens x kv_bytes_per_token; a page is the block, so
+        this is the token count rounded up per sequence to whole blocks —
+        exactly the pages a shrink must keep)."""
+        return self.gpu.counts().kv_pages_allocated * self.page_size
+
+    def reclaim(self, inflight: int, kv_used_bytes: float | None = None) -> int:
+        """KV->weights switch on a draining worker (cluster.py:351-365).
+        ``kv_used_bytes=None`` takes the pool's live blocks (kv_used_bytes())."""
         if self.gpu.role == Role.DEDICATED:
             self.cluster.enter_grace(self.instance)
-        return self.cluster.reclaim_on_completion(self.gpu, inflight, self.instance.max_batch, kv_used_bytes)
+        used = self.kv_used_bytes() if kv_used_bytes is None else kv_used_bytes
+        return self.cluster.reclaim_on_completion(self.gpu, inflight, self.instance.max_batch, used)
 
     def release(self) -> None:
         """End of grace (cluster.py:367-387): KV pages back to free, slots kept."""
@@ -240,13 +343,18 @@ class UniversalWorker:
         self.open_seqs.discard(seq)
 
     # ------------------------------------------------------------ compute
-    def prefill(self, seq: int, tokens_dev: torch.Tensor, pos0: int = 0, stream_from: int | None = None):
-        """Prefill on the paged pool; returns (logits view [vocab], next-token device scalar)."""
+    def prefill(self, seq: int, tokens_dev: torch.Tensor, pos0: int = 0, stream_from: int | None = None,
+                streamer=None):
+        """Prefill on the paged pool; returns (logits view [vocab], next-token device scalar).
+        ``stream_from``: layer l >= stream_from waits for range l - stream_from
+        of ``streamer`` (default: the worker's activation streamer)."""
         e = self.models[self.active_model]
         rows = tokens_dev.numel()
         if rows > self.max_tokens:  # the workspace is sized for max_tokens rows
             raise ValueError(f"prefill of {rows} tokens exceeds this worker's max_tokens={self.max_tokens}")
-        st = self.streamer if stream_from is not None else None
+        st = (streamer or self.streamer) if stream_from is not None else None
+        if st is None:
+            self._fence_loader(e.cfg.name)
         caller = torch.cuda.current_stream(self.dev)
         if caller != self.compute:
             self.compute.wait_stream(caller)  # inputs produced on the caller's stream
@@ -263,6 +371,8 @@ class UniversalWorker:
         n = seqs_dev.numel()
         if n > self.max_tokens:
             raise ValueError(f"decode batch {n} exceeds this worker's max_tokens={self.max_tokens}")
+        if not torch.cuda.is_current_stream_capturing():  # decode_graphed fences before capturing
+            self._fence_loader(e.cfg.name)
         caller = torch.cuda.current_stream(self.dev)
         if caller != self.compute:
             self.compute.wait_stream(caller)
@@ -333,11 +443,27 @@ class UniversalWorker:
         ev1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ev0.record(self.compute)
+        self.residency(name)
         inst, evicted, sw_ms, sw_kernel_ms = self.switch_memory(name)
         slot = self.slot(name)
         k = slot.layers_loaded
         stream_from = None
+        streamer = None
         streamed = 0
+        ld = self._loaders.get(slot.slot_id)
+        if ld is not None and ld.n_ranges and ld.full:
+            # The slot's background prewarm is still landing: prefill rides it,
+            # layer l waiting for that prewarm's range l + 1 (range 0 is the
+            # embedding) — no second copy of anything.
+            N.call("ws_streamer_wait", ld.streamer, 0, C.c_void_p(self.compute.cuda_stream))
+            streamer, stream_from = ld.streamer, -1
+            streamed = int(e.layout.total - e.layout.prefix_bytes(k))
+            k = L
+        elif ld is not None and ld.n_ranges:
+            # a prefix-only prewarm still landing: wait for its last range, stream the rest
+            N.call("ws_streamer_wait", ld.streamer, ld.n_ranges - 1, C.c_void_p(self.compute.cuda_stream))
+            k = ld.k
+            ld.n_ranges = 0
         if k < L and source is None and e.packed is not None:
             rows = e.packed.rows(k)
             flat = (C.c_int64 * (6 * len(rows)))(*[v for r in rows for v in r])
@@ -361,7 +487,7 @@ class UniversalWorker:
         seq = self.open_seq(rows + 1)
         with torch.cuda.stream(self.compute):
             toks = prompt_host.to(self.dev, non_blocking=True)
-        _, nt = self.prefill(seq, toks, 0, stream_from)
+        _, nt = self.prefill(seq, toks, 0, stream_from, streamer)
         with torch.cuda.stream(self.compute):
             out = torch.empty(1, dtype=torch.int32, pin_memory=True)
             out.copy_(nt, non_blocking=True)
@@ -369,7 +495,9 @@ class UniversalWorker:
         ev1.synchronize()
         ttft = (time.perf_counter() - t0) * 1e3
         stream_ms = 0.0
-        if stream_from is not None:
+        if ld is not None and ld.n_ranges:
+            ld.n_ranges = 0  # every range landed before the prefill finished
+        if stream_from is not None and streamer is None:
             times = (C.c_float * (L - k + 1))()
             N.call("ws_streamer_times", self.streamer, times, L - k + 1)
             stream_ms = times[L - k]
@@ -390,3 +518,6 @@ class UniversalWorker:
         if self.streamer:
             N.fns["ws_streamer_destroy"](self.streamer)
             self.streamer = None
+        for ld in self._loaders.values():
+            N.fns["ws_streamer_destroy"](ld.streamer)
+        self._loaders.clear()

@@ -23,7 +23,7 @@ def run_smoke() -> None:
     host = pinned_host_copy(flat)
     w.register(cfg, host)
     w.set_packed(cfg.name, pack_stream(cfg, flat))
-    w.prewarm(cfg.name, layers=1)
+    w.prewarm(cfg.name, layers=1, full=False)  # embedding + layer 0 resident: layer 1 + head stream
     prompt = torch.randint(0, cfg.vocab, (512,), generator=torch.Generator().manual_seed(0),
                            dtype=torch.int32).pin_memory()
     res = w.activate_instance(cfg.name, prompt)

@@ -79,7 +79,7 @@ def llama8b(cuda_device):
     torch.cuda.empty_cache()
     w = UniversalWorker(0, pool_pages=8192, max_tokens=S)
     w.register(cfg, host)
-    w.prewarm(cfg.name, layers=4)
+    w.prewarm(cfg.name, layers=4, full=False)
     yield cfg, w, host, packed
     w.release()
     w.close()
@@ -148,7 +148,7 @@ def test_llama3_8b_full_width_depth_within_2e2(cuda_device, layers):
     w = UniversalWorker(0, pool_pages=-(-cfg.layout().total // M.PAGE) + 160, max_tokens=S)
     try:
         w.register(cfg, host)
-        w.prewarm(cfg.name, layers=1)
+        w.prewarm(cfg.name, layers=1, full=False)
         rows = []
         for seed in (3, 4):
             prompt = _prompt(cfg.vocab, seed).pin_memory()
@@ -184,7 +184,7 @@ def test_full_width_families_two_layers_match_oracle(cuda_device, name):
     w = UniversalWorker(0, pool_pages=pages + -(-(S + 8) // tpb) + 16, max_tokens=S)
     try:
         w.register(cfg, host)
-        w.prewarm(cfg.name, layers=1)
+        w.prewarm(cfg.name, layers=1, full=False)
         prompt = _prompt(cfg.vocab, 21).pin_memory()
         res = w.activate_instance(cfg.name, prompt, keep_seq=True)
         assert res.streamed_layers == 1

@@ -132,7 +132,7 @@ def _prompt(cfg, seed, n=512):
 
 def test_tiny_cold_then_warm_prefill_matches_oracle(tiny):
     cfg, w, weights = tiny
-    w.prewarm(cfg.name, layers=1)  # embedding + layer 0 resident (BASELINE config 1)
+    w.prewarm(cfg.name, layers=1, full=False)  # embedding + layer 0 resident (BASELINE config 1)
     assert w.slot(cfg.name).layers_loaded == 1
     prompt = _prompt(cfg, 0).pin_memory()
     cold = w.activate_instance(cfg.name, prompt)
