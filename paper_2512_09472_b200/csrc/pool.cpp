@@ -202,7 +202,7 @@ int device_switch(ws_pool* p, const ws::SwitchRules& rules, const std::vector<in
   WS_CUDA(cudaGetLastError());
   WS_CUDA(cudaEventRecord(p->sw_stop, stream));
   p->sw_recorded = true;
-  p->sw_entries = (int64_t)n_set + (int64_t)migs.size() + (rules.n ? p->n : 0);
+  p->sw_entries = (int64_t)n_set + (int64_t)migs.size() + (rules.n ? (rules.hi ? rules.hi : p->n) - rules.lo : 0);
   return WS_OK;
 }
 
@@ -379,22 +379,28 @@ int place_slot(const ws_pool* p, int64_t n, uint64_t key, Slot& s) {
 }
 
 // Remove n KV pages (highest ids), relocating live blocks. Host ledger first,
-// then one switch launch.
+// then one switch launch. The victims are exactly the KV pages with id >=
+// the lowest victim, so the device applies them as one ranged rule (KV ->
+// free on [lowest, n)) instead of an uploaded page list.
 int kv_shrink(ws_pool* p, int64_t n, cudaStream_t stream) {
   if (n <= 0) return WS_OK;
   if (n > p->n_kv) WS_FAIL(WS_ERR_INVALID, "shrink %lld > kv %lld", (long long)n, (long long)p->n_kv);
-  std::vector<int32_t> victims;
-  victims.reserve(n);
-  for (int64_t q = p->n - 1; q >= 0 && (int64_t)victims.size() < n; --q)
-    if (p->owner[q] == kOwnerKV) victims.push_back((int32_t)q);
-  int32_t lowest_victim = victims.back();
+  int32_t* own = p->owner.data();
+  int64_t lowest = p->n, seen = 0;
+  std::vector<int32_t> live;  // victims holding a live block, descending
+  while (seen < n) {
+    --lowest;
+    if (own[lowest] == kOwnerKV) {
+      ++seen;
+      if (p->kv_seq[lowest] >= 0) live.push_back((int32_t)lowest);
+    }
+  }
   std::vector<ws::Migration> migs;
   int64_t cursor = 0;
-  for (auto it = victims.rbegin(); it != victims.rend(); ++it) {  // ascending page order
+  for (auto it = live.rbegin(); it != live.rend(); ++it) {  // ascending page order
     const int32_t v = *it;
-    if (p->kv_seq[v] < 0) continue;
-    while (cursor < lowest_victim && !(p->owner[cursor] == kOwnerKV && p->kv_seq[cursor] < 0)) ++cursor;
-    if (cursor >= lowest_victim)
+    while (cursor < lowest && !(own[cursor] == kOwnerKV && p->kv_seq[cursor] < 0)) ++cursor;
+    if (cursor >= lowest)
       WS_FAIL(WS_ERR_KV_BUSY, "KV shrink by %lld pages would drop live blocks", (long long)n);
     migs.push_back({v, (int32_t)cursor, p->kv_seq[v], p->kv_blk[v]});
     ++cursor;
@@ -404,15 +410,16 @@ int kv_shrink(ws_pool* p, int64_t n, cudaStream_t stream) {
     p->kv_blk[m.dst] = m.block;
     p->bt_host[(int64_t)m.seq * p->max_blocks + m.block] = m.dst;
   }
-  for (int32_t v : victims) {
-    p->owner[v] = kOwnerFree;
+  for (int32_t v : live) {
     p->kv_seq[v] = -1;
     p->kv_blk[v] = -1;
   }
+  for (int64_t q = lowest; q < p->n; ++q) own[q] = own[q] == kOwnerKV ? kOwnerFree : own[q];
   p->n_kv -= n;
   p->n_free += n;
-  ws::SwitchRules none{};
-  return device_switch(p, none, victims, kOwnerFree, migs, stream);
+  ws::SwitchRules r = one_rule(kOwnerKV, kOwnerFree);
+  r.lo = lowest;
+  return device_switch(p, r, {}, 0, migs, stream);
 }
 
 int kv_grow(ws_pool* p, int64_t n, cudaStream_t stream) {
@@ -672,8 +679,15 @@ int ws_slot_create_keyed(ws_pool* p, int64_t slot_id, int64_t pages, int32_t map
   p->n_free -= pages;
   p->n_slot += pages;
   Slot& ref = p->slots[slot_id] = std::move(s);
-  ws::SwitchRules none{};
-  if (int e = device_switch(p, none, ref.pages, (int32_t)slot_id, {}, 0)) return e;
+  if (ref.kind == kWindowed && pages) {  // a contiguous run: one ranged rule, no page list
+    ws::SwitchRules r = one_rule(kOwnerFree, (int32_t)slot_id);
+    r.lo = ref.pages[0];
+    r.hi = ref.pages[0] + pages;
+    if (int e = device_switch(p, r, {}, 0, {}, 0)) return e;
+  } else {
+    ws::SwitchRules none{};
+    if (int e = device_switch(p, none, ref.pages, (int32_t)slot_id, {}, 0)) return e;
+  }
   if (map_now)
     if (int e = map_range(p, ref, 0, pages)) return e;
   if (va_out) *va_out = p->on_device() ? reinterpret_cast<void*>(ref.base) : nullptr;

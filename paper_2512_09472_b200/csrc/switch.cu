@@ -23,7 +23,8 @@ __global__ void __launch_bounds__(kThreads) switch_kernel(SwitchArgs a, int n_ru
   const int cta = blockIdx.x;
   if (cta < n_rule_ctas) {
     if (a.rules.n == 0) return;
-    for (int64_t p = (int64_t)cta * kThreads + threadIdx.x; p < a.n_pages;
+    const int64_t hi = a.rules.hi ? a.rules.hi : a.n_pages;
+    for (int64_t p = a.rules.lo + (int64_t)cta * kThreads + threadIdx.x; p < hi;
          p += (int64_t)n_rule_ctas * kThreads) {
       int32_t o = a.owner[p];
 #pragma unroll
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(kThreads) switch_kernel(SwitchArgs a, int n_ru
 void launch_switch(const SwitchArgs& a, cudaStream_t stream) {
   int n_rule_ctas = 0;
   if (a.rules.n > 0) {
-    int64_t need = (a.n_pages + kThreads - 1) / kThreads;
+    int64_t need = ((a.rules.hi ? a.rules.hi : a.n_pages) - a.rules.lo + kThreads - 1) / kThreads;
     n_rule_ctas = (int)(need < 2 * kNumSMs ? need : 2 * kNumSMs);
   }
   int n_set_ctas = (a.n_set + kThreads - 1) / kThreads;

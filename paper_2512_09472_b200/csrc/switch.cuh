@@ -17,6 +17,7 @@ struct SwitchRules {
   int32_t n;
   int32_t from[kMaxRules];
   int32_t to[kMaxRules];
+  int64_t lo, hi;  // rules apply to pages [lo, hi) only (hi = 0: up to n_pages)
 };
 
 // Live KV block relocation: copy page src -> dst, then table[seq][block] = dst.

@@ -155,7 +155,7 @@ class UniversalWorker:
 
     # ------------------------------------------------------------ prewarm
     def prewarm(self, name: str, layers: int | None = None, source: torch.Tensor | None = None,
-                full: bool = True, wait: str | None = "ready") -> PrewarmSlot:
+                full: bool = True, wait: str | None = "ready", head: bool = False) -> PrewarmSlot:
         """prewarm(model, layers): take a slot (cluster.py:245-274) and start
         loading the model into it on the copy engine (engine.py:885-919).
 
@@ -166,8 +166,12 @@ class UniversalWorker:
         "full" at L (engine.py:658-686) — and the slot's ``layers_loaded`` /
         ``weight_bytes_loaded`` follow the per-layer copy events
         (``residency()``); ``full=False`` stops after k layers (a worker
-        prewarmed to exactly k, BASELINE configs[1]). ``wait``: "ready"
-        (return once k layers are resident), "full", or None (return at once).
+        prewarmed to exactly k, BASELINE configs[1]); ``head=True`` with it
+        also loads the final norm + lm_head (the reference's uniform
+        layer_bytes folds the embedding and head into every layer,
+        cluster.py:85-88 — with the head resident, a k-layer prefix holds about
+        the reference's k x layer_bytes). ``wait``: "ready" (return once k
+        layers are resident), "full", or None (return at once).
 
         One copy range per unit: the embedding, each decoder layer, then the
         final norm + lm_head; a windowed slot needs no driver call at all, a
@@ -187,6 +191,9 @@ class UniversalWorker:
         units = [(0, 0, lay.layers[0]["begin"])] + [(x["begin"], x["begin"], x["end"] - x["begin"]) for x in lay.layers]
         units.append((lay.final_norm, lay.final_norm, lay.total - lay.final_norm))
         n = len(units) if full else layers + 1
+        if not full and head:
+            units = units[:layers + 1] + units[-1:]
+            n += 1
         slot.layers_loaded = 0
         slot.weight_bytes_loaded = 0.0
         slot.load_start = time.perf_counter() * 1e3
@@ -203,6 +210,7 @@ class UniversalWorker:
         N.call("ws_streamer_start", ld.streamer, C.c_void_p(slot.va), C.c_void_p(src.data_ptr()), flat, n,
                C.c_void_p(self.copy.cuda_stream))
         ld.n_ranges, ld.full, ld.k = n, full, layers
+        slot.head_resident = full or head
         if wait == "ready":  # range k = embedding + layers [0, k); k = L: everything
             N.call("ws_streamer_sync", ld.streamer, layers if layers < L else n - 1)
         elif wait == "full":
@@ -234,9 +242,11 @@ class UniversalWorker:
         N.call("ws_streamer_progress", ld.streamer, C.byref(d))
         e = self.models[name]
         L = e.cfg.layers
-        got = max(0, min(d.value - 1, L))
+        got = max(0, min(d.value - 1, L if ld.full else ld.k))
         slot.layers_loaded = max(slot.layers_loaded, got)
-        slot.weight_bytes_loaded = float(e.layout.prefix_bytes(slot.layers_loaded)) if d.value else 0.0
+        head = e.layout.total - e.layout.final_norm if (not ld.full and slot.head_resident
+                                                        and d.value == ld.n_ranges) else 0
+        slot.weight_bytes_loaded = float(e.layout.prefix_bytes(slot.layers_loaded) + head) if d.value else 0.0
         if d.value == ld.n_ranges:  # every range landed: settle (engine.py:634-640)
             if ld.full:
                 slot.layers_loaded = L
@@ -262,14 +272,17 @@ class UniversalWorker:
             N.call("ws_streamer_sync", ld.streamer, ld.n_ranges - 1 if layers is None else min(layers, ld.n_ranges - 1))
         return self.residency(name)
 
-    def drop_suffix(self, name: str, layers: int) -> None:
-        """Forget residency of layers >= ``layers`` (bytes stay, ledger says
-        they are gone), so the next activation streams them again."""
+    def drop_suffix(self, name: str, layers: int, head: bool = False) -> None:
+        """Forget residency of layers >= ``layers`` (and of the final norm +
+        lm_head unless ``head``): bytes stay, the ledger says they are gone,
+        so the next activation streams them again."""
         self.wait_resident(name)
         s = self.slot(name)
         e = self.models[name]
         s.layers_loaded = layers
-        s.weight_bytes_loaded = float(e.layout.prefix_bytes(layers))
+        s.head_resident = head
+        s.weight_bytes_loaded = float(e.layout.prefix_bytes(layers)
+                                      + (e.layout.total - e.layout.final_norm if head else 0))
 
     # ------------------------------------------------------------ switch
     def switch_memory(self, name: str):
@@ -466,6 +479,8 @@ class UniversalWorker:
             ld.n_ranges = 0
         if k < L and source is None and e.packed is not None:
             rows = e.packed.rows(k)
+            if slot.head_resident:
+                rows = rows[:-1]  # final norm + lm_head already resident
             flat = (C.c_int64 * (6 * len(rows)))(*[v for r in rows for v in r])
             self.copy.wait_stream(self.compute)  # copy after the switch (pages owned)
             self.unpack.wait_stream(self.compute)
@@ -477,6 +492,8 @@ class UniversalWorker:
         elif k < L:
             src = source if source is not None else e.host
             ranges = e.layout.stream_ranges(k)
+            if slot.head_resident:
+                ranges = ranges[:-1]
             flat = (C.c_int64 * (3 * len(ranges)))(*[v for r in ranges for v in r])
             self.copy.wait_stream(self.compute)  # copy after the switch (pages owned)
             N.call("ws_streamer_start", self.streamer, C.c_void_p(slot.va), C.c_void_p(src.data_ptr()),
@@ -502,6 +519,7 @@ class UniversalWorker:
             N.call("ws_streamer_times", self.streamer, times, L - k + 1)
             stream_ms = times[L - k]
         slot.layers_loaded = L
+        slot.head_resident = True
         slot.weight_bytes_loaded = float(e.layout.total)
         inst.state = InstanceState.ACTIVE
         if not keep_seq:

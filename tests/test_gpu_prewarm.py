@@ -27,7 +27,8 @@ def _setup(names):
 
     base = M.TINY.with_(hidden=4096, heads=32, kv_heads=8, head_dim=128, ffn=14336, layers=6, vocab=8192)
     cfgs = [base.with_(name=n) for n in names]
-    w = UniversalWorker(0, pool_pages=len(cfgs) * 760 + 256, max_tokens=S)
+    pages = sum(-(-c.layout().total // M.PAGE) for c in cfgs)
+    w = UniversalWorker(0, pool_pages=pages + 256, max_tokens=S)
     hosts = {}
     for i, c in enumerate(cfgs):
         hosts[c.name] = pinned_host_copy(synth_flat(c, seed=40 + i, device="cuda"))
@@ -93,6 +94,30 @@ def test_activation_rides_inflight_prewarm_and_eviction_fences_copies(cuda_devic
         freed = w.reclaim(inflight=1)
         cap = w.gpu.kv_capacity_pages
         assert w.gpu.kv_pages_mapped * w.page_size >= used and freed > 0 and cap > 0
+        w.release()
+    finally:
+        w.close()
+
+
+def test_prefix_prewarm_with_head_streams_only_layers(cuda_device):
+    """prewarm(k, full=False, head=True): embedding, layers [0, k) and the
+    final norm + lm_head resident; a cold activation streams only layers
+    k..L-1 (no tail range) and matches a warm run bit for bit."""
+    w, (cfg,), hosts = _setup(["hd"])
+    try:
+        g = torch.Generator().manual_seed(5)
+        prompt = torch.randint(0, cfg.vocab, (S,), generator=g, dtype=torch.int32).pin_memory()
+        slot = w.prewarm(cfg.name, layers=2, full=False, head=True, wait="full")
+        lay = cfg.layout()
+        assert w.residency(cfg.name) == 2 and slot.head_resident
+        assert slot.weight_bytes_loaded == float(lay.prefix_bytes(2) + lay.total - lay.final_norm)
+        cold = w.activate_instance(cfg.name, prompt)
+        assert cold.streamed_layers == cfg.layers - 2
+        assert cold.streamed_bytes == lay.final_norm - lay.prefix_bytes(2)
+        l1 = w.logits[: cfg.vocab].clone()
+        w.release()
+        warm = w.activate_instance(cfg.name, prompt)
+        assert warm.streamed_bytes == 0 and torch.equal(w.logits[: cfg.vocab], l1)
         w.release()
     finally:
         w.close()
