@@ -364,11 +364,11 @@ def run_ours(args, rank, world, local_rank):
     prompts = [torch.randint(0, cfg.vocab, (S,), generator=gp, dtype=torch.int32).pin_memory()
                for _ in range(n_prompts)]
 
-    def leg(k_resident, source=None):
+    def leg(k_resident, source=None, head=False):
         out = []
         for i in range(Wm + n_prompts):
             if k_resident is not None:
-                w.drop_suffix(cfg.name, k_resident)
+                w.drop_suffix(cfg.name, k_resident, head=head)
             barrier()
             r = w.activate_instance(cfg.name, prompts[(i - Wm) % n_prompts] if i >= Wm else prompt_pinned,
                                     source=source)
@@ -409,6 +409,15 @@ def run_ours(args, rank, world, local_rank):
     w.set_packed(cfg.name, packed)
     cold_kreq_packed = leg(k_req_packed)
     w.models[cfg.name].packed = None
+    # the same policy at the reference's BYTE budget: its uniform layer_bytes
+    # (cluster.py:85-88) folds the embedding and lm_head into every layer, so
+    # k prewarmed layers are k x partition/L bytes; spent as embedding +
+    # lm_head + as many whole layers as fit, the stream is layers only
+    lay = entry.layout
+    budget = k_req * spec.partition_bytes / cfg.layers
+    head_b = lay.total - lay.final_norm
+    m_budget = max(m for m in range(cfg.layers + 1) if m == 0 or lay.prefix_bytes(m) + head_b <= budget)
+    cold_budget = leg(m_budget, head=True)
 
     # ---- value: warm prefill throughput, prompt + weights resident in HBM
     w.switch_memory(cfg.name)
@@ -610,7 +619,8 @@ def run_ours(args, rank, world, local_rank):
                 "slot_map_us_per_page": map_pp.value * 1e3, "reference_mu_us_per_page": 39.0,
                 "slot_placement": ["windowed", "composite", "scattered"][_placement(w, slot)],
                 "prewarm_ms": getattr(slot, "prewarm_ms", None),
-                "note": "2 MiB ledger pages backed by 32 MiB physical handles mapped once into the page window; "
+                "handle_mib": _handle_pages(w) * 2,
+                "note": "2 MiB ledger pages backed by large physical handles mapped once into the page window; "
                         "a windowed slot is a window range (no driver call to map, evict or re-prewarm); "
                         "reference mu = config.py:38"},
         # last key: the driver's stdout tail keeps the end of the line
@@ -645,7 +655,13 @@ def run_ours(args, rank, world, local_rank):
                     "cold_k_required_packed_over_warm_p50":
                         pct([r.ttft_ms for r in cold_kreq_packed], 50) / pct(warm_ttft, 50),
                     "k_required_note": "k = required_prewarm_layers (cluster.py:145-166) at the measured PCIe "
-                                       "stream bandwidth (plain / packed) and the measured per-token prefill cost"},
+                                       "stream bandwidth (plain / packed) and the measured per-token prefill cost",
+                    "k_required_byte_budget_gb": budget / 1e9,
+                    "byte_budget_resident": f"embedding + lm_head + layers [0, {m_budget})",
+                    "cold_byte_budget_p50": pct([r.ttft_ms for r in cold_budget], 50),
+                    "cold_byte_budget_p99": pct([r.ttft_ms for r in cold_budget], 99),
+                    "cold_byte_budget_over_warm_p50": pct([r.ttft_ms for r in cold_budget], 50) / pct(warm_ttft, 50),
+                    "cold_byte_budget_streamed_bytes": cold_budget[0].streamed_bytes},
 
     }
     if rank == 0:
@@ -662,6 +678,16 @@ def _placement(w, slot):
     kind, nh = C.c_int32(), C.c_int64()
     N.call("ws_slot_placement", w.gpu.pool, slot.slot_id, C.byref(kind), C.byref(nh))
     return kind.value
+
+
+def _handle_pages(w):
+    import ctypes as C
+
+    from paper_2512_09472_b200 import _native as N
+
+    v = C.c_int64()
+    N.call("ws_pool_handle_pages", w.gpu.pool, C.byref(v))
+    return v.value
 
 
 def _cpu_model():
