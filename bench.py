@@ -431,6 +431,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         launches0 = N.kernel_launches()
+        fallbacks0 = N.fallback_counts()
         ev0.record(w.compute)
         for _ in range(K):
             s = w.open_seq(S)
@@ -439,6 +440,7 @@ def run_ours(args, rank, world, local_rank):
         ev1.record(w.compute)
         torch.cuda.synchronize()
         launches = N.kernel_launches() - launches0
+        fallbacks = {k: v - fallbacks0[k] for k, v in N.fallback_counts().items()}
     clk.__exit__(None, None, None)
     barrier()
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -614,6 +616,7 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "clocks": clk_sum,
         "gpu_launches": launches,
+        "legacy_fallbacks_in_timed_region": fallbacks,
         "setup_s": setup_s,
         "vmm": {"pool_init_ms": init_ms.value, "pool_pages": pool_pages,
                 "slot_map_us_per_page": map_pp.value * 1e3, "reference_mu_us_per_page": 39.0,

@@ -41,6 +41,11 @@ const char* ws_last_error(void);
 int ws_version(int* major, int* minor);
 /* Kernel launches issued by this library since load (evidence for gpu_launches). */
 int ws_kernel_launches(int64_t* out);
+/* Launches that fell back to a legacy kernel because the shape is outside the
+ * tcgen05 tilings, by kind: [0] GEMM on mma.sync, [1] GEMM on the CUDA-core
+ * GEMV, [2] prefill attention on mma.sync. Explicit A/B selections
+ * (ws_model_set_gemm) are not fallbacks and are not counted. */
+int ws_fallback_counts(int64_t* out, int32_t n);
 
 /* ======================================================================
  * Planning math — bit-exact float64 restatements of the reference's

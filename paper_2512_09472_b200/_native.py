@@ -74,6 +74,7 @@ class PoolCounts(C.Structure):
 SIGNATURES: dict[str, list] = {
     "ws_version": [P(C.c_int), P(C.c_int)],
     "ws_kernel_launches": [P(i64)],
+    "ws_fallback_counts": [P(i64), i32],
     "ws_required_prewarm_layers": [i64, i32, i32, f64, f64, f64, i32, P(i32)],
     "ws_catchup_stall_ms": [i64, i32, i32, f64, f64, i32, f64, i32, P(f64)],
     "ws_reservation_target": [f64, i32, i32, f64, P(f64)],
@@ -179,3 +180,10 @@ def declared_symbols() -> list[str]:
     for h in sorted(hdr.glob("*.h")):
         names += re.findall(r"^\s*(?:int|const char\*)\s+(ws_\w+)\s*\(", h.read_text(), re.M)
     return names
+
+
+def fallback_counts() -> dict:
+    """Legacy-kernel fallbacks since load (ws_fallback_counts)."""
+    out = (C.c_int64 * 3)()
+    call("ws_fallback_counts", out, 3)
+    return {"gemm_mma_sync": out[0], "gemm_gemv": out[1], "attn_prefill_mma_sync": out[2]}

@@ -38,4 +38,14 @@ constexpr int kNumSMs = 148;
 // Count of kernel launches issued by this library (ws_kernel_launches()).
 void count_launch(int n = 1);
 
+// Shapes outside the tcgen05 tilings run a legacy kernel; every such launch
+// is counted (ws_fallback_counts) and the first of each kind logged to stderr.
+enum FallbackKind {
+  kFallbackGemmMma = 0,   // GEMM on the mma.sync kernel (M >= 16, no tcgen05 tiling)
+  kFallbackGemv = 1,      // GEMM on the CUDA-core GEMV (M < 16, no skinny tcgen05 tiling)
+  kFallbackAttnMma = 2,   // prefill attention on the mma.sync kernel (head_dim / GQA outside attn_tc)
+  kFallbackKinds = 3
+};
+void count_fallback(FallbackKind k, const char* what);
+
 }  // namespace ws

@@ -2,6 +2,7 @@
 
 #include <cuda_runtime.h>
 #include <atomic>
+#include <cstdio>
 #include <mutex>
 #include <string>
 
@@ -35,6 +36,14 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static std::atomic<int64_t> g_fallbacks[kFallbackKinds];
+static std::atomic<bool> g_fallback_logged[kFallbackKinds];
+void count_fallback(FallbackKind k, const char* what) {
+  g_fallbacks[k].fetch_add(1, std::memory_order_relaxed);
+  if (!g_fallback_logged[k].exchange(true))  // first occurrence per kind goes to stderr
+    fprintf(stderr, "[warmserve] fallback (counted in ws_fallback_counts[%d]): %s\n", (int)k, what);
+}
 const char* last_error() { return g_err.c_str(); }
 
 const Driver* driver() {
@@ -59,6 +68,11 @@ const Driver* driver() {
 extern "C" const char* ws_last_error(void) { return ws::last_error(); }
 extern "C" int ws_kernel_launches(int64_t* out) {
   *out = ws::g_launches.load();
+  return WS_OK;
+}
+
+extern "C" int ws_fallback_counts(int64_t* out, int32_t n) {
+  for (int32_t i = 0; i < n && i < ws::kFallbackKinds; ++i) out[i] = ws::g_fallbacks[i].load();
   return WS_OK;
 }
 

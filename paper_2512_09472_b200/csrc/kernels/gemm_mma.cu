@@ -216,10 +216,13 @@ void launch_gemm(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
     e.bias = bias;
     if (launch_gemm_skinny(A, B, M, N, K, e, st)) return;
   }
-  if (M < 16)
+  if (M < 16) {
+    count_fallback(kFallbackGemv, "GEMM with < 16 rows outside the skinny tcgen05 tiling runs the CUDA-core GEMV");
     launch_gemv(A, B, M, N, K, epi, C, bias, st);
-  else if (!launch_gemm_tc(A, B, M, N, K, epi, C, bias, st))
-    launch_gemm_mma(A, B, M, N, K, epi, C, bias, st);  // shapes outside the tcgen05 tiling
+  } else if (!launch_gemm_tc(A, B, M, N, K, epi, C, bias, st)) {
+    count_fallback(kFallbackGemmMma, "GEMM shape outside the tcgen05 tiling runs the mma.sync kernel");
+    launch_gemm_mma(A, B, M, N, K, epi, C, bias, st);
+  }
 }
 
 void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,

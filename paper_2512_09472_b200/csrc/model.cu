@@ -399,9 +399,12 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     const int r0 = m->prune_last && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
     const bf16* q_rows = qkv + (int64_t)r0 * q;
     float* x_rows = x + (int64_t)r0 * d;
-    if ((m->gemm_impl & 2) ||
-        !launch_attn_prefill_tc(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st))
+    if (m->gemm_impl & 2) {
       launch_attn_prefill(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st);
+    } else if (!launch_attn_prefill_tc(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st)) {
+      count_fallback(kFallbackAttnMma, "prefill attention shape outside attn_tc (head_dim / GQA) runs mma.sync");
+      launch_attn_prefill(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st);
+    }
     if (int e = row_parallel(m, attn, W<bf16>(wts, Ly.wo), n, d, o, x_rows, partial, st)) return e;
     launch_rmsnorm(x_rows, W<bf16>(wts, Ly.ffn_norm), h, n, d, c.rms_eps, st);
     gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st);

@@ -28,6 +28,25 @@ from .devmem import view
 from .models import PAGE, ModelConfig, model_spec
 
 
+def _nvtx(fn):
+    """NVTX range per worker op (prewarm / switch_memory / activate_instance /
+    prefill / decode / reclaim / release), named ws.<op>: the op boundaries
+    show up on an nsys / ncu timeline next to the kernels they issue."""
+    import functools
+
+    name = "ws." + fn.__name__
+
+    @functools.wraps(fn)
+    def wrapped(*a, **k):
+        torch.cuda.nvtx.range_push(name)
+        try:
+            return fn(*a, **k)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    return wrapped
+
+
 @dataclass
 class ModelEntry:
     cfg: ModelConfig
@@ -154,6 +173,7 @@ class UniversalWorker:
         return view(self.slot(name).va, (e.layout.total // 2,), torch.bfloat16, self.device)
 
     # ------------------------------------------------------------ prewarm
+    @_nvtx
     def prewarm(self, name: str, layers: int | None = None, source: torch.Tensor | None = None,
                 full: bool = True, wait: str | None = "ready", head: bool = False) -> PrewarmSlot:
         """prewarm(model, layers): take a slot (cluster.py:245-274) and start
@@ -285,6 +305,7 @@ class UniversalWorker:
                                       + (e.layout.total - e.layout.final_norm if head else 0))
 
     # ------------------------------------------------------------ switch
+    @_nvtx
     def switch_memory(self, name: str):
         """Weight->KV memory switch (promote_to_dedicated, cluster.py:291-342):
         evict other slots (async VMM unmap), every free page becomes KV via the
@@ -317,6 +338,7 @@ class UniversalWorker:
         exactly the pages a shrink must keep)."""
         return self.gpu.counts().kv_pages_allocated * self.page_size
 
+    @_nvtx
     def reclaim(self, inflight: int, kv_used_bytes: float | None = None) -> int:
         """KV->weights switch on a draining worker (cluster.py:351-365).
         ``kv_used_bytes=None`` takes the pool's live blocks (kv_used_bytes())."""
@@ -325,6 +347,7 @@ class UniversalWorker:
         used = self.kv_used_bytes() if kv_used_bytes is None else kv_used_bytes
         return self.cluster.reclaim_on_completion(self.gpu, inflight, self.instance.max_batch, used)
 
+    @_nvtx
     def release(self) -> None:
         """End of grace (cluster.py:367-387): KV pages back to free, slots kept."""
         for s in list(self.open_seqs):
@@ -356,6 +379,7 @@ class UniversalWorker:
         self.open_seqs.discard(seq)
 
     # ------------------------------------------------------------ compute
+    @_nvtx
     def prefill(self, seq: int, tokens_dev: torch.Tensor, pos0: int = 0, stream_from: int | None = None,
                 streamer=None):
         """Prefill on the paged pool; returns (logits view [vocab], next-token device scalar).
@@ -379,6 +403,7 @@ class UniversalWorker:
             caller.wait_stream(self.compute)  # outputs visible to the caller's stream
         return self.logits[: e.cfg.vocab], self.next_tok[:1]
 
+    @_nvtx
     def decode(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor, max_ctx: int):
         e = self.models[self.active_model]
         n = seqs_dev.numel()
@@ -398,6 +423,7 @@ class UniversalWorker:
             caller.wait_stream(self.compute)
         return self.logits[: n * e.cfg.vocab].view(n, e.cfg.vocab), self.next_tok[:n]
 
+    @_nvtx
     def decode_graphed(self, seqs_dev: torch.Tensor, pos_dev: torch.Tensor, tokens_dev: torch.Tensor,
                        max_ctx: int, ctx_bucket: int = 256):
         """decode() replayed from a CUDA graph: the step's 8-11 kernels per layer
@@ -443,6 +469,7 @@ class UniversalWorker:
         return self.logits[: n * vocab].view(n, vocab), self.next_tok[:n]
 
     # ------------------------------------------------------------ activation
+    @_nvtx
     def activate_instance(self, name: str, prompt_host: torch.Tensor, source: torch.Tensor | None = None,
                           keep_seq: bool = False) -> ActivationResult:
         """Cold (or warm) start: switch memory, stream the non-resident layers

@@ -86,7 +86,10 @@ def llama8b(cuda_device):
 
 
 def test_llama3_8b_full_depth_cold_k4_plain_and_packed_match_oracle(llama8b):
+    from paper_2512_09472_b200 import _native as N
+
     cfg, w, host, packed = llama8b
+    fb0 = N.fallback_counts()
     results = []
     for seed in (7, 8):
         prompt = _prompt(cfg.vocab, seed).pin_memory()
@@ -126,6 +129,7 @@ def test_llama3_8b_full_depth_cold_k4_plain_and_packed_match_oracle(llama8b):
         print(f"\nseed {seed}: rel {rel:.2e} (bf16 floor {floor:.2e}), token gpu {cold.token} ref {int(top2.indices[0])} "
               f"(margin {results[-1]['ref_margin']:.3e}); TTFT cold {cold.ttft_ms:.1f} / packed "
               f"{coldp.ttft_ms:.1f} / warm {warm.ttft_ms:.1f} ms; oracle {oracle_s:.0f} s")
+    assert N.fallback_counts() == fb0, "the benchmarked path fell back to a legacy kernel"
     _report("r2_llama8b_full_parity.json", {"config": "llama3-8b, 32 layers, k=4, 2048 tokens", "rows": results})
     for r in results:
         assert r["rel"] <= 1.25 * r["bf16_floor_rel"], r
