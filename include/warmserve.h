@@ -171,6 +171,24 @@ int ws_slot_map_chunk(ws_pool* pool, int64_t slot_id, int64_t first, int64_t cou
 int ws_slot_evict(ws_pool* pool, int64_t slot_id, void* fence_stream);
 int ws_slot_info(ws_pool* pool, int64_t slot_id, int64_t* pages_out, int64_t* mapped_out, void** va_out);
 int ws_slot_pages(ws_pool* pool, int64_t slot_id, int32_t* ids_out, int64_t cap, int64_t* n_out);
+/* ---- peer-HBM weight source ----
+ * Export the physical handles covering a WINDOWED slot as POSIX fds (the
+ * pool's handles are created exportable when the system supports it): fds[i]
+ * and sizes[i] (bytes) for each handle, offset_out = the slot's byte offset in
+ * the first one. The fds belong to the caller (send them to the peer process,
+ * e.g. SCM_RIGHTS, then close). */
+int ws_pool_export_slot(ws_pool* pool, int64_t slot_id, int32_t* fds, int64_t* sizes, int64_t cap,
+                        int64_t* n_out, int64_t* offset_out);
+/* Import exported handles into this process and map them, read-only, for
+ * `device`: a device pointer to the peer's memory (over NVLink when the
+ * exporter is another GPU). The layer streamer copies from it
+ * (ws_streamer_start src_base). The caller still owns / closes the fds. */
+typedef struct ws_peer_map ws_peer_map;
+int ws_peer_map_import(int32_t device, const int32_t* fds, const int64_t* sizes, int64_t n, void** va_out,
+                       ws_peer_map** out);
+int ws_peer_map_release(ws_peer_map* map);
+int ws_device_can_access_peer(int32_t device, int32_t peer_device, int32_t* out);
+
 /* Placement of a slot: kind 0 windowed, 1 composite, 2 scattered (ledger-only
  * pools); handles_out = physical handles a composite slot maps. */
 int ws_slot_placement(ws_pool* pool, int64_t slot_id, int32_t* kind_out, int64_t* handles_out);

@@ -99,6 +99,10 @@ SIGNATURES: dict[str, list] = {
     "ws_slot_info": [vp, i64, P(i64), P(i64), P(vp)],
     "ws_slot_pages": [vp, i64, P(i32), i64, P(i64)],
     "ws_slot_placement": [vp, i64, P(i32), P(i64)],
+    "ws_pool_export_slot": [vp, i64, P(i32), P(i64), i64, P(i64), P(i64)],
+    "ws_peer_map_import": [i32, P(i32), P(i64), i64, P(vp), P(vp)],
+    "ws_peer_map_release": [vp],
+    "ws_device_can_access_peer": [i32, i32, P(i32)],
     "ws_kv_map_all": [vp, vp, P(i64)],
     "ws_kv_reclaim": [vp, i32, i32, f64, vp, P(i64)],
     "ws_kv_resize": [vp, i64, vp],

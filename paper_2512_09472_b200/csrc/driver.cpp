@@ -54,7 +54,9 @@ const Driver* driver() {
            load("cuMemUnmap", &g_drv.cuMemUnmap) && load("cuMemSetAccess", &g_drv.cuMemSetAccess) &&
            load("cuMemGetAllocationGranularity", &g_drv.cuMemGetAllocationGranularity) &&
            load("cuTensorMapEncodeTiled", &g_drv.cuTensorMapEncodeTiled) &&
-           load("cuGetErrorString", &g_drv.cuGetErrorString);
+           load("cuGetErrorString", &g_drv.cuGetErrorString) &&
+           load("cuMemExportToShareableHandle", &g_drv.cuMemExportToShareableHandle) &&
+           load("cuMemImportFromShareableHandle", &g_drv.cuMemImportFromShareableHandle);
   });
   if (!g_ok) {
     set_error(g_load_err);

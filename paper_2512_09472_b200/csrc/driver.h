@@ -22,6 +22,11 @@ struct Driver {
                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   CUresult (*cuGetErrorString)(CUresult, const char**);
+  // peer weight source: a pool's physical handles exported as POSIX fds and
+  // mapped by another process (another GPU over NVLink, or the same GPU)
+  CUresult (*cuMemExportToShareableHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                                           unsigned long long);
+  CUresult (*cuMemImportFromShareableHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
 };
 
 // Returns nullptr (and sets the last error) if the driver is unavailable.

@@ -126,6 +126,7 @@ struct ws_pool {
   const ws::Driver* drv = nullptr;
   std::vector<CUmemGenericAllocationHandle> handles;  // handle h backs pages [h*hpages, ...)
   int64_t hpages = 64;                                // ledger pages per physical handle
+  bool exportable = false;                            // handles carry a POSIX-fd shareable type
   CUdeviceptr window = 0;
   int32_t* owner_dev = nullptr;
   char* stage_host = nullptr;  // pinned staging for switch lists
@@ -488,10 +489,18 @@ int ws_pool_create_ex(int32_t device, int64_t total_pages, int64_t page_size, in
     }
     const int64_t H = p->n_handles();
     p->handles.reserve(H);
+    // Exportable handles (POSIX fd) so a peer process can map this pool's
+    // slots as its cold-start weight source; plain handles if unsupported.
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     for (int64_t h = 0; h < H; ++h) {
       const size_t bytes = (size_t)(p->handle_size(h) * page_size);
       CUmemGenericAllocationHandle hd;
       CUresult r = p->drv->cuMemCreate(&hd, bytes, &prop, 0);
+      if (r != CUDA_SUCCESS && h == 0 && prop.requestedHandleTypes != CU_MEM_HANDLE_TYPE_NONE) {
+        prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+        r = p->drv->cuMemCreate(&hd, bytes, &prop, 0);
+      }
+      p->exportable = prop.requestedHandleTypes == CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
       if (r == CUDA_SUCCESS) {
         p->handles.push_back(hd);
         r = p->drv->cuMemMap(p->window + h * handle_pages * page_size, bytes, 0, hd, 0);
@@ -955,6 +964,34 @@ int pool_kv_view(ws_pool* p, char** window, int64_t* page_size, int32_t** block_
   return WS_OK;
 }
 }  // namespace ws
+
+// ---------------------------------------------------------------- peer source
+// Export the physical handles that cover slot pages [0, pages) of a windowed
+// slot as POSIX fds (the caller passes them to the peer process, e.g. over a
+// Unix socket with SCM_RIGHTS, and closes its copies). `offset_out` is the
+// slot's byte offset inside the first exported handle.
+extern "C" int ws_pool_export_slot(ws_pool* p, int64_t slot_id, int32_t* fds, int64_t* sizes, int64_t cap,
+                                   int64_t* n_out, int64_t* offset_out) {
+  if (int e = check_pool(p)) return e;
+  if (!p->on_device()) WS_FAIL(WS_ERR_NO_DEVICE, "ledger-only pool");
+  if (!p->exportable) WS_FAIL(WS_ERR_STATE, "pool handles are not exportable on this system");
+  auto it = p->slots.find(slot_id);
+  if (it == p->slots.end()) WS_FAIL(WS_ERR_NO_SLOT, "no slot %lld", (long long)slot_id);
+  const Slot& s = it->second;
+  if (s.kind != kWindowed || s.pages.empty()) WS_FAIL(WS_ERR_STATE, "only windowed slots are exported");
+  const int64_t first = s.pages.front(), last = s.pages.back();
+  const int64_t h0 = first / p->hpages, h1 = last / p->hpages;
+  if (h1 - h0 + 1 > cap) WS_FAIL(WS_ERR_INVALID, "fd buffer too small (%lld handles)", (long long)(h1 - h0 + 1));
+  for (int64_t h = h0; h <= h1; ++h) {
+    int fd = -1;
+    DRV(p->drv->cuMemExportToShareableHandle(&fd, p->handles[h], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    fds[h - h0] = fd;
+    sizes[h - h0] = p->handle_size(h) * p->page;
+  }
+  *n_out = h1 - h0 + 1;
+  *offset_out = (first - h0 * p->hpages) * p->page;
+  return WS_OK;
+}
 
 extern "C" int ws_pool_map_stats(ws_pool* p, int64_t* remapped, int64_t* reused) {
   if (int e = check_pool(p)) return e;

@@ -476,6 +476,8 @@ class UniversalWorker:
         on the copy engine, prefill the prompt with per-layer waits, return
         the first token on the host. prompt_host: pinned int32 tokens."""
         e = self.models[name]
+        if source is not None and hasattr(source, "tensor"):  # a peer_source.PeerSource
+            source = source.tensor
         if not 1 <= prompt_host.numel() <= self.max_tokens:  # checked before any state changes
             raise ValueError(f"prompt of {prompt_host.numel()} tokens: need 1..max_tokens={self.max_tokens}")
         L = e.cfg.layers
