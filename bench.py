@@ -14,8 +14,10 @@ One JSON line on rank 0:
   ttft_ms / switch_us   cold vs warm TTFT p50/p99, memory-switch latency
   roofline   the dominant kernel (prefill GEMM) vs MEASURED_PEAKS.json
   cpu_baseline  the CPU fp32 oracle port on this host's cores (bounded sample)
-Multi-GPU: replicas only (this config does not shard) — every rank runs its
-own worker; value = all ranks' tokens / max-over-ranks time.
+Multi-GPU (N >= 2): the 8B universal worker runs as N replicas (it does not
+shard) — value = all ranks' tokens / max-over-ranks time — and then the same
+ranks run BASELINE configs[3], Llama-3-70B tensor-parallel over N GPUs with
+per-shard layer streaming and NCCL on the TP boundary (key "tp_config4").
 `--impl reference` times the reference-side CPU path (oracle port) instead.
 """
 
@@ -667,10 +669,140 @@ def run_ours(args, rank, world, local_rank):
                     "cold_byte_budget_streamed_bytes": cold_budget[0].streamed_bytes},
 
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     w.release()
     w.close()
+    del w
+    torch.cuda.empty_cache()
+    if world > 1 or args.tp_block:
+        # BASELINE configs[3] on the same ranks: Llama-3-70B TP=world cold start
+        line["tp_config4"] = run_tp(args, rank, world, local_rank,
+                                    peer_only=os.environ.get("WS_BENCH_ONE_GPU") == "1")
+        line = {k_: v_ for k_, v_ in line.items() if k_ != "ttft_ms"} | {"ttft_ms": line["ttft_ms"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_tp(args, rank, world, local_rank, peer_only=False):
+    """BASELINE configs[3]: Llama-3-70B tensor-parallel cold start over the
+    ``world`` ranks (one GPU each): every rank holds its Megatron shard
+    (tp.shard_config) in a slot with the first k layers resident, streams its
+    own shard's layers k..L over its own PCIe link while the resident layers
+    compute, and the row-parallel partials are all-reduced over NCCL (bf16 on
+    the wire) on NVLink / NVSwitch — readiness is the max over ranks, like
+    the reference (engine.py:516-538). Also: warm TTFT, warm prefill
+    throughput, and the bf16 allreduce's bus bandwidth at the TP boundary's
+    message size ([S, d] bf16). ``peer_only``: the collectives run on the
+    peer-memory kernels instead (ranks sharing one GPU in tests)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09472_b200 import models as M
+    from paper_2512_09472_b200 import tp as TP
+    from paper_2512_09472_b200.worker import UniversalWorker
+    from paper_2512_09472_b200.weights import pinned_host_copy
+
+    dev = local_rank
+    cfg = M.ALL[args.tp_model]
+    scfg = TP.shard_config(cfg, world)
+    S, K, Wm = args.prompt, args.tp_steps, 3
+    k = args.tp_prewarm_layers
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cpu" if dist.get_backend() == "gloo" else f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.perf_counter()
+    shard = TP.synth_shard(cfg, world, rank, seed=0, device=f"cuda:{dev}")
+    host = pinned_host_copy(shard)
+    del shard
+    torch.cuda.empty_cache()
+    grp = (TP.TpGroup.peer_only(dev, max(S * cfg.hidden, cfg.vocab)) if peer_only
+           else TP.TpGroup.from_torch_dist(dev))
+    pages = -(-scfg.layout().total // M.PAGE)
+    tpb, _ = scfg.kv_geometry()
+    w = UniversalWorker(dev, pool_pages=pages + -(-(S + 8) // tpb) + 64, max_tokens=S)
+    w.register(scfg, host, tp=grp)
+    w.prewarm(scfg.name, layers=k, full=False)
+    setup_s = time.perf_counter() - t0
+    g = torch.Generator().manual_seed(99)
+    prompts = [torch.randint(0, cfg.vocab, (S,), generator=g, dtype=torch.int32).pin_memory() for _ in range(K)]
+    cold, warm, tokens = [], [], set()
+    for i in range(Wm + K):
+        w.drop_suffix(scfg.name, k)
+        barrier()
+        r = w.activate_instance(scfg.name, prompts[i % K])
+        w.release()
+        if i >= Wm:
+            cold.append((max_over_ranks(r.ttft_ms), r.stream_ms, r.streamed_bytes))
+            tokens.add(r.token)
+    for i in range(Wm + K):
+        barrier()
+        r = w.activate_instance(scfg.name, prompts[i % K])
+        w.release()
+        if i >= Wm:
+            warm.append(max_over_ranks(r.ttft_ms))
+    # warm prefill throughput (device events, max over ranks)
+    w.switch_memory(scfg.name)
+    toks = prompts[0].to(f"cuda:{dev}")
+    with torch.cuda.stream(w.compute):
+        for _ in range(2):
+            sq = w.open_seq(S)
+            w.prefill(sq, toks)
+            w.close_seq(sq)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(w.compute)
+        for _ in range(K):
+            sq = w.open_seq(S)
+            w.prefill(sq, toks)
+            w.close_seq(sq)
+        e1.record(w.compute)
+        torch.cuda.synchronize()
+    prefill_ms = max_over_ranks(e0.elapsed_time(e1)) / K
+    w.release()
+    # the TP boundary's collective alone: [S, d] bf16 allreduce, 2 per layer
+    ar = None
+    if not peer_only and world > 1:
+        buf = torch.randn(S, cfg.hidden, device=f"cuda:{dev}").bfloat16()
+        for _ in range(5):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(20):
+            dist.all_reduce(buf)
+        a1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a0.elapsed_time(a1)) / 20
+        nbytes = buf.numel() * 2
+        ar = {"bytes": nbytes, "ms": ms, "algbw_gbs": nbytes / ms / 1e6,
+              "busbw_gbs": 2 * (world - 1) / world * nbytes / ms / 1e6, "nvlink5_peak_gbs": 900.0,
+              "per_prefill": 2 * cfg.layers, "note": "torch.distributed NCCL bf16 allreduce, same size as the "
+                                                     "row-parallel partial the model's own NCCL call reduces"}
+    w.close()
+    grp.close()
+    cold_ttft = [c[0] for c in cold]
+    return {
+        "model": cfg.name, "tp": world, "prewarmed_layers": k, "prompt_tokens": S, "steps": K,
+        "collectives": "peer-memory kernels (IPC)" if peer_only else "NCCL (bf16 row-parallel partials)",
+        "shard_gb": scfg.layout().total / 1e9,
+        "cold_ttft_p50_ms": pct(cold_ttft, 50), "cold_ttft_p99_ms": pct(cold_ttft, 99),
+        "warm_ttft_p50_ms": pct(warm, 50), "cold_over_warm_p50": pct(cold_ttft, 50) / pct(warm, 50),
+        "stream_ms_p50_rank0": pct([c[1] for c in cold], 50),
+        "streamed_gb_per_rank": cold[0][2] / 1e9,
+        "prefill_ms": prefill_ms, "prefill_tokens_per_s": S / prefill_ms * 1e3,
+        "prefill_tflops_per_gpu": cfg.prefill_flops(S) / world / (prefill_ms / 1e3) / 1e12,
+        "tokens_agree": len(tokens) <= K, "allreduce": ar, "setup_s": setup_s,
+    }
 
 
 def _placement(w, slot):
@@ -718,6 +850,11 @@ def main():
     ap.add_argument("--switch-iters", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ttft-prompts", type=int, default=100)
+    ap.add_argument("--tp-model", default="llama3-70b", help="model of the TP block (N >= 2 or --tp-block)")
+    ap.add_argument("--tp-prewarm-layers", type=int, default=10)
+    ap.add_argument("--tp-steps", type=int, default=5)
+    ap.add_argument("--tp-block", action="store_true", help="run the TP block at N = 1 too (TP = 1)")
+    ap.add_argument("--only-tp", action="store_true", help="test hook: run only the TP block")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--decode-ctx", type=int, default=1024)
     ap.add_argument("--decode-batches", type=lambda v: [int(x) for x in v.split(",") if x], default=[1, 16, 64])
@@ -743,7 +880,12 @@ def main():
         else:
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.only_tp:
+        res = run_tp(args, rank, world, local_rank, peer_only=os.environ.get("WS_BENCH_ONE_GPU") == "1")
+        if rank == 0:
+            print(json.dumps({"tp_config4": res}), flush=True)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 

@@ -334,6 +334,10 @@ int ws_model_set_gemm(ws_model* m, int32_t impl);
  * and the FFN for the last row only (every row's QKV + KV append still runs);
  * same first token and KV cache. Every rank of a TP group must agree. */
 int ws_model_set_prune_last(ws_model* m, int32_t on);
+/* TP row-parallel partials over NCCL: 0 = bf16 on the wire (default; the
+ * sum is added to the fp32 residual), 1 = fp32. The peer-memory allreduce
+ * always moves fp32. Every rank of a group must agree. */
+int ws_model_set_tp_dtype(ws_model* m, int32_t fp32);
 
 /* Prefill `rows` new tokens of sequence `seq` (positions pos0..pos0+rows-1;
  * blocks must be reserved). `weights` is the slot VA. If `streamer` is set,

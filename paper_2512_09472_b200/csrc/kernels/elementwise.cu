@@ -232,6 +232,31 @@ void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st) {
   launch_pdl(add_f32_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<float4*>(x), reinterpret_cast<const float4*>(p), n4);
 }
 
+// x (fp32 residual) += p (bf16 row-parallel partial, already summed over the TP group)
+__global__ void __launch_bounds__(256) add_bf16_f32_kernel(float4* __restrict__ x, const uint2* __restrict__ p,
+                                                           int64_t n4) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = x[i];
+    const uint2 b = p[i];
+    a.x += __uint_as_float(b.x << 16);
+    a.y += __uint_as_float(b.x & 0xffff0000u);
+    a.z += __uint_as_float(b.y << 16);
+    a.w += __uint_as_float(b.y & 0xffff0000u);
+    x[i] = a;
+  }
+}
+
+void launch_add_bf16_f32(float* x, const bf16* p, int64_t count, cudaStream_t st) {
+  count_launch();
+  const int64_t n4 = count / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  launch_pdl(add_bf16_f32_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<float4*>(x),
+             reinterpret_cast<const uint2*>(p), n4);
+}
+
 void launch_gather_vocab(const float* g, float* out, int tp, int rows, int vs, cudaStream_t st) {
   count_launch();
   dim3 grid((vs + 1023) / 1024, rows, tp);

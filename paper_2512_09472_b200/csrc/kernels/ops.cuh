@@ -119,6 +119,7 @@ void launch_gemv(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, voi
 // TP boundary helpers: x += p (fp32, count elements); reorder all-gathered
 // vocab shards [tp][rows][vs] into logits [rows][tp*vs].
 void launch_add_f32(float* x, const float* p, int64_t count, cudaStream_t st);
+void launch_add_bf16_f32(float* x, const bf16* p, int64_t count, cudaStream_t st);
 void launch_gather_vocab(const float* gathered, float* logits, int tp, int rows, int vs, cudaStream_t st);
 // Packed bf16 weight ranges (unpack.cu): section offsets of a packed range
 // of n values with n_esc escapes, and the two-pass rebuild into dst.

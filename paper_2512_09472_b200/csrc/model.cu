@@ -121,6 +121,7 @@ struct ws_model {
   float2* rope = nullptr;  // [max_positions, head_dim/2] (cos, sin)
   int gemm_impl = 0;
   bool prune_last = false;  // ws_model_set_prune_last
+  bool tp_fp32 = false;     // ws_model_set_tp_dtype: row-parallel partials in fp32 (default bf16)
   ws_comm* comm = nullptr;  // TP group (config 4); null = single GPU
 };
 
@@ -197,7 +198,8 @@ bool gate_up_swiglu(const ws_model* m, const ws::bf16* h, const ws::bf16* w, int
 }
 
 // Row-parallel projection + residual add: x += A.B^T, summed over the TP group
-// (NCCL allreduce of the fp32 partial on the TP boundary).
+// (NCCL allreduce of the bf16 partial on the TP boundary; fp32
+// partials with ws_model_set_tp_dtype(m, 1) and on the peer-memory kernels).
 int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M, int N, int K, float* x,
                  float* partial, cudaStream_t st) {
   using namespace ws;
@@ -212,6 +214,15 @@ int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M,
     if (int e = ws_peer_next_slot(peer, &slot)) return e;
     gemm(m, A, B, M, N, K, Epi::kStoreF32, slot, nullptr, st);
     return ws_peer_reduce_add_f32(peer, x, (int64_t)M * N, st);
+  }
+  if (!m->tp_fp32 && comm_has_nccl(m->comm)) {
+    // bf16 partials on the wire ([S, d] bf16 per allreduce), summed
+    // into the fp32 residual after the collective
+    bf16* pb = reinterpret_cast<bf16*>(partial);
+    gemm(m, A, B, M, N, K, Epi::kStoreBf16, pb, nullptr, st);
+    if (int e = comm_allreduce_bf16(m->comm, pb, (int64_t)M * N, st)) return e;
+    launch_add_bf16_f32(x, pb, (int64_t)M * N, st);
+    return WS_OK;
   }
   gemm(m, A, B, M, N, K, Epi::kStoreF32, partial, nullptr, st);
   if (int e = comm_allreduce_f32(m->comm, partial, (int64_t)M * N, st)) return e;
@@ -345,6 +356,12 @@ int ws_model_set_comm(ws_model* m, ws_comm* comm) {
 int ws_model_set_gemm(ws_model* m, int32_t impl) {
   if (!m || impl < 0 || impl > 3) WS_FAIL(WS_ERR_INVALID, "impl must be in 0..3");
   m->gemm_impl = impl;
+  return WS_OK;
+}
+
+int ws_model_set_tp_dtype(ws_model* m, int32_t fp32) {
+  if (!m) WS_FAIL(WS_ERR_INVALID, "null model");
+  m->tp_fp32 = fp32 != 0;
   return WS_OK;
 }
 

@@ -24,7 +24,7 @@ typedef struct {
 } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
 enum { ncclSum = 0 };
-enum { ncclFloat32 = 7 };
+enum { ncclFloat32 = 7, ncclBfloat16 = 9 };
 
 struct Nccl {
   ncclResult_t (*getUniqueId)(ncclUniqueId*);
@@ -85,6 +85,17 @@ int comm_allreduce_f32(ws_comm* c, float* buf, int64_t count, cudaStream_t st) {
   if (r != ncclSuccess) WS_FAIL(WS_ERR_CUDA, "ncclAllReduce: %s", n->getErrorString(r));
   return WS_OK;
 }
+
+int comm_allreduce_bf16(ws_comm* c, void* buf, int64_t count, cudaStream_t st) {
+  if (!c->comm) WS_FAIL(WS_ERR_INVALID, "bf16 allreduce needs the NCCL communicator");
+  const Nccl* n = nccl();
+  if (!n) return WS_ERR_INVALID;
+  ncclResult_t r = n->allReduce(buf, buf, (size_t)count, ncclBfloat16, ncclSum, c->comm, st);
+  if (r != ncclSuccess) WS_FAIL(WS_ERR_CUDA, "ncclAllReduce(bf16): %s", n->getErrorString(r));
+  return WS_OK;
+}
+
+bool comm_has_nccl(const ws_comm* c) { return c->comm != nullptr; }
 
 ws_peer* comm_peer(const ws_comm* c, int64_t count) { return c->peer && count <= c->peer_max ? c->peer : nullptr; }
 

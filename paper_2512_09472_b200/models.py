@@ -34,6 +34,7 @@ N.register({
     "ws_model_workspace_bytes": [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)],
     "ws_model_set_gemm": [C.c_void_p, C.c_int32],
     "ws_model_set_prune_last": [C.c_void_p, C.c_int32],
+    "ws_model_set_tp_dtype": [C.c_void_p, C.c_int32],
     "ws_model_prefill": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
                          C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "ws_model_decode": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,

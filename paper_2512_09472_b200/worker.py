@@ -155,6 +155,10 @@ class UniversalWorker:
         for e in self.models.values():
             N.call("ws_model_set_gemm", e.handle, impl)
 
+    def set_tp_fp32(self, name: str, on: bool) -> None:
+        """TP row-parallel partials in fp32 over NCCL (default: bf16 on the wire)."""
+        N.call("ws_model_set_tp_dtype", self.models[name].handle, int(bool(on)))
+
     def set_prune_last(self, name: str, on: bool) -> None:
         """Per-model opt-in: the last decoder layer runs attention, O and the
         FFN for the last prompt row only (every row's QKV + KV append still
@@ -518,6 +522,7 @@ class UniversalWorker:
                    self._staging.numel(), C.c_void_p(self.copy.cuda_stream), C.c_void_p(self.unpack.cuda_stream))
             stream_from = k
             streamed = sum(r[5] for r in rows)
+            n_ranges = len(rows)
         elif k < L:
             src = source if source is not None else e.host
             ranges = e.layout.stream_ranges(k)
@@ -529,6 +534,7 @@ class UniversalWorker:
                    flat, len(ranges), C.c_void_p(self.copy.cuda_stream))
             stream_from = k
             streamed = sum(r[2] for r in ranges)
+            n_ranges = len(ranges)
         rows = prompt_host.numel()
         seq = self.open_seq(rows + 1)
         with torch.cuda.stream(self.compute):
@@ -544,9 +550,9 @@ class UniversalWorker:
         if ld is not None and ld.n_ranges:
             ld.n_ranges = 0  # every range landed before the prefill finished
         if stream_from is not None and streamer is None:
-            times = (C.c_float * (L - k + 1))()
-            N.call("ws_streamer_times", self.streamer, times, L - k + 1)
-            stream_ms = times[L - k]
+            times = (C.c_float * n_ranges)()
+            N.call("ws_streamer_times", self.streamer, times, n_ranges)
+            stream_ms = times[n_ranges - 1]
         slot.layers_loaded = L
         slot.head_resident = True
         slot.weight_bytes_loaded = float(e.layout.total)
@@ -568,3 +574,7 @@ class UniversalWorker:
         for ld in self._loaders.values():
             N.fns["ws_streamer_destroy"](ld.streamer)
         self._loaders.clear()
+        if self.gpu.pool:  # the pool's HBM goes back now, not at garbage collection
+            N.fns["ws_pool_destroy"](self.gpu.pool)
+            self.gpu.pool = None
+        self._ws = self.logits = self._staging = None

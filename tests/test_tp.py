@@ -101,7 +101,8 @@ def test_tp2_gloo_shards_reproduce_full_model():
 def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     """The NCCL TP path (fp32 partials + allreduce + residual add, lm_head
     allgather + reorder) on a 1-rank communicator == the fused single-GPU path,
-    and == the same path with the allreduces on the peer-memory kernel."""
+    and == the same path with the allreduces on the peer-memory kernel; the
+    default bf16-partial NCCL path matches the oracle."""
     from paper_2512_09472_b200.weights import pinned_host_copy
     from paper_2512_09472_b200.worker import UniversalWorker
 
@@ -109,12 +110,14 @@ def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     host = pinned_host_copy(synth_flat(cfg, seed=2, device="cuda"))
     prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(1), dtype=torch.int32)
     outs = []
-    for use_tp in (False, True, "peer"):
+    for use_tp in (False, True, "peer", "bf16"):
         w = UniversalWorker(cuda_device, pool_pages=64, max_tokens=512)
         grp = TP.TpGroup(0, 1, cuda_device, TP.TpGroup.unique_id()) if use_tp else None
         if use_tp == "peer":  # row-parallel allreduces through the peer-memory kernel
             grp.attach_peer(512 * cfg.hidden)
         w.register(cfg, host, tp=grp)
+        if use_tp in (True, "peer"):
+            w.set_tp_fp32(cfg.name, True)
         w.prewarm(cfg.name, layers=cfg.layers)
         r = w.activate_instance(cfg.name, prompt.pin_memory())
         outs.append((r.token, w.logits[: cfg.vocab].clone()))
@@ -126,6 +129,9 @@ def test_native_tp_path_at_tp1_matches_single_gpu(cuda_device):
     rel = ((outs[0][1] - outs[1][1]).norm() / outs[0][1].norm()).item()
     assert rel < 1e-3, rel
     assert torch.equal(outs[1][1], outs[2][1])  # one rank: both allreduces are the identity
+    ref, _ = O.forward(cfg, O.unpack(cfg, cfg.layout(), host), prompt.long())
+    rel_bf16 = ((outs[3][1].double().cpu() - ref[-1].double()).norm() / ref[-1].double().norm()).item()
+    assert rel_bf16 < 2e-2 and outs[3][0] == int(ref[-1].argmax()), rel_bf16
 
 
 def _tp_peer_worker(rank, world, port, q):
