@@ -666,7 +666,9 @@ def run_ours(args, rank, world, local_rank):
                     "cold_byte_budget_p50": pct([r.ttft_ms for r in cold_budget], 50),
                     "cold_byte_budget_p99": pct([r.ttft_ms for r in cold_budget], 99),
                     "cold_byte_budget_over_warm_p50": pct([r.ttft_ms for r in cold_budget], 50) / pct(warm_ttft, 50),
-                    "cold_byte_budget_streamed_bytes": cold_budget[0].streamed_bytes},
+                    "cold_byte_budget_streamed_bytes": cold_budget[0].streamed_bytes,
+                    "cold_byte_budget_stream_ms_p50": pct([r.stream_ms for r in cold_budget], 50),
+                    "cold_byte_budget_device_ms_p50": pct([r.device_ms for r in cold_budget], 50)},
 
     }
     w.release()
@@ -723,8 +725,12 @@ def run_tp(args, rank, world, local_rank, peer_only=False):
     host = pinned_host_copy(shard)
     del shard
     torch.cuda.empty_cache()
-    grp = (TP.TpGroup.peer_only(dev, max(S * cfg.hidden, cfg.vocab)) if peer_only
-           else TP.TpGroup.from_torch_dist(dev))
+    if peer_only:
+        grp = TP.TpGroup.peer_only(dev, max(S * cfg.hidden, cfg.vocab))
+    elif world > 1:
+        grp = TP.TpGroup.from_torch_dist(dev)
+    else:
+        grp = TP.TpGroup(0, 1, dev, TP.TpGroup.unique_id())
     pages = -(-scfg.layout().total // M.PAGE)
     tpb, _ = scfg.kv_geometry()
     w = UniversalWorker(dev, pool_pages=pages + -(-(S + 8) // tpb) + 64, max_tokens=S)
@@ -733,7 +739,7 @@ def run_tp(args, rank, world, local_rank, peer_only=False):
     setup_s = time.perf_counter() - t0
     g = torch.Generator().manual_seed(99)
     prompts = [torch.randint(0, cfg.vocab, (S,), generator=g, dtype=torch.int32).pin_memory() for _ in range(K)]
-    cold, warm, tokens = [], [], set()
+    cold, warm, agree = [], [], True
     for i in range(Wm + K):
         w.drop_suffix(scfg.name, k)
         barrier()
@@ -741,7 +747,7 @@ def run_tp(args, rank, world, local_rank, peer_only=False):
         w.release()
         if i >= Wm:
             cold.append((max_over_ranks(r.ttft_ms), r.stream_ms, r.streamed_bytes))
-            tokens.add(r.token)
+            agree &= max_over_ranks(r.token) == -max_over_ranks(-r.token)  # every rank got the same token
     for i in range(Wm + K):
         barrier()
         r = w.activate_instance(scfg.name, prompts[i % K])
@@ -801,7 +807,7 @@ def run_tp(args, rank, world, local_rank, peer_only=False):
         "streamed_gb_per_rank": cold[0][2] / 1e9,
         "prefill_ms": prefill_ms, "prefill_tokens_per_s": S / prefill_ms * 1e3,
         "prefill_tflops_per_gpu": cfg.prefill_flops(S) / world / (prefill_ms / 1e3) / 1e12,
-        "tokens_agree": len(tokens) <= K, "allreduce": ar, "setup_s": setup_s,
+        "ranks_agree_on_tokens": agree, "allreduce": ar, "setup_s": setup_s,
     }
 
 
