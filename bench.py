@@ -675,11 +675,20 @@ def run_ours(args, rank, world, local_rank):
     w.close()
     del w
     torch.cuda.empty_cache()
+    if args.config3_switches > 0:
+        # BASELINE configs[2]: 4 models co-prewarmed, weight<->KV switch burst
+        # (tools/config3_switch_burst.py; its ledger-vs-oracle replay is
+        # tests/test_gpu_config3.py)
+        sys.path.insert(0, str(ROOT / "tools"))
+        from config3_switch_burst import run_burst
+
+        line["config3_switch_burst"] = run_burst(switches=args.config3_switches, device=dev)
+        torch.cuda.empty_cache()
     if world > 1 or args.tp_block:
         # BASELINE configs[3] on the same ranks: Llama-3-70B TP=world cold start
         line["tp_config4"] = run_tp(args, rank, world, local_rank,
                                     peer_only=os.environ.get("WS_BENCH_ONE_GPU") == "1")
-        line = {k_: v_ for k_, v_ in line.items() if k_ != "ttft_ms"} | {"ttft_ms": line["ttft_ms"]}
+    line = {k_: v_ for k_, v_ in line.items() if k_ != "ttft_ms"} | {"ttft_ms": line["ttft_ms"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -862,6 +871,8 @@ def main():
     ap.add_argument("--tp-block", action="store_true", help="run the TP block at N = 1 too (TP = 1)")
     ap.add_argument("--only-tp", action="store_true", help="test hook: run only the TP block")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config3-switches", type=int, default=1000,
+                    help="BASELINE configs[2] switch burst length (0: skip)")
     ap.add_argument("--decode-ctx", type=int, default=1024)
     ap.add_argument("--decode-batches", type=lambda v: [int(x) for x in v.split(",") if x], default=[1, 16, 64])
     args = ap.parse_args()
