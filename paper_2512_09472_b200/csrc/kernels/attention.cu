@@ -6,7 +6,10 @@
 // softmax in fp32 registers (exp2 with the log2e-folded scale).
 // Decode: split-K over the context, one CTA per (split, kv head, sequence),
 // the GQA group on the M side of mma.sync, then a combine kernel.
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "../common.h"
 #include "device.cuh"
@@ -14,6 +17,9 @@
 #include "pdl.cuh"
 
 namespace ws {
+
+bool kv_window_tmap(const KvGeom& kv, int hd, CUtensorMap* out);  // attn_tc.cu
+
 namespace {
 
 using namespace dev;
@@ -231,28 +237,65 @@ constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = 3;
 // 64-key splits.
 constexpr int kDecTargetCtas = kNumSMs;
 
-template <int HD>
+template <int HD, bool TMA>
 struct DecodeSmem {
-  static constexpr int kStride = HD + 8;  // padded rows: conflict-free ldmatrix
-  static constexpr int kTile = kDecKeys * kStride;
+  static constexpr int kStride = TMA ? HD : HD + 8;  // cp.async: padded rows (conflict-free ldmatrix)
+  static constexpr int kTile = kDecKeys * kStride;    // elements
   static constexpr int kWarp = kDecStages * 2 * kTile;  // K and V per stage
-  static constexpr int kBytes = kDecWarps * kWarp * 2;
+  static constexpr int kRing = kDecWarps * kWarp * 2;   // bytes
+  static constexpr int kBar = kRing;                    // TMA: [warp][stage] full barriers
+  static constexpr int kMerge = (kDecWarps * 16 + 16) * (HD + 2) * 4;  // warp merge + cluster partial
+  static constexpr int kUsed = TMA ? kRing + kDecWarps * kDecStages * 8 + 1024 : kRing;  // + 1 KB alignment
+  static constexpr int kBytes = kUsed > kMerge ? kUsed : kMerge;
 };
 
+__device__ __forceinline__ void dec_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nDEC_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DEC_DONE;\nbra DEC_WAIT;\nDEC_DONE:\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // partial layout per (seq, q head, part): o[HD] (unnormalised), m, l
-template <int HD>
+//
+// TMA (sm_100a): when a block holds whole 16-token runs (tpb % 16 == 0) a
+// tile's K (and V) is 16 consecutive rows of the page window's 2D tensor map
+// (rows of HD bf16, 64 x 16 boxes, 128B swizzle, shared with attn_tc): lane 0
+// of the warp issues HD/64 box loads per operand on the stage's mbarrier
+// (expect_tx), the warp waits on its parity — 2*HD/64 instructions per tile
+// instead of 2*16*HD/8 16-byte cp.async, and the swizzled rows need no padding
+// for conflict-free ldmatrix. Other geometries (70B: 6 tokens per block) keep
+// the cp.async row gather.
+template <int HD, bool TMA>
 __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
-    int n_splits, int split_keys, bf16* __restrict__ out, int in_cluster) {
+    int n_splits, int split_keys, bf16* __restrict__ out, int in_cluster,
+    const __grid_constant__ CUtensorMap kvmap) {
   pdl_trigger();
-  pdl_wait();
-  using S = DecodeSmem<HD>;
+  using S = DecodeSmem<HD, TMA>;
   constexpr int ST = S::kStride, CH = HD / 8;
   extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* sbase = smem_raw;
+  if constexpr (TMA) {  // SWIZZLE_128B destinations need 1 KB alignment
+    const uint32_t raw = smem_u32(smem_raw);
+    sbase = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  }
   const int split = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  bf16* sw = reinterpret_cast<bf16*>(smem_raw) + warp * S::kWarp;
+  bf16* sw = reinterpret_cast<bf16*>(sbase) + warp * S::kWarp;
+  const uint32_t bar0 = smem_u32(sbase + S::kBar) + warp * kDecStages * 8;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kDecWarps * kDecStages; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(sbase + S::kBar) + 8 * i));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  pdl_wait();
   const int G = heads / kv.kv_heads;
   const int len = pos[b] + 1;  // the new token's K/V is already appended
   const int k_lo = split * split_keys, k_hi = min(len, k_lo + split_keys);
@@ -266,7 +309,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
   // page of one of the warp's next 32 tiles (a coalesced block-table read per
   // 32 tiles, issued 32 tiles ahead), so no tile load waits on a block-table
   // lookup or a division by tpb.
-  const bool aligned = kv.tpb % kDecKeys == 0;
+  const bool aligned = TMA || kv.tpb % kDecKeys == 0;
   auto page_of = [&](int j) -> int32_t {
     return j < my_n ? bt[(k_lo + (warp + j * kDecWarps) * kDecKeys) / kv.tpb] : 0;
   };
@@ -275,6 +318,14 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     pg_cur = page_of(lane);
     pg_nxt = page_of(32 + lane);
   }
+  // byte offset of element (row, col) in a K or V tile
+  auto toff = [](int row, int col) -> int {
+    if constexpr (TMA)
+      return (col >> 6) * (kDecKeys * 128) + row * 128 + ((((col >> 3) & 7) ^ (row & 7)) << 4);
+    else
+      return (row * ST + col) * 2;
+  };
+  const int rows_pp = (int)(kv.page_size / (HD * 2));
   auto load = [&](int stage, int j) {
     bf16* tk = sw + stage * 2 * S::kTile;
     bf16* tv = tk + S::kTile;
@@ -286,15 +337,42 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
       }
       const int32_t page = __shfl_sync(0xffffffffu, pg_cur, j & 31);
       const int key0 = k_lo + t * kDecKeys, rows = k_hi - key0;
-      const bf16* tile = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) +
-                         (int64_t)(key0 % kv.tpb) * HD;
+      if constexpr (TMA) {
+        // rows past k_hi in the tile's page hold finite data (the pool is
+        // zeroed at creation and only ever holds bf16 weights / KV): their
+        // scores are masked, so P = 0 and they add nothing
+        if (lane == 0) {
+          const int y = page * rows_pp + (key0 % kv.tpb);
+          const uint32_t bar = bar0 + stage * 8, dk = smem_u32(tk), dv = smem_u32(tv);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // ldmatrix reads before the refill
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                       "r"(2 * kDecKeys * HD * 2)
+                       : "memory");
 #pragma unroll
-      for (int i = lane; i < kDecKeys * CH; i += 32) {
-        const int r = i / CH, c = i % CH;
-        cp_async16(tk + r * ST + c * 8, tile + k_plane + i * 8, r < rows);
-        cp_async16(tv + r * ST + c * 8, tile + v_plane + i * 8, r < rows);
+          for (int hh = 0; hh < HD / 64; ++hh) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+                ::"r"(dk + hh * kDecKeys * 128), "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(k_plane / HD))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+                ::"r"(dv + hh * kDecKeys * 128), "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(v_plane / HD))
+                : "memory");
+          }
+        }
+        (void)rows;
+        return;
+      } else {
+        const bf16* tile = reinterpret_cast<const bf16*>(kv.window + (int64_t)page * kv.page_size) +
+                           (int64_t)(key0 % kv.tpb) * HD;
+#pragma unroll
+        for (int i = lane; i < kDecKeys * CH; i += 32) {
+          const int r = i / CH, c = i % CH;
+          cp_async16(tk + r * ST + c * 8, tile + k_plane + i * 8, r < rows);
+          cp_async16(tv + r * ST + c * 8, tile + v_plane + i * 8, r < rows);
+        }
+        return;
       }
-      return;
     }
 #pragma unroll
     for (int i = lane; i < kDecKeys * CH; i += 32) {
@@ -312,7 +390,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
 #pragma unroll
   for (int s = 0; s < kDecStages - 1; ++s) {
     if (s < my_n) load(s, s);
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
   }
 
   // Q as the A operand: rows = the group's q heads (rows >= G are zero)
@@ -340,11 +418,15 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
   for (int it = 0; it < my_n; ++it) {
     const int nx = it + kDecStages - 1;
     if (nx < my_n) load(nx % kDecStages, nx);
-    cp_async_commit();
-    cp_async_wait<kDecStages - 1>();
-    __syncwarp();
-    const bf16* tk = sw + (it % kDecStages) * 2 * S::kTile;
-    const bf16* tv = tk + S::kTile;
+    if constexpr (TMA) {
+      dec_mbar_wait(bar0 + (it % kDecStages) * 8, (it / kDecStages) & 1);
+    } else {
+      cp_async_commit();
+      cp_async_wait<kDecStages - 1>();
+      __syncwarp();
+    }
+    const uint8_t* tk = reinterpret_cast<const uint8_t*>(sw + (it % kDecStages) * 2 * S::kTile);
+    const uint8_t* tv = tk + S::kTile * 2;
     float s[2][4];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -353,7 +435,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
       uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(b0, b1, b2, b3, tk + ((lane & 7) + ((lane >> 4) << 3)) * ST + kk * 16 + ((lane >> 3) & 1) * 8);
+      ldmatrix_x4(b0, b1, b2, b3, tk + toff((lane & 7) + ((lane >> 4) << 3), kk * 16 + ((lane >> 3) & 1) * 8));
       uint32_t bl[2] = {b0, b1}, bh[2] = {b2, b3};
       mma_bf16_16816(s[0], qf[kk], bl);
       mma_bf16_16816(s[1], qf[kk], bh);
@@ -405,14 +487,14 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
 #pragma unroll
     for (int d = 0; d < HD / 16; ++d) {
       uint32_t b0, b1, b2, b3;
-      ldmatrix_x4_trans(b0, b1, b2, b3, tv + ((lane & 7) + ((lane >> 3) & 1) * 8) * ST + d * 16 + (lane >> 4) * 8);
+      ldmatrix_x4_trans(b0, b1, b2, b3, tv + toff((lane & 7) + ((lane >> 3) & 1) * 8, d * 16 + (lane >> 4) * 8));
       uint32_t bl[2] = {b0, b1}, bh[2] = {b2, b3};
       mma_bf16_16816(o[2 * d], a, bl);
       mma_bf16_16816(o[2 * d + 1], a, bh);
     }
     __syncwarp();  // every lane is done with this stage before it is refilled
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
@@ -592,18 +674,18 @@ void launch_decode(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <int HD>
-void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
-                 const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
-                 cudaStream_t st) {
-  using S = DecodeSmem<HD>;
+template <int HD, bool TMA>
+void decode_launch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
+                   const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
+                   const CUtensorMap& map, cudaStream_t st) {
+  using S = DecodeSmem<HD, TMA>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+    cudaFuncSetAttribute(attn_decode_kernel<HD, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     attr = true;
   }
   static int max_cluster = -1;
-  if (max_cluster < 0) max_cluster = decode_cluster_limit(attn_decode_kernel<HD>, S::kBytes);
+  if (max_cluster < 0) max_cluster = decode_cluster_limit(attn_decode_kernel<HD, TMA>, S::kBytes);
   // enough (split, kv head, seq) units to fill the SMs; >= 64 keys per split
   const int units = n_seqs * kv.kv_heads;
   int n_splits = std::max(1, std::min({(kDecTargetCtas + units - 1) / units, (max_ctx + 63) / 64, kMaxSplits}));
@@ -614,13 +696,30 @@ void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const 
   const int in_cluster = n_splits > 1 && n_splits <= max_cluster;
   dim3 grid(n_splits, kv.kv_heads, n_seqs);
   count_launch();
-  launch_decode(attn_decode_kernel<HD>, grid, dim3(kDecWarps * 32), S::kBytes, in_cluster ? n_splits : 0, st, qkv,
-                kv, layer, seqs, ctx, heads, scale * 1.4426950408889634f, scratch, n_splits, split_keys, out,
-                in_cluster);
+  launch_decode(attn_decode_kernel<HD, TMA>, grid, dim3(kDecWarps * 32), S::kBytes, in_cluster ? n_splits : 0, st,
+                qkv, kv, layer, seqs, ctx, heads, scale * 1.4426950408889634f, scratch, n_splits, split_keys, out,
+                in_cluster, map);
   if (n_splits > 1 && !in_cluster) {
     count_launch();
     launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
   }
+}
+
+template <int HD>
+void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
+                 const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
+                 cudaStream_t st) {
+  // TMA tiles need whole 16-token runs per block and the window addressable
+  // as HD-wide rows; WS_DEC_TMA=0 forces the cp.async gather (A/B)
+  static const bool tma_env = !(std::getenv("WS_DEC_TMA") && std::getenv("WS_DEC_TMA")[0] == '0');
+  CUtensorMap map{};
+  if constexpr (HD % 64 == 0) {
+    if (tma_env && kv.tpb % kDecKeys == 0 && kv_window_tmap(kv, HD, &map)) {
+      decode_launch<HD, true>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st);
+      return;
+    }
+  }
+  decode_launch<HD, false>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st);
 }
 
 }  // namespace

@@ -993,6 +993,33 @@ void dispatch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, 
 
 }  // namespace
 
+// The page window as a TMA tensor (rows of hd bf16, 64 x 16 boxes, 128B
+// swizzle), cached per (window, extent, hd): shared with the decode kernel.
+bool kv_window_tmap(const KvGeom& kv, int hd, CUtensorMap* out) {
+  struct Entry {
+    const char* window;
+    int64_t pages;
+    int hd;
+    bool ok;
+    CUtensorMap map;
+  };
+  static Entry cache[4];
+  static int next = 0;
+  for (const Entry& e : cache)
+    if (e.window == kv.window && e.pages == kv.n_pages && e.hd == hd) {
+      *out = e.map;
+      return e.ok;
+    }
+  Entry& e = cache[next];
+  next = (next + 1) % 4;
+  e.window = kv.window;
+  e.pages = kv.n_pages;
+  e.hd = hd;
+  e.ok = hd % 64 == 0 && kv.page_size % (hd * 2) == 0 && window_map(&e.map, kv, hd);
+  *out = e.map;
+  return e.ok;
+}
+
 #ifdef WS_ATTN_TRACE
 extern "C" int ws_attn_trace(long long* out) {
   cudaDeviceSynchronize();

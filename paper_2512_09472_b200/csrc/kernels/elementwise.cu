@@ -1,6 +1,8 @@
 // HBM-bound per-token kernels: embedding gather, RMSNorm, SwiGLU, RoPE +
 // paged KV append, argmax. Each moves 16-byte vectors with one row (or one
 // token x head) per CTA/warp; grids cover all rows so every SM streams.
+#include <algorithm>
+
 #include "../common.h"
 #include "device.cuh"
 #include "ops.cuh"
@@ -149,51 +151,78 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(bf16* __restrict__ qkv,
 }
 
 // Row-wise argmax over fp32 logits (first index on ties, like torch.argmax).
-__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V,
-                                                      int32_t* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int r = blockIdx.x;
-  const float* row = logits + (int64_t)r * V;
-  float best = -INFINITY;
-  int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    float v = row[i];
-    if (v > best || (v == best && i < idx)) {
-      best = v;
-      idx = i;
-    }
-  }
+// A row is split over gridDim.x CTAs (a decode step's 128k-entry row on one
+// CTA took ~60 us); each CTA reduces its chunk to one 64-bit key =
+// (order-preserving float bits << 32) | ~index, so max(key) is the largest
+// logit at the smallest index; the last CTA of the row (arrival counter,
+// reset by that CTA, so CUDA-graph replays stay valid) reduces the keys.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)o << 32) | (uint32_t)(~(uint32_t)i);
+}
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long k) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    float ob = __shfl_xor_sync(0xffffffffu, best, o);
-    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-    if (ob > best || (ob == best && oi < idx)) {
-      best = ob;
-      idx = oi;
-    }
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, k, o);
+    k = x > k ? x : k;
   }
-  __shared__ float sb[32];
-  __shared__ int si[32];
-  if ((threadIdx.x & 31) == 0) {
-    sb[threadIdx.x >> 5] = best;
-    si[threadIdx.x >> 5] = idx;
-  }
+  __shared__ unsigned long long sk[32];
+  if ((threadIdx.x & 31) == 0) sk[threadIdx.x >> 5] = k;
   __syncthreads();
   if (threadIdx.x < 32) {
-    const int nw = blockDim.x / 32;
-    best = threadIdx.x < nw ? sb[threadIdx.x] : -INFINITY;
-    idx = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+    k = threadIdx.x < blockDim.x / 32 ? sk[threadIdx.x] : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      float ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (ob > best || (ob == best && oi < idx)) {
-        best = ob;
-        idx = oi;
-      }
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, k, o);
+      k = x > k ? x : k;
     }
-    if (threadIdx.x == 0) out[r] = idx;
+  }
+  return k;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) argmax_kernel(const float* __restrict__ logits, int V, int chunk,
+                                                     int32_t* __restrict__ out, unsigned long long* part,
+                                                     unsigned int* count) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.y, nb = gridDim.x, b = blockIdx.x;
+  const float* row = logits + (int64_t)r * V;
+  const int lo = b * chunk, hi = min(V, lo + chunk);
+  unsigned long long k = 0ull;
+  if ((V & 3) == 0) {  // rows 16-byte aligned, chunk a multiple of 4
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    for (int i = lo / 4 + threadIdx.x; i < hi / 4; i += blockDim.x) {
+      const float4 v = __ldcs(r4 + i);
+      unsigned long long x = argmax_key(v.x, 4 * i);
+      x = max(x, argmax_key(v.y, 4 * i + 1));
+      x = max(x, argmax_key(v.z, 4 * i + 2));
+      x = max(x, argmax_key(v.w, 4 * i + 3));
+      k = max(k, x);
+    }
+  } else {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) k = max(k, argmax_key(row[i], i));
+  }
+  k = block_max_u64(k);
+  if (nb == 1) {
+    if (threadIdx.x == 0) out[r] = (int32_t)~(uint32_t)k;
+    return;
+  }
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[(int64_t)r * nb + b] = k;
+    __threadfence();
+    last = atomicAdd(count + r, 1u) == (unsigned)nb - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  unsigned long long m = 0ull;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) m = max(m, __ldcg(part + (int64_t)r * nb + i));
+  m = block_max_u64(m);
+  if (threadIdx.x == 0) {
+    out[r] = (int32_t)~(uint32_t)m;
+    count[r] = 0u;  // ready for the next launch (graph replays included)
   }
 }
 
@@ -299,9 +328,16 @@ void launch_rope_kv(bf16* qkv, const float2* rope, const KvGeom& kv, int layer, 
   launch_pdl(rope_kv_kernel, dim3(blocks), dim3(256), 0, st, qkv, rope, kv, layer, rows, heads, seq, pos, seq0, pos0);
 }
 
-void launch_argmax(const float* logits, int M, int V, int32_t* out, float*, cudaStream_t st) {
+void launch_argmax(const float* logits, int M, int V, int32_t* out, void* scratch, cudaStream_t st) {
+  // enough CTAs to stream the logits from every SM: ~2 per SM over all rows,
+  // chunks of >= 2048 logits, at most kArgmaxMaxSplit per row
+  int nb = scratch ? std::min({kArgmaxMaxSplit, std::max(1, 2 * kNumSMs / M), (V + 2047) / 2048}) : 1;
+  const int chunk = ((V + nb - 1) / nb + 3) / 4 * 4;
+  nb = (V + chunk - 1) / chunk;
+  auto* part = static_cast<unsigned long long*>(scratch);
+  auto* count = reinterpret_cast<unsigned int*>(part + (int64_t)kArgmaxMaxRows * kArgmaxMaxSplit);
   count_launch();
-  launch_pdl(argmax_kernel, dim3(M), dim3(1024), 0, st, logits, V, out);
+  launch_pdl(argmax_kernel, dim3(nb, M), dim3(256), 0, st, logits, V, chunk, out, part, count);
 }
 
 }  // namespace ws

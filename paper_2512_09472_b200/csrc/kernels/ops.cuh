@@ -128,7 +128,11 @@ void packed_sections(int64_t n, int64_t n_esc, int64_t* codes_off, int64_t* idx_
 void launch_unpack_bf16(void* dst, const void* packed, int64_t n, int e_base, int64_t n_esc, cudaStream_t st);
 void huff_sections(int64_t n, int64_t* lut_off, int64_t* offs_off, int64_t* words_off);
 void launch_unpack_huff(void* dst, const void* packed, int64_t n, cudaStream_t st);
-// Logits (fp32) for M rows and their argmax.
-void launch_argmax(const float* logits, int M, int V, int32_t* out, float* scratch, cudaStream_t st);
+// Argmax of M rows of fp32 logits. scratch: argmax_scratch_bytes() of
+// device memory, ZEROED once at allocation (per-row arrival counters that the
+// kernel resets itself); null runs one CTA per row. M <= kArgmaxMaxRows.
+constexpr int kArgmaxMaxRows = 256, kArgmaxMaxSplit = 32;
+constexpr int64_t argmax_scratch_bytes() { return (int64_t)kArgmaxMaxRows * kArgmaxMaxSplit * 8 + kArgmaxMaxRows * 4; }
+void launch_argmax(const float* logits, int M, int V, int32_t* out, void* scratch, cudaStream_t st);
 
 }  // namespace ws

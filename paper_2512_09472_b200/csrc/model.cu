@@ -119,6 +119,7 @@ struct ws_model {
   Layout layout;
   int device = 0;
   float2* rope = nullptr;  // [max_positions, head_dim/2] (cos, sin)
+  void* argmax_scratch = nullptr;  // split-row argmax: per-row partial keys + arrival counters (zeroed)
   int gemm_impl = 0;
   bool prune_last = false;  // ws_model_set_prune_last
   bool tp_fp32 = false;     // ws_model_set_tp_dtype: row-parallel partials in fp32 (default bf16)
@@ -252,7 +253,7 @@ int lm_head(const ws_model* m, const ws::bf16* hl, const ws::bf16* W, int rows, 
     if (int e = comm_allgather_f32(m->comm, shard, gathered, (int64_t)rows * Vs, st)) return e;
     launch_gather_vocab(gathered, logits, comm_size(m->comm), rows, Vs, st);
   }
-  launch_argmax(logits, rows, c.vocab, next, nullptr, st);
+  launch_argmax(logits, rows, c.vocab, next, m->argmax_scratch, st);
   return WS_OK;
 }
 
@@ -324,7 +325,10 @@ int ws_model_create(const ws_model_config* cfg, int32_t device, ws_model** out) 
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaMalloc(&m->rope, tab.size() * sizeof(float2)) != cudaSuccess ||
       cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice) !=
-          cudaSuccess) {
+          cudaSuccess ||
+      cudaMalloc(&m->argmax_scratch, ws::argmax_scratch_bytes()) != cudaSuccess ||
+      cudaMemset(m->argmax_scratch, 0, ws::argmax_scratch_bytes()) != cudaSuccess) {
+    if (m->rope) cudaFree(m->rope);
     delete m;
     WS_FAIL(WS_ERR_CUDA, "RoPE table upload failed");
   }
@@ -335,6 +339,7 @@ int ws_model_create(const ws_model_config* cfg, int32_t device, ws_model** out) 
 int ws_model_destroy(ws_model* m) {
   if (!m) return WS_OK;
   if (m->rope) cudaFree(m->rope);
+  if (m->argmax_scratch) cudaFree(m->argmax_scratch);
   delete m;
   return WS_OK;
 }
