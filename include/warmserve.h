@@ -369,6 +369,15 @@ int ws_model_set_comm(ws_model* m, ws_comm* comm);
 int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
             void* C, const void* bias, int32_t impl, void* stream);
 
+/* Standalone prefill-attention entry for tests/bench: causal GQA attention of
+ * `rows` queries (positions pos0..pos0+rows-1) of sequence `seq` over its
+ * paged K/V of `layer` in the pool ([0, pos0+rows) must already be appended).
+ * qkv: bf16 [rows, (heads + 2 kv_heads) head_dim] (q columns used); out: bf16
+ * [rows, heads head_dim]. Geometry from the model's config. impl: 0 the
+ * tcgen05 kernels (dispatch as in prefill), 1 the legacy mma.sync kernel. */
+int ws_attn_prefill(ws_model* m, ws_pool* pool, int32_t layer, int32_t seq, const void* qkv, int32_t rows,
+                    int32_t pos0, void* out, int32_t impl, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

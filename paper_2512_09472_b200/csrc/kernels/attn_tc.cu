@@ -594,13 +594,29 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 // P_X (bf16) overwrites S_X in place and PV reads it from TMEM. The MMA warp
 // ping-pongs the tiles — PV_A(j), S_A(j+1), PV_B(j), S_B(j+1) — so the exp2
 // stream of one tile runs under the tensor work of the other.
-// Warps 0-3 softmax A, 4-7 softmax B (thread = query row), 8 TMEM alloc + MMA
-// issue, 9 K gather, 10 V gather, 11 Q loads.
+// Softmax warps first (tile A then B; thread = query row; with the column
+// split two warps per 32 rows, 64 key columns each), then one warp each for
+// TMEM alloc + MMA issue, the K gather, the V gather and the Q loads.
 namespace pair2 {
-constexpr int NSK = 3, NSV = 2;  // K tiles are needed a full softmax earlier than V tiles
-// 12 warps: 3 per SM sub-partition, so each thread may hold 168 registers
-// (the softmax row of S_j is 128 of them)
-constexpr int kThreads2 = 384;
+#ifndef WS_ATTN_POLY
+#define WS_ATTN_POLY 2
+#endif
+constexpr int kPolyPairs = WS_ATTN_POLY;
+#ifndef WS_ATTN_SPLIT
+#define WS_ATTN_SPLIT 0
+#endif
+// Column split (off by default; A/B variant): two softmax warps per (tile,
+// 32-row quarter), each over 64 of the 128 key columns — 16 softmax warps, 4
+// per SM sub-partition, row maxima exchanged through shared memory. Measured
+// 45.7 vs 45.0 us at 8B / 2048 tokens: the per-tile softmax drops from ~2200
+// to ~1850 clocks but the exchange and the busier MUFU pipe eat the gain
+// (prefill attention).
+constexpr int kHalves = WS_ATTN_SPLIT ? 2 : 1;
+constexpr int kCols = kKeys / kHalves;
+constexpr int kSoftWarps = 8 * kHalves;
+constexpr int kMmaWarp = kSoftWarps, kKWarp = kSoftWarps + 1, kVWarp = kSoftWarps + 2, kQWarp = kSoftWarps + 3;
+constexpr int kThreads2 = (kSoftWarps + 4) * 32;
+constexpr int NSK = kHalves == 2 ? 2 : 3, NSV = 2;  // K tiles are needed a full softmax earlier than V tiles
 template <int HD>
 struct Smem {
   static constexpr int kTile = kRows * HD * 2;
@@ -608,7 +624,8 @@ struct Smem {
   static constexpr int kK = kQ + 2 * kTile;         // NSK stages
   static constexpr int kV = kK + NSK * kTile;       // NSV stages
   static constexpr int kBar = kV + NSV * kTile;
-  static constexpr int kBytes = kBar + 256 + 1024;
+  static constexpr int kX = kBar + 256;             // column split: row max / row sum exchange
+  static constexpr int kBytes = kX + (kHalves == 2 ? (2 * 2 * 2 + 2 * 2) * kRows * 4 : 0) + 1024;
 };
 constexpr int kQFull = 0, kQEmpty = 2, kKFull = 4, kKEmpty = kKFull + NSK, kVFull = kKEmpty + NSK,
               kVEmpty = kVFull + NSV, kSFull = kVEmpty + NSV, kPFull = kSFull + 2, kPvDone = kPFull + 2,
@@ -667,9 +684,9 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(B(pair2::kSFull + x), 1);
-      mbar_init(B(pair2::kPFull + x), 128);
+      mbar_init(B(pair2::kPFull + x), 128 * kHalves);
       mbar_init(B(pair2::kPvDone + x), 1);
-      mbar_init(B(pair2::kOFree + x), 128);
+      mbar_init(B(pair2::kOFree + x), 128 * kHalves);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -677,7 +694,7 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
   for (int i = threadIdx.x; i < (NSK + NSV) * S::kTile / 16; i += pair2::kThreads2)
     reinterpret_cast<uint4*>(gbase + S::kK)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(B(pair2::kTmemSlot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
@@ -689,7 +706,7 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
   if (threadIdx.x == 0) TRACE(0, 0);  // CTA start (after the PDL wait)
 
   Item it;
-  if (warp == 11) {
+  if (warp == kQWarp) {
     // ===================== Q loads (one warp) =====================
     for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
       for (int x = 0; x < 2; ++x) {
@@ -704,9 +721,9 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         cp_async_arrive(B(pair2::kQFull + x));
       }
     }
-  } else if (warp == 9 || warp == 10) {
-    // ===================== K (warp 9) / V (warp 10) page gathers =====================
-    const bool is_v = warp == 10;
+  } else if (warp == kKWarp || warp == kVWarp) {
+    // ===================== K / V page gathers (one warp each) =====================
+    const bool is_v = warp == kVWarp;
     const int32_t* bt = kv.block_tables + (int64_t)seq * kv.max_blocks;
     const uint32_t ring = is_v ? S::kV : S::kK;
     const int full0 = is_v ? pair2::kVFull : pair2::kKFull, empty0 = is_v ? pair2::kVEmpty : pair2::kKEmpty;
@@ -741,7 +758,7 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
       constexpr uint32_t id_s = idesc(kKeys, false), id_pv = idesc(HD, true);
@@ -805,12 +822,21 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
-    // ===================== softmax (warps 0-3: tile A, 4-7: tile B) =====================
-    const int x = warp >> 2, qd = warp & 3;
+  } else if (warp < kSoftWarps) {
+    // ===================== softmax =====================
+    // warp = (tile x, column half hf, row quarter qd): thread = query row
+    // qd*32 + lane of tile x, over kCols of the 128 key columns. With the
+    // column split the two warps of a (tile, quarter) exchange their row
+    // maxima through shared memory (named barrier per pair, parity double-
+    // buffered slots) so they agree on the reference max and the rescale.
+    const int x = warp / (4 * kHalves), hf = (warp >> 2) % kHalves, qd = warp & 3;
     const int rl = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const uint32_t tS = tmem + lane_off + x * 128, tO = tmem + lane_off + 256 + x * HD;
+    const uint32_t tS = tmem + lane_off + x * 128, tO = tmem + lane_off + 256 + x * HD + hf * (HD / kHalves);
+    float* xmax = reinterpret_cast<float*>(gbase + S::kX);  // [parity][tile][half][row]
+    float* xsum = xmax + 2 * 2 * kHalves * kRows;          // [tile][half][row]
+    const uint32_t nb = 1 + x * 4 + qd;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(nb) : "memory"); };
     int g = 0;
     for (int r = 0; item_of(r, c, G, n_items, n_hp, n_qt, rows, pos0, it); ++r) {
       const int qpos = pos0 + it.q0 + rl;
@@ -819,30 +845,37 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         mbar_wait(B(pair2::kSFull + x), g & 1);
         if (threadIdx.x == 0 && r == 0) TRACE(2, j);
         fence_after();
-        const int key0 = j * kKeys;
-        const bool diag = key0 + kKeys - 1 > pos0 + it.q0 || key0 + kKeys > it.n_keys;
-        uint32_t v[kKeys];
-        TLD32(tS + 0, (v + 0));
-        TLD32(tS + 32, (v + 32));
-        TLD32(tS + 64, (v + 64));
-        TLD32(tS + 96, (v + 96));
+        const int key0 = j * kKeys + hf * kCols;  // this thread's first key column
+        const bool diag = j * kKeys + kKeys - 1 > pos0 + it.q0 || j * kKeys + kKeys > it.n_keys;
+        uint32_t v[kCols];
+#pragma unroll
+        for (int cc = 0; cc < kCols / 32; ++cc) TLD32(tS + hf * kCols + cc * 32, (v + cc * 32));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (threadIdx.x == 0 && r == 0) TRACE(4, j);
         if (diag) {
 #pragma unroll
-          for (int i = 0; i < kKeys; ++i)
+          for (int i = 0; i < kCols; ++i)
             if (key0 + i > qpos || key0 + i >= it.n_keys) v[i] = __float_as_uint(-INFINITY);
         }
         // row max over raw scores (scale > 0 commutes with max): 3-input max, 4 chains
         float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kKeys; i += 8) {
+        for (int i = 0; i < kCols; i += 8) {
           m0 = fmax3(m0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
           m1 = fmax3(m1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
           m2 = fmax3(m2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
           m3 = fmax3(m3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
         }
-        const float mx = fmax3(m0, m1, fmaxf(m2, m3)) * scale_log2;
+        float mraw = fmax3(m0, m1, fmaxf(m2, m3));
+        if constexpr (kHalves == 2) {
+          // both halves have loaded S_j (tcgen05.wait::ld above) once they meet
+          // here, so P may overwrite S_j's columns afterwards
+          float* slot = xmax + ((g & 1) * 2 + x) * 2 * kRows;
+          slot[hf * kRows + rl] = mraw;
+          pair_sync();
+          mraw = fmaxf(mraw, slot[(hf ^ 1) * kRows + rl]);
+        }
+        const float mx = mraw * scale_log2;
         float alpha = 1.f;
         if (mx > m_used + 8.f) {  // lazy rescale (exact: O/l share the reference max)
           alpha = m_used == -INFINITY ? 0.f : fast_exp2(m_used - mx);
@@ -850,17 +883,17 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         }
         const float mref = m_used == -INFINITY ? 0.f : m_used;
         if (threadIdx.x == 0 && r == 0) TRACE(5, j);
-        // p = exp2(s * scale - mref) two at a time (FFMA2); 3 of every 8 pairs on
-        // the FMA-pipe polynomial, the rest on MUFU; P packed in place as bf16x2
+        // p = exp2(s * scale - mref) two at a time (FFMA2); kPolyPairs of every 8
+        // pairs on the FMA-pipe polynomial, the rest on MUFU; P packed in place
         const uint64_t sc2 = pk2(scale_log2, scale_log2), nm2 = pk2(-mref, -mref);
         uint64_t s2[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) s2[i] = 0;
 #pragma unroll
-        for (int q = 0; q < kKeys / 2; ++q) {
+        for (int q = 0; q < kCols / 2; ++q) {
           const uint64_t x2 = ffma2(pk2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1])), sc2, nm2);
           uint64_t p2;
-          if ((q & 7) < 3) {
+          if ((q & 7) < kPolyPairs) {
             p2 = exp2_poly2(x2);
           } else {
             const float2 xf = up2(x2);
@@ -873,16 +906,18 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         const float2 sa = up2(fadd2(fadd2(s2[0], s2[1]), fadd2(s2[2], s2[3])));
         l = l * alpha + (sa.x + sa.y);
         if (threadIdx.x == 0 && r == 0) TRACE(6, j);
-        TST32(tS + 0, (v + 0));  // P_j overwrites S_j's first 64 columns (this thread's row)
-        TST32(tS + 32, (v + 32));
+        // P_j (bf16 pairs) overwrites the first half of S_j's columns: keys
+        // [hf*kCols, +kCols) -> packed columns [hf*kCols/2, +kCols/2)
+#pragma unroll
+        for (int cc = 0; cc < kCols / 64; ++cc) TST32(tS + hf * (kCols / 2) + cc * 32, (v + cc * 32));
         if (j > 0) {  // O_x holds P_0..P_{j-1} V once PV_x(j-1) retired
           mbar_wait(B(pair2::kPvDone + x), (g - 1) & 1);
           fence_after();
         }
         if (threadIdx.x == 0 && r == 0) TRACE(7, j);
-        if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {
+        if (__any_sync(0xffffffffu, alpha != 1.f) && j > 0) {  // this warp's O columns
 #pragma unroll 1
-          for (int cc = 0; cc < HD / 32; ++cc) {
+          for (int cc = 0; cc < HD / kHalves / 32; ++cc) {
             uint32_t o[32];
             TLD32(tO + cc * 32, o);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -896,21 +931,29 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
         mbar_arrive(B(pair2::kPFull + x));
         if (threadIdx.x == 0 && r == 0) TRACE(3, j);
       }
-      // epilogue: O_x / l -> bf16 rows of head h0 + x; O_x is released as soon as it is in registers
+      // epilogue: O_x / l -> bf16 rows of head h0 + x (this warp's columns);
+      // O_x is released as soon as it is in registers
+      float lt = l;
+      if constexpr (kHalves == 2) {
+        xsum[(x * 2 + hf) * kRows + rl] = l;
+        pair_sync();
+        lt += xsum[(x * 2 + (hf ^ 1)) * kRows + rl];
+      }
       mbar_wait(B(pair2::kPvDone + x), (g - 1) & 1);
       fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      uint32_t o[HD];
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      constexpr int OC = HD / kHalves;
+      uint32_t o[OC];
 #pragma unroll
-      for (int cc = 0; cc < HD / 32; ++cc) TLD32(tO + cc * 32, (o + cc * 32));
+      for (int cc = 0; cc < OC / 32; ++cc) TLD32(tO + cc * 32, (o + cc * 32));
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       fence_before();
       mbar_arrive(B(pair2::kOFree + x));
       const int grow = it.q0 + rl;
       if (grow < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + (it.h0 + x) * HD);
+        uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)grow * heads * HD + (it.h0 + x) * HD + hf * OC);
 #pragma unroll
-        for (int q = 0; q < HD / 8; ++q)
+        for (int q = 0; q < OC / 8; ++q)
           dst[q] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
                               pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
                               pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
@@ -927,7 +970,7 @@ __global__ void __launch_bounds__(pair2::kThreads2, 1)
     g_attn_cta[c][1] = attn_gtimer();
   }
 #endif
-  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
 // 2D view of the page window as rows of HD bf16 (one token of one K or V

@@ -536,6 +536,25 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   return WS_OK;
 }
 
+int ws_attn_prefill(ws_model* m, ws_pool* pool, int32_t layer, int32_t seq, const void* qkv, int32_t rows,
+                    int32_t pos0, void* out, int32_t impl, void* stream) {
+  using namespace ws;
+  if (!m || !pool || !qkv || !out || rows < 1 || pos0 < 0 || layer < 0 || layer >= m->cfg.layers)
+    WS_FAIL(WS_ERR_INVALID, "bad attention arguments");
+  KvGeom kv;
+  if (int e = kv_geom(m, pool, &kv)) return e;
+  if ((pos0 + rows + kv.tpb - 1) / kv.tpb > kv.max_blocks) WS_FAIL(WS_ERR_INVALID, "sequence too long");
+  const ws_model_config& c = m->cfg;
+  const float scale = 1.0f / std::sqrt((float)c.head_dim);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bf16* q = static_cast<const bf16*>(qkv);
+  bf16* o = static_cast<bf16*>(out);
+  if (impl == 1 || !launch_attn_prefill_tc(q, o, kv, layer, seq, rows, pos0, c.heads, scale, st))
+    launch_attn_prefill(q, o, kv, layer, seq, rows, pos0, c.heads, scale, st);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
 int ws_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epi, void* C,
             const void* bias, int32_t impl, void* stream) {
   using namespace ws;

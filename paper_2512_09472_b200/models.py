@@ -41,6 +41,8 @@ N.register({
                         C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "ws_gemm": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                 C.c_void_p, C.c_int32, C.c_void_p],
+    "ws_attn_prefill": [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                        C.c_void_p, C.c_int32, C.c_void_p],
     "ws_nccl_unique_id": [C.POINTER(C.c_uint8), C.c_int32],
     "ws_comm_create": [C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)],
     "ws_comm_destroy": [C.c_void_p],
