@@ -87,6 +87,7 @@ template <int MODE>
 __device__ __forceinline__ void store_out(const TcEpilogue& ep, const SkinnyArgs& a, int row, const float* v,
                                           int c0) {
   // v[j]: batch row c0 + j of output column `row`
+  if (row >= (MODE == (int)Epi::kSwiGLU ? a.N / 2 : a.N)) return;  // ragged last unit
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int b = c0 + j;
@@ -377,6 +378,7 @@ __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEp
     for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
   }
   const int row = unit * kRows + i;
+  if (row >= (MODE == (int)Epi::kSwiGLU ? args.N / 2 : args.N)) return;  // ragged last unit
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int b = q4 * 4 + k;
@@ -568,15 +570,21 @@ bool gemm_skinny_enabled() {
   return g_skinny_mode == 1;
 }
 
+// N need not be a multiple of the 128-row unit for the plain epilogues (a
+// vocabulary of 32064 rows: Phi-3's lm_head): the last unit's weight rows past
+// N are zero-filled by the TMA bounds and its outputs past N are not stored.
 bool gemm_skinny_supported(int M, int N, int K, Epi mode) {
-  return gemm_skinny_enabled() && M >= 1 && M <= 128 && K >= kBox && K % kBox == 0 &&
-         N % (kRows * (mode == Epi::kSwiGLU ? 2 : 1)) == 0;
+  const bool ragged_ok = mode == Epi::kStoreBf16 || mode == Epi::kBiasBf16 || mode == Epi::kStoreF32 ||
+                         mode == Epi::kAddF32;
+  return gemm_skinny_enabled() && M >= 1 && M <= 128 && K >= kBox && K % kBox == 0 && N >= 1 &&
+         (N % (kRows * (mode == Epi::kSwiGLU ? 2 : 1)) == 0 || ragged_ok);
 }
 
 bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const TcEpilogue& e, cudaStream_t st) {
   if (!gemm_skinny_supported(M, N, K, e.mode)) return false;
   if (e.mode == Epi::kRopeKV && e.kv.head_dim != 64 && e.kv.head_dim != 128) return false;  // heads tile 128 rows
   if (e.norm_role == 1 && e.mode != Epi::kAddF32) return false;
+  if (e.norm_role != 0 && N % kRows) return false;  // folded norms work on whole 32-column groups
   if (e.norm_role == 2 && (e.mode == Epi::kAddF32 || e.mode == Epi::kStoreF32)) return false;
   const int NB = e.mode == Epi::kSwiGLU ? 2 : 1;
   // Widest iteration (up to 4 boxes = 512 contiguous bytes of each weight row
@@ -587,7 +595,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   const int mp = (M + 15) / 16 * 16;
   int sub = 4;
   while (sub > 1 && (K % (sub * kBox) || 3 * sub * (NB * kW_BYTES + mp * kBox * 2) > kSmemBudget)) sub /= 2;
-  const int units = N / (kRows * NB), kbs = K / (kBox * sub);
+  const int units = (N + kRows * NB - 1) / (kRows * NB), kbs = K / (kBox * sub);
   SkinnyArgs a{};
   a.sub = sub;
   a.kbs = kbs;

@@ -80,16 +80,17 @@ def measured_config(cfg, measured: Measured, shapes: dict, reference_model: str 
 
 
 def run_measured(engine_module, cfg, requests, policy: str, measured: Measured, shapes: dict,
-                 reference_model: str = "llama3-8b"):
+                 reference_model: str = "llama3-8b", cluster_cls=None):
     """Replay `requests` through the reference engine on this framework's
-    Cluster with measured latencies; returns the engine's MetricsReport."""
+    Cluster (or ``cluster_cls``, a subclass of it) with measured latencies;
+    returns the engine's MetricsReport."""
     from . import cluster as ours
     from . import memswitch as ours_ms
 
     saved = {k: getattr(engine_module, k) for k in ("Cluster", "required_prewarm_layers", "catchup_stall_ms",
                                                     "pipelined_load", "background_kv_mapping")}
     try:
-        engine_module.Cluster = ours.Cluster
+        engine_module.Cluster = cluster_cls or ours.Cluster
         engine_module.required_prewarm_layers = ours.required_prewarm_layers
         engine_module.catchup_stall_ms = ours.catchup_stall_ms
         engine_module.pipelined_load = ours_ms.pipelined_load

@@ -296,6 +296,21 @@ class UniversalWorker:
             N.call("ws_streamer_sync", ld.streamer, ld.n_ranges - 1 if layers is None else min(layers, ld.n_ranges - 1))
         return self.residency(name)
 
+    @_nvtx
+    def evict(self, name: str):
+        """evict_slot (cluster.py:276-289) on this worker: copies still landing
+        in the slot are fenced on the compute stream first (its pages may
+        become another slot or KV next), then the pages return to the free
+        list and the VA is unmapped in the background."""
+        slot = self.slot(name)
+        if slot is None:
+            return None
+        ld = self._loaders.get(slot.slot_id)
+        if ld is not None and ld.n_ranges:
+            N.call("ws_streamer_wait", ld.streamer, ld.n_ranges - 1, C.c_void_p(self.compute.cuda_stream))
+            ld.n_ranges = 0
+        return self.cluster.evict_slot(self.gpu, name)
+
     def drop_suffix(self, name: str, layers: int, head: bool = False) -> None:
         """Forget residency of layers >= ``layers`` (and of the final norm +
         lm_head unless ``head``): bytes stay, the ledger says they are gone,
