@@ -684,6 +684,31 @@ def run_ours(args, rank, world, local_rank):
 
         line["config3_switch_burst"] = run_burst(switches=args.config3_switches, device=dev)
         torch.cuda.empty_cache()
+    if args.config5_policies:
+        # BASELINE configs[4]: the reference engine's 8-worker decision log
+        # replayed on real workers (tools/config5_live.py; ledger checked
+        # against the engine after every op); logical GPU g on rank g % world
+        sys.path.insert(0, str(ROOT / "tools"))
+        from config5_live import HostImages, load_trace, replay_gpu, summarize
+
+        trace = load_trace()
+        pols = [p_ for p_ in args.config5_policies.split(",") if p_]
+        mine = [g for g in range(trace["gpus"]) if g % world == rank]
+        need = sorted({o["model"] for p_ in pols for o in trace["policies"][p_]["ops"]
+                       if o["gpu"] in mine and "model" in o})
+        t_c5 = time.perf_counter()
+        images = HostImages(need, dev)
+        c5 = {"setup_s": time.perf_counter() - t_c5, "logical_gpus_per_rank": len(mine)}
+        for p_ in pols:
+            res = [replay_gpu(trace, p_, g, dev, images) for g in mine]
+            if world > 1:
+                allres = [None] * world
+                dist.all_gather_object(allres, res)
+                res = [x for r_ in allres for x in r_]
+            c5[p_] = summarize(trace, p_, res)
+        line["config5_live"] = c5
+        del images
+        torch.cuda.empty_cache()
     if world > 1 or args.tp_block:
         # BASELINE configs[3] on the same ranks: Llama-3-70B TP=world cold start
         line["tp_config4"] = run_tp(args, rank, world, local_rank,
@@ -871,6 +896,8 @@ def main():
     ap.add_argument("--tp-block", action="store_true", help="run the TP block at N = 1 too (TP = 1)")
     ap.add_argument("--only-tp", action="store_true", help="test hook: run only the TP block")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config5-policies", default="warmserve,no_prewarm",
+                    help="BASELINE configs[4] live replay policies ('' to skip)")
     ap.add_argument("--config3-switches", type=int, default=1000,
                     help="BASELINE configs[2] switch burst length (0: skip)")
     ap.add_argument("--decode-ctx", type=int, default=1024)
