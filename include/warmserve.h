@@ -302,6 +302,19 @@ int ws_peer_allreduce_f32(ws_peer* p, float* buf, int64_t count, void* stream);
  * copy and no separate residual-add launch. */
 int ws_peer_next_slot(ws_peer* p, float** slot);
 int ws_peer_reduce_add_f32(ws_peer* p, float* x, int64_t count, void* stream);
+/* Row-parallel projection fused with its allreduce (replaces the
+ * reference's TP sync term engine.py:110-113): x[M, N] += sum over ranks of
+ * A_r[M, K] W_r[N, K]^T. For prefill-sized shapes (M >= 256, N % 256 == 0,
+ * K % 64 == 0) the CTA-pair tcgen05 GEMM stores its bf16 partial into the
+ * exported slot and publishes every 128 x 256 block with a system-scope flag;
+ * a reduce kernel running beside it (programmatic dependent launch) has the
+ * block's owner rank sum the W partials in rank order as soon as they are all
+ * published, and every rank add the owner's reduced block into x — the link
+ * traffic (2(W-1)/W of the bf16 partial per rank) overlaps the GEMM tile by
+ * tile. Other shapes: fp32 partial into the slot + ws_peer_reduce_add_f32.
+ * Results are bit-identical on all ranks. Every rank must make the same calls. */
+int ws_peer_gemm_reduce_add(ws_peer* p, const void* A, const void* W, int32_t M, int32_t N, int32_t K, float* x,
+                            void* stream);
 /* recv[r * count + i] = rank r's send[i] (the vocab-parallel lm_head shards). */
 int ws_peer_allgather_f32(ws_peer* p, const float* send, float* recv, int64_t count, void* stream);
 /* A TP communicator with no NCCL behind it: every collective on `peer`

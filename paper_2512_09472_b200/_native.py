@@ -133,6 +133,7 @@ SIGNATURES: dict[str, list] = {
     "ws_comm_set_peer": [vp, vp, i64],
     "ws_peer_next_slot": [vp, P(vp)],
     "ws_peer_reduce_add_f32": [vp, vp, i64, vp],
+    "ws_peer_gemm_reduce_add": [vp, vp, vp, i32, i32, i32, vp, vp],
     "ws_peer_allgather_f32": [vp, vp, vp, i64, vp],
     "ws_comm_create_peer": [i32, i32, i32, vp, i64, P(vp)],
 }

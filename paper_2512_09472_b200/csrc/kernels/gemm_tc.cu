@@ -765,6 +765,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if (ep.tile_flags != nullptr) {  // publish: these 128 rows x 256 columns are in C
+        st.drain();
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __threadfence_system();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (r_in == 0)
+          asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(ep.tile_flags + 2 * tile + rank),
+                       "r"(ep.tile_epoch)
+                       : "memory");
+      }
       if (sliced && sq + 1 < sched.slices) {  // publish: slice sq of these 128 rows is in x
         st.drain();
         asm volatile("fence.proxy.async.global;\n" ::: "memory");

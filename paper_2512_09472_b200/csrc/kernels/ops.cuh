@@ -89,6 +89,13 @@ struct TcEpilogue {
   bf16* norm_out = nullptr;
   float* row_ss = nullptr;
   float* row_scale = nullptr;
+  // Tile publication (CTA-pair tcgen05 kernel, kStoreBf16 / kStoreF32 only):
+  // once the TMA stores of a CTA's 128 rows x 256 columns of tile t have
+  // landed, tile_flags[2 t + rank in pair] = tile_epoch with a system-scope
+  // release, so a consumer on this or a peer GPU can take the block while the
+  // GEMM still runs (peer.cu's fused row-parallel allreduce).
+  uint32_t* tile_flags = nullptr;
+  uint32_t tile_epoch = 0;
 };
 bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim);
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,

@@ -210,7 +210,9 @@ int row_parallel(const ws_model* m, const ws::bf16* A, const ws::bf16* B, int M,
   }
   if (ws_peer* peer = comm_peer(m->comm, (int64_t)M * N)) {
     // peer memory: the GEMM writes its partial straight into this rank's
-    // exported slot, one kernel sums all ranks' slots into the residual
+    // exported slot; prefill shapes reduce it block by block beside the GEMM
+    // (ws_peer_gemm_reduce_add), decode shapes with one reduce-add kernel
+    if (!(m->gemm_impl & 1)) return ws_peer_gemm_reduce_add(peer, A, B, M, N, K, x, st);
     float* slot = nullptr;
     if (int e = ws_peer_next_slot(peer, &slot)) return e;
     gemm(m, A, B, M, N, K, Epi::kStoreF32, slot, nullptr, st);

@@ -28,11 +28,20 @@
 #include <vector>
 
 #include "common.h"
+#include "kernels/ops.cuh"
+#include "kernels/pdl.cuh"
+
+using bf16_t = __nv_bfloat16;
 
 namespace {
 
 constexpr int kMaxPeers = 8;
-constexpr int64_t kFlagBytes = 4096;  // flag row + padding; data slots follow
+// Fused GEMM + allreduce: per 128-row x 256-column block of the row-parallel
+// output, a "partial stored" flag (written by the GEMM epilogue) and a
+// "block reduced" flag (written by its owner rank's reduce), per rank.
+constexpr int kMaxBlocks = 8192;
+constexpr int64_t kRowFlagBytes = 4096;  // epoch flag rows of the unfused kernels
+constexpr int64_t kFlagBytes = kRowFlagBytes + 2 * kMaxBlocks * 4;  // + tile flags; data slots follow
 
 int64_t slot_bytes(int64_t max_count) { return (max_count * 4 + 255) / 256 * 256; }
 
@@ -154,6 +163,103 @@ __global__ void __launch_bounds__(256, 4) peer_gather_chunks_kernel(const __grid
     const float v = __ldcv(a.res[i / chunk] + i);
     out[i] = ACC ? out[i] + v : v;
   }
+}
+
+// ---- fused row-parallel GEMM + allreduce (prefill-sized TP partials) ----
+// Block b = 128 rows x 256 columns of the [M, N] output: tile b / 2 of the
+// CTA-pair GEMM (m-block tile % mb, n-block tile / mb), rows (b & 1) * 128.
+// Phase 1: rank r owns blocks b % W == r; as soon as every rank's GEMM has
+// published block b, the owner sums the W bf16 partials in rank order (fp32)
+// into its own reduced region (bf16) and publishes it. Phase 2: every rank
+// takes every block from its owner once published: x += reduced. Each CTA
+// walks its blocks in tile order, so both phases trail the GEMM's waves tile
+// by tile over the links instead of waiting for the whole partial; every
+// element is reduced once, in rank order: all ranks hold the same bits.
+struct TileArgs {
+  const bf16_t* part[kMaxPeers];  // every rank's partial slot (bf16 [M, N])
+  bf16_t* red[kMaxPeers];         // every rank's reduced region (bf16 [M, N], owner blocks only)
+  const uint32_t* done[kMaxPeers];  // every rank's "partial stored" flags
+  uint32_t* reduced[kMaxPeers];     // every rank's "block reduced" flags
+  int rank, world, M, N, mb;        // mb: 256-row m-blocks
+};
+
+__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t epoch) {
+  while ((int32_t)(ld_acquire_sys(f) - epoch) < 0) __nanosleep(64);
+}
+
+__global__ void __launch_bounds__(256, 4) peer_tile_reduce_kernel(const __grid_constant__ TileArgs a, float* x,
+                                                               uint32_t epoch) {
+  // no griddepcontrol.wait: launched as the GEMM's programmatic dependent, it
+  // runs beside the GEMM and synchronises on the per-block flags (a flag is
+  // only published after the GEMM passed its own wait, i.e. after every
+  // earlier kernel of the stream completed)
+  const int nb = a.N / 256, blocks = a.mb * 2 * nb;
+  __shared__ bool ready;
+  auto rows_of = [&](int b, int& r0, int& c0) {
+    const int tile = b >> 1;
+    r0 = (tile % a.mb) * 256 + (b & 1) * 128;
+    c0 = (tile / a.mb) * 256;
+  };
+  // phase 1: owned blocks
+  for (int b = a.rank + (int)blockIdx.x * a.world; b < blocks; b += (int)gridDim.x * a.world) {
+    if (threadIdx.x < a.world) wait_flag(a.done[threadIdx.x] + b, epoch);
+    __syncthreads();
+    int r0, c0;
+    rows_of(b, r0, c0);
+    const int rows = min(128, a.M - r0);
+    // 128 x 256 bf16 = 4096 16-byte vectors; thread: 16 of them
+    for (int v = threadIdx.x; v < rows * 32; v += 256) {
+      const int64_t off = (int64_t)(r0 + v / 32) * a.N + c0 + (v % 32) * 8;
+      float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < a.world; ++p) {
+        const uint4 u = __ldcv(reinterpret_cast<const uint4*>(a.part[p] + off));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          s[2 * k] += __uint_as_float(w[k] << 16);
+          s[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+        }
+      }
+      uint4 o;
+      uint32_t* ow = &o.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(s[2 * k], s[2 * k + 1]);
+        ow[k] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      *reinterpret_cast<uint4*>(a.red[a.rank] + off) = o;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(a.reduced[a.rank] + b, epoch);
+  }
+  // phase 2: every block, from its owner
+  for (int b = (int)blockIdx.x; b < blocks; b += (int)gridDim.x) {
+    const int owner = b % a.world;
+    if (threadIdx.x == 0) wait_flag(a.reduced[owner] + b, epoch);
+    __syncthreads();
+    int r0, c0;
+    rows_of(b, r0, c0);
+    const int rows = min(128, a.M - r0);
+    for (int v = threadIdx.x; v < rows * 32; v += 256) {
+      const int64_t off = (int64_t)(r0 + v / 32) * a.N + c0 + (v % 32) * 8;
+      const uint4 u = __ldcv(reinterpret_cast<const uint4*>(a.red[owner] + off));
+      float4* xp = reinterpret_cast<float4*>(x + off);
+      float4 x0 = xp[0], x1 = xp[1];
+      x0.x += __uint_as_float(u.x << 16);
+      x0.y += __uint_as_float(u.x & 0xffff0000u);
+      x0.z += __uint_as_float(u.y << 16);
+      x0.w += __uint_as_float(u.y & 0xffff0000u);
+      x1.x += __uint_as_float(u.z << 16);
+      x1.y += __uint_as_float(u.z & 0xffff0000u);
+      x1.z += __uint_as_float(u.w << 16);
+      x1.w += __uint_as_float(u.w & 0xffff0000u);
+      xp[0] = x0;
+      xp[1] = x1;
+    }
+    __syncthreads();  // `ready`-free: the next block's wait is issued after every thread left this one
+  }
+  (void)ready;
 }
 
 }  // namespace
@@ -299,6 +405,53 @@ int ws_peer_next_slot(ws_peer* p, float** slot) {
   if (!p || !slot) WS_FAIL(WS_ERR_INVALID, "bad peer slot query");
   const uint32_t next = p->epoch + 1;
   *slot = reinterpret_cast<float*>(p->bufs[p->rank] + kFlagBytes + (int64_t)(next & 1) * slot_bytes(p->max_count));
+  return WS_OK;
+}
+
+int ws_peer_gemm_reduce_add(ws_peer* p, const void* A, const void* W, int32_t M, int32_t N, int32_t K, float* x,
+                            void* stream) {
+  if (!p || !A || !W || !x || M < 1 || N < 1 || K < 1 || (int64_t)M * N > p->max_count ||
+      reinterpret_cast<uintptr_t>(x) % 16)
+    WS_FAIL(WS_ERR_INVALID, "bad fused GEMM + allreduce (M x N <= max_count, 16-byte aligned x)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bf16_t* a = static_cast<const bf16_t*>(A);
+  const bf16_t* w = static_cast<const bf16_t*>(W);
+  const int mb = (M + 255) / 256;
+  const bool fused = p->world > 1 && M >= 256 && N % 256 == 0 && K % 64 == 0 && mb * 2 * (N / 256) <= kMaxBlocks;
+  if (!fused) {  // unfused: fp32 partial into the slot, then one reduce-add kernel
+    float* slot = nullptr;
+    if (int e = ws_peer_next_slot(p, &slot)) return e;
+    ws::launch_gemm(a, w, M, N, K, ws::Epi::kStoreF32, slot, nullptr, st);
+    if (p->world == 1) {
+      ws::launch_add_f32(x, slot, (int64_t)M * N, st);
+      return WS_OK;
+    }
+    return run_epoch(p, x, (int64_t)M * N, 1, st);
+  }
+  const uint32_t epoch = ++p->epoch;
+  const int64_t sb = slot_bytes(p->max_count);
+  const int64_t slot = kFlagBytes + (int64_t)(epoch & 1) * sb, res = kFlagBytes + (2 + (int64_t)(epoch & 1)) * sb;
+  TileArgs t{};
+  t.rank = p->rank;
+  t.world = p->world;
+  t.M = M;
+  t.N = N;
+  t.mb = mb;
+  for (int r = 0; r < p->world; ++r) {
+    t.part[r] = reinterpret_cast<const bf16_t*>(p->bufs[r] + slot);
+    t.red[r] = reinterpret_cast<bf16_t*>(p->bufs[r] + res);
+    t.done[r] = reinterpret_cast<const uint32_t*>(p->bufs[r] + kRowFlagBytes);
+    t.reduced[r] = reinterpret_cast<uint32_t*>(p->bufs[r] + kRowFlagBytes + kMaxBlocks * 4);
+  }
+  ws::TcEpilogue e;
+  e.mode = ws::Epi::kStoreBf16;
+  e.C = p->bufs[p->rank] + slot;
+  e.tile_flags = reinterpret_cast<uint32_t*>(p->bufs[p->rank] + kRowFlagBytes);
+  e.tile_epoch = epoch;
+  if (!ws::launch_gemm_tc_epi(a, w, M, N, K, e, st)) WS_FAIL(WS_ERR_CUDA, "fused row-parallel GEMM declined");
+  ws::count_launch();
+  ws::launch_pdl(peer_tile_reduce_kernel, dim3(ws::kNumSMs), dim3(256), 0, st, t, x, epoch);
+  WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 

@@ -75,6 +75,22 @@ class PeerAllreduce:
         N.call("ws_peer_reduce_add_f32", self._h, C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(st.cuda_stream))
         return x
 
+    def gemm_reduce_add_(self, x: torch.Tensor, A: torch.Tensor, W: torch.Tensor,
+                         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """x[M, N] += sum over ranks of A_r W_r^T (bf16 A [M, K], W [N, K]):
+        the row-parallel GEMM fused with its allreduce (ws_peer_gemm_reduce_add)."""
+        if x.dtype != torch.float32 or A.dtype != torch.bfloat16 or W.dtype != torch.bfloat16:
+            raise ValueError("gemm_reduce_add_ takes fp32 x and bf16 A, W")
+        M, K = A.shape
+        Nn = W.shape[0]
+        if tuple(x.shape) != (M, Nn) or W.shape[1] != K or not (x.is_contiguous() and A.is_contiguous()
+                                                                and W.is_contiguous()):
+            raise ValueError("gemm_reduce_add_: x [M, N], A [M, K], W [N, K], contiguous")
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        N.call("ws_peer_gemm_reduce_add", self._h, C.c_void_p(A.data_ptr()), C.c_void_p(W.data_ptr()), M, Nn, K,
+               C.c_void_p(x.data_ptr()), C.c_void_p(st.cuda_stream))
+        return x
+
     def close(self) -> None:
         if self._h:
             torch.cuda.synchronize()

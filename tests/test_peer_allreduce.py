@@ -14,6 +14,10 @@ import torch
 
 # two-shot from 1 MiB (262,144 floats): ragged sizes exercise the scalar tails of
 # the chunk reduce / gather (n % 4 != 0, a short last chunk)
+# (M, N, K) of the fused row-parallel GEMM + allreduce: 256-row tiles, a ragged
+# last 128-row block (300, 1537), several waves of tiles (1024 x 1024), and the
+# unfused fallback below 256 rows (40)
+FUSED = [(512, 1024, 512), (300, 512, 256), (1024, 1024, 320), (40, 256, 128), (1537, 256, 256)]
 SIZES = [1, 3, 1000, 4096 * 8 + 5, 1 << 20, 17, 1 << 20, (1 << 18) + 3, (1 << 20) + 7, (1 << 18) + 1]
 
 
@@ -40,7 +44,7 @@ def _worker(rank, world, port, q):
 
         torch.cuda.set_device(0)
         pa = PeerAllreduce(max_count=(1 << 20) + 64)
-        bad = []
+        bad, fused_out = [], []
         for step, n in enumerate(SIZES):
             t = _inputs(rank, n, step).cuda()
             pa.allreduce_(t)
@@ -61,10 +65,31 @@ def _worker(rank, world, port, q):
             want = _inputs(9, n, 50 + step) + s
             if not torch.equal(x.cpu(), want):
                 bad.append(("fused", n, (x.cpu() - want).abs().max().item()))
+        # row-parallel GEMM fused with its allreduce: block-pipelined two-shot
+        # (M >= 256) and the unfused fallback (M < 256); x identical on all ranks
+        for step, (M, Nn, K) in enumerate(FUSED):
+            g = torch.Generator().manual_seed(7 * step + rank)
+            A = torch.randn(M, K, generator=g).bfloat16()
+            Wt = (torch.randn(Nn, K, generator=g) * 0.05).bfloat16()
+            x0 = torch.randn(M, Nn, generator=torch.Generator().manual_seed(99 + step))
+            x = x0.cuda()
+            pa.gemm_reduce_add_(x, A.cuda(), Wt.cuda())
+            torch.cuda.synchronize()
+            want = x0.clone()
+            for r in range(world):
+                gr = torch.Generator().manual_seed(7 * step + r)
+                Ar = torch.randn(M, K, generator=gr).bfloat16()
+                Wr = (torch.randn(Nn, K, generator=gr) * 0.05).bfloat16()
+                want += Ar.float() @ Wr.float().T
+            got = x.cpu()
+            rel = ((got - want).norm() / (want - x0).norm()).item()
+            if not rel < 1e-2:
+                bad.append(("gemm_reduce_add", M, Nn, K, rel))
+            fused_out.append(got)
         with pytest.raises(Exception):
             pa.allreduce_(torch.zeros(8, device="cuda", dtype=torch.float64))
         pa.close()
-        q.put((rank, bad))
+        q.put((rank, (bad, [t.numpy().tobytes() for t in fused_out])))
     finally:
         dist.destroy_process_group()
 
@@ -88,4 +113,6 @@ def test_peer_allreduce_processes_share_one_gpu(cuda_device, world):
             if p.exitcode is None:
                 p.kill()
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    assert res == {r: [] for r in range(world)}, res
+    assert {r: v[0] for r, v in res.items()} == {r: [] for r in range(world)}, res
+    # the fused GEMM + allreduce leaves the same bits on every rank
+    assert all(res[r][1] == res[0][1] for r in range(world))
