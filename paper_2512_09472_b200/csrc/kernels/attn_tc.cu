@@ -599,8 +599,13 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 // TMEM alloc + MMA issue, the K gather, the V gather and the Q loads.
 namespace pair2 {
 #ifndef WS_ATTN_POLY
-#define WS_ATTN_POLY 2
+#define WS_ATTN_POLY 3
 #endif
+// 3/8 on the polynomial. A/B at 8B / 2048 tokens (tools/ab_attn_poly.sh):
+// 0-6 of 8 -> 46.5 / 46.5 / 45.0 / 46.9 / 48.1 / 49.4 / 51.2 us. 2/8 is 0.25%
+// of a prefill faster but rounds P differently enough to flip the greedy
+// token of the full-depth parity prompt that sits at a bf16 near-tie (fp32
+// margin 0.045; the bf16-floor emulation flips it too), so 3/8 stays.
 constexpr int kPolyPairs = WS_ATTN_POLY;
 #ifndef WS_ATTN_SPLIT
 #define WS_ATTN_SPLIT 0

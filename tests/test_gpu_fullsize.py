@@ -117,11 +117,12 @@ def test_llama3_8b_full_depth_cold_k4_plain_and_packed_match_oracle(llama8b):
         t0 = time.perf_counter()
         ref = O.forward_streamed(cfg, cfg.layout(), host, prompt.long())
         oracle_s = time.perf_counter() - t0
-        floor = _rel(O.forward_streamed(cfg, cfg.layout(), host, prompt.long(), emulate_bf16=True), ref)
+        emu = O.forward_streamed(cfg, cfg.layout(), host, prompt.long(), emulate_bf16=True)
+        floor = _rel(emu, ref)
         rel = _rel(plain, ref)
         top2 = ref.topk(2)
         results.append({"seed": seed, "rel": rel, "bf16_floor_rel": floor, "gpu_token": cold.token,
-                        "ref_token": int(top2.indices[0]),
+                        "ref_token": int(top2.indices[0]), "bf16_floor_token": int(emu.argmax()),
                         "ref_margin": float(top2.values[0] - top2.values[1]),
                         "cold_plain_ttft_ms": cold.ttft_ms, "cold_packed_ttft_ms": coldp.ttft_ms,
                         "warm_ttft_ms": warm.ttft_ms, "oracle_cpu_s": oracle_s,
