@@ -48,6 +48,16 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def bench_config(args, world: int) -> dict:
+    """The workload both arms name (BASELINE configs[1]); arm-specific
+    details go under other keys."""
+    layers = REF_SHAPES[args.model]["layers"] if args.model in REF_SHAPES else None
+    return {"workload": f"{args.model} universal worker, first {args.prewarm_layers} of {layers} layers prewarmed, "
+                        f"{args.prompt}-token prompt (BASELINE configs[1])",
+            "model": args.model, "prompt_tokens": args.prompt, "prewarmed_layers": args.prewarm_layers,
+            "parallelism": "replicas" if world > 1 else "single"}
+
+
 def pct(xs, q):
     xs = sorted(xs)
     if not xs:
@@ -293,10 +303,10 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded random-init weights of the named shape, random token ids)",
-        "config": {"workload": f"{args.model} universal worker, 2048-token prompt prefill (BASELINE configs[1]); "
-                               "the reference has no GPU path (its prefill is the linear model engine.py:107-108), "
-                               "so its arm is the CPU fp32 oracle port of the full forward",
-                   "model": args.model, "prompt_tokens": args.prompt},
+        "config": bench_config(args, world),
+        "arm": "the reference has no GPU path (its prefill is the linear model engine.py:107-108), so its arm is "
+               "the CPU fp32 oracle port of the full forward of the same workload (every layer of the prefill; the "
+               "prewarmed prefix changes nothing on a CPU)",
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample,
                          "cpu": _cpu_model()},
         "ledger_us": _ref_ledger_ops(),
@@ -578,13 +588,10 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": Wm,
         "ms_per_step": prefill_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded random-init weights of the named shape, random token ids)",
-        "config": {"workload": f"{cfg.name} universal worker, first {args.prewarm_layers} of {cfg.layers} layers "
-                               f"prewarmed, {S}-token prompt (BASELINE configs[1])",
-                   "model": cfg.name, "prompt_tokens": S, "prewarmed_layers": args.prewarm_layers,
-                   "weight_source": "pinned host memory (PCIe H2D on the copy engine)",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "no flush needed: 16 GB of weights per step > 126 MB L2",
-                   "pool_pages": pool_pages, "pool_gib": pool_pages * M.PAGE / (1 << 30)},
+        "config": bench_config(args, world),
+        "setup": {"weight_source": "pinned host memory (PCIe H2D on the copy engine)",
+                  "l2": "no flush needed: 16 GB of weights per step > 126 MB L2",
+                  "pool_pages": pool_pages, "pool_gib": pool_pages * M.PAGE / (1 << 30)},
         "e2e": {"value": e2e_value, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(statistics.median(r.streamed_bytes for r in cold_packed)) + S * 4,
                 "d2h_bytes_per_step": 4,
