@@ -27,6 +27,8 @@
 #include "pdl.cuh"
 
 namespace ws {
+
+bool kv_window_tmap(const KvGeom& kv, int hd, CUtensorMap* out);  // attn_tc.cu
 namespace {
 
 using namespace dev;
@@ -509,6 +511,112 @@ __device__ __forceinline__ void epilogue_tile_tma(const TcEpilogue& ep, const CU
   }
 }
 
+// QKV + RoPE + paged KV append through the staging boxes (CTA-pair kernel,
+// ep.kv_tma): this warp's 32 rows x one head (128 columns) are rotated in
+// registers and staged as two 64-column SWIZZLE_128B boxes; q heads leave by
+// TMA into the qkv buffer (map_c), k / v heads as two 16-token boxes each
+// into the page window (map_kv: rows of head_dim bf16, 64 x 16 boxes) at the
+// pages the block table names. A 16-token group that is not fully inside the
+// prompt is stored row by row instead. Replaces 32-line-per-instruction
+// direct stores (the QKV GEMM ran 25% slower with this epilogue than plain).
+__device__ __forceinline__ void epilogue_rope_tma(const TcEpilogue& ep, const CUtensorMap* map_c,
+                                                  const CUtensorMap* map_kv, uint32_t stg_base, int lane,
+                                                  uint32_t tacc, int row0, int n0, int M) {
+  constexpr int HD = 128;
+  const KvGeom& kv = ep.kv;
+  const int row = row0 + lane;
+  const bool valid = row < M;
+  const int pos = ep.pos0 + (valid ? row : row0);
+  const float2* cs = ep.rope + (int64_t)pos * (HD / 2);
+  // pages of the warp's two 16-token groups (rows row0.., row0 + 16..)
+  const int32_t* bt = kv.block_tables + (int64_t)ep.seq0 * kv.max_blocks;
+  const int rows_pp = (int)(kv.page_size / (HD * 2));
+  const int p0 = ep.pos0 + row0;
+  const bool g_full0 = row0 + 15 < M, g_full1 = row0 + 31 < M;
+  const int32_t pg0 = g_full0 ? bt[p0 / kv.tpb] : 0, pg1 = g_full1 ? bt[(p0 + 16) / kv.tpb] : 0;
+  bf16* page = nullptr;
+  if (valid) {
+    const int32_t pg = bt[pos / kv.tpb];
+    page = reinterpret_cast<bf16*>(kv.window + (int64_t)pg * kv.page_size) + (int64_t)(pos % kv.tpb) * HD;
+  }
+  const bool my_group_tma = (lane < 16) ? g_full0 : g_full1;
+#pragma unroll 1
+  for (int hl = 0; hl < BN / HD; ++hl) {
+    const int hs = (n0 + hl * HD) / HD;  // head slot in [0, H + 2KV)
+    const bool is_v = hs >= ep.heads + kv.kv_heads;
+    const bool is_k = !is_v && hs >= ep.heads;
+    // both boxes free: every earlier TMA store has read its smem
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {  // c: columns [32c, 32c+32) and their rotate_half partners +64
+      uint32_t a[32], b[32];
+      const int ca = hl * 4 + c, cb = ca + 2;
+      TMEM_LD32(tacc + ca * 32, a);
+      TMEM_LD32(tacc + cb * 32, b);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      float fa[32], fb[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        fa[j] = __uint_as_float(a[j]);
+        fb[j] = __uint_as_float(b[j]);
+      }
+      if (ep.bias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          fa[j] += bf2f(ep.bias[n0 + ca * 32 + j]);
+          fb[j] += bf2f(ep.bias[n0 + cb * 32 + j]);
+        }
+      }
+      if (!is_v) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 t = cs[c * 32 + j];
+          const float x = fa[j], y = fb[j];
+          fa[j] = x * t.x - y * t.y;
+          fb[j] = y * t.x + x * t.y;
+        }
+      }
+      if ((is_k || is_v) && valid && !my_group_tma) {  // a partial 16-token group: row stores
+        const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
+        bf16* dst = page + kv.plane(ep.layer, is_v ? 1 : 0, kvh);
+        store_bf16x32(dst + c * 32, fa);
+        store_bf16x32(dst + c * 32 + HD / 2, fb);
+      }
+      stage_bf16(stg_base, lane, c, fa);         // box 0: head columns [0, 64)
+      stage_bf16(stg_base + 4096, lane, c, fb);  // box 1: head columns [64, 128)
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      if (!is_k && !is_v) {
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx)
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map_c),
+                       "r"(n0 + hl * HD + bx * 64), "r"(row0), "r"(stg_base + bx * 4096)
+                       : "memory");
+      } else {
+        const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
+        const int plane_rows = (int)(kv.plane(ep.layer, is_v ? 1 : 0, kvh) / HD);
+        const int y0 = pg0 * rows_pp + plane_rows + p0 % kv.tpb;
+        const int y1 = pg1 * rows_pp + plane_rows + (p0 + 16) % kv.tpb;
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+          if (g_full0)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map_kv),
+                         "r"(bx * 64), "r"(y0), "r"(stg_base + bx * 4096)
+                         : "memory");
+          if (g_full1)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map_kv),
+                         "r"(bx * 64), "r"(y1), "r"(stg_base + bx * 4096 + 2048)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+}
+
 // Work schedule of the pair kernel: tiles go round-robin to the pairs (m
 // fastest), so all pairs run the same k-range of neighbouring tiles at the
 // same time and each weight block is read from HBM once (L2 reuse).
@@ -572,7 +680,8 @@ template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                     int N, int K, const __grid_constant__ TcEpilogue ep,
-                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TailSched sched) {
+                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TailSched sched,
+                    const __grid_constant__ CUtensorMap map_kv) {
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -750,8 +859,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
       }
       if constexpr (MODE == (int)Epi::kRopeKV) {
-        const int row = m0 + r_in;
-        epilogue_tile<MODE>(ep, tacc, row < M ? row : -1, n0, N, ep.kv.head_dim);
+        if (ep.kv_tma) {
+          epilogue_rope_tma(ep, &map_c, &map_kv, st.base, lane, tacc, m0 + q * 32, n0, M);
+        } else {
+          const int row = m0 + r_in;
+          epilogue_tile<MODE>(ep, tacc, row < M ? row : -1, n0, N, ep.kv.head_dim);
+        }
       } else {
         epilogue_tile_tma<MODE>(ep, &map_c, st, tacc, m0 + q * 32, n0);
       }
@@ -913,9 +1026,19 @@ bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
   } else if constexpr (MODE != (int)Epi::kRopeKV) {
     if (!make_out_map(&mc, e.C, M, N, 2)) return false;
   }
+  CUtensorMap mkv = mc;
+  TcEpilogue ee = e;
+  if constexpr (MODE == (int)Epi::kRopeKV) {
+    // TMA stores of the rotated rows: one sequence (prefill), 16-token runs
+    // per block starting at a run boundary, head_dim 128, the window mappable
+    static const bool on = !(getenv("WS_ROPE_TMA") && getenv("WS_ROPE_TMA")[0] == '0');
+    ee.kv_tma = on && e.kv.head_dim == 128 && !e.seq_arr && !e.pos_arr && e.kv.tpb % 16 == 0 && e.pos0 % 16 == 0 &&
+                make_out_map(&mc, e.C, M, N, 2) && kv_window_tmap(e.kv, 128, &mkv);
+  }
   const TailSched sched = tail_schedule(MODE, tiles, n_pairs, K / BK, st);
   count_launch();
-  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, e, mc, sched);
+  launch_pdl(gemm_tc2_kernel<MODE>, dim3(2 * n_pairs), dim3(THREADS), P_SMEM_BYTES, st, ma, mb, M, N, K, ee, mc, sched,
+             mkv);
   return true;
 }
 

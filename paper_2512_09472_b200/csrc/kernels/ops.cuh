@@ -96,6 +96,10 @@ struct TcEpilogue {
   // GEMM still runs (peer.cu's fused row-parallel allreduce).
   uint32_t* tile_flags = nullptr;
   uint32_t tile_epoch = 0;
+  // kRopeKV on the CTA-pair kernel: set by the launcher when the rotated K/V
+  // rows can leave as TMA boxes of 16 tokens into the page window (prefill of
+  // one sequence, block-aligned pos0, 16-token runs per block)
+  int kv_tma = 0;
 };
 bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim);
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
