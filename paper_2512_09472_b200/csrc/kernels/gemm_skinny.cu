@@ -51,6 +51,7 @@ constexpr int kSmemBudget = 216 * 1024;     // TMA ring, one CTA per SM
 struct SkinnyArgs {
   int M, N, K, Mp, stages, stage_bytes, total_iters, sub, kbs;
   float* partial;      // [grid][2][NB*128][Mp]
+  int csplit;          // >= 2: cluster split-K (see launch_gemm_skinny); 0: stream-K
 };
 
 // Residual producer of a folded RMSNorm (norm_role 1): x_new is final (one
@@ -117,6 +118,160 @@ __device__ __forceinline__ void store_out(const TcEpilogue& ep, const SkinnyArgs
 __device__ __forceinline__ int cta_of(int64_t it, int G, int total) { return (int)(((it + 1) * G - 1) / total); }
 __device__ __forceinline__ int it_begin(int c, int G, int total) { return (int)((int64_t)c * total / G); }
 
+// Epilogue of one (unit, weight row i, 4 batch rows) after the split-K sum:
+// folded-norm row scales, SwiGLU, then store / add / norm-produce.
+template <int MODE>
+__device__ __forceinline__ void fixup_store(const SkinnyArgs& args, const TcEpilogue& ep, int unit, int i, int q4,
+                                            const float4* sum, const float* row_scale) {
+  constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  float v[4] = {sum[0].x, sum[0].y, sum[0].z, sum[0].w};
+  float u[4] = {sum[NB - 1].x, sum[NB - 1].y, sum[NB - 1].z, sum[NB - 1].w};
+  if (ep.norm_role == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sc = q4 * 4 + k < args.M ? row_scale[q4 * 4 + k] : 0.f;
+      v[k] *= sc;
+      u[k] *= sc;
+    }
+  }
+  if constexpr (NB == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
+  }
+  const int row = unit * kRows + i;
+  if (row >= (MODE == (int)Epi::kSwiGLU ? args.N / 2 : args.N)) return;  // ragged last unit
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = q4 * 4 + k;
+    if (b >= args.M) break;
+    if constexpr (MODE == (int)Epi::kAddF32) {
+      float* dst = static_cast<float*>(ep.C) + (int64_t)b * args.N + row;
+      if (ep.norm_role == 1)
+        norm_produce(ep, args.N, b, row, *dst + v[k], dst);
+      else
+        *dst += v[k];
+    } else if constexpr (MODE == (int)Epi::kStoreF32) {
+      static_cast<float*>(ep.C)[(int64_t)b * args.N + row] = v[k];
+    } else if constexpr (MODE == (int)Epi::kSwiGLU) {
+      static_cast<bf16*>(ep.C)[(int64_t)b * (args.N / 2) + row] = f2bf(v[k]);
+    } else {
+      float x = v[k];
+      if constexpr (MODE == (int)Epi::kBiasBf16) x += bf2f(ep.bias[row]);
+      static_cast<bf16*>(ep.C)[(int64_t)b * args.N + row] = f2bf(x);
+    }
+  }
+}
+
+// RoPE + paged KV append of one rotate-half pair (columns col_a, col_b = col_a
+// + hd/2 of a head) for 4 batch rows, after the split-K sums va / vb.
+__device__ __forceinline__ void rope_store(const SkinnyArgs& args, const TcEpilogue& ep, int col_a, int q4,
+                                           float* va, float* vb, const float* row_scale) {
+  const KvGeom& kv = ep.kv;
+  const int hd = kv.head_dim, half = hd / 2, col_b = col_a + half, dd = col_a % half;
+  if (ep.norm_role == 2) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float sc = q4 * 4 + k < args.M ? row_scale[q4 * 4 + k] : 0.f;
+      va[k] *= sc;
+      vb[k] *= sc;
+    }
+  }
+  const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
+  const int hs = col_a / hd;  // head slot in [0, H + 2KV)
+  const bool is_v = hs >= ep.heads + kv.kv_heads, is_k = !is_v && hs >= ep.heads;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = q4 * 4 + k;
+    if (b >= args.M) break;
+    const int pos = ep.pos_arr ? ep.pos_arr[b] : ep.pos0 + b;
+    float x = va[k] + bias_a, y = vb[k] + bias_b;
+    if (!is_v) {
+      const float2 c = ep.rope[(int64_t)pos * half + dd];
+      const float rx = x * c.x - y * c.y, ry = y * c.x + x * c.y;
+      x = rx;
+      y = ry;
+    }
+    if (!is_k && !is_v) {
+      bf16* q = static_cast<bf16*>(ep.C) + (int64_t)b * args.N;
+      q[col_a] = f2bf(x);
+      q[col_b] = f2bf(y);
+    } else {
+      const int seq = ep.seq_arr ? ep.seq_arr[b] : ep.seq0;
+      const int32_t page = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
+      const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
+      bf16* dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page * kv.page_size) +
+                  kv.plane(ep.layer, is_v ? 1 : 0, kvh) + (int64_t)(pos % kv.tpb) * hd;
+      dst[dd] = f2bf(x);
+      dst[dd + half] = f2bf(y);
+    }
+  }
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t local, int cta) {
+  uint32_t remote;
+  float4 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(cta));
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
+// Cluster split-K reduction: the S CTAs of a cluster computed k-slices of one
+// unit and left their fp32 partials [NB][128][Mp] at shared address `part` in
+// their own shared memory. Each CTA's epilogue warps (t = 0..127) sum, in
+// k (= cluster rank) order over distributed shared memory, the 32-row blocks
+// b of the unit with b mod S == rank (rotate-half pair blocks for RoPE) and
+// apply the epilogue — the fix-up pass without a launch or a global round trip.
+template <int MODE>
+__device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcEpilogue& ep, int unit, int rank,
+                                               uint32_t part, const float* row_scale, int t) {
+  constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  const int S = args.csplit, Mp = args.Mp, quads = Mp / 4;
+  const int warp = t >> 5, lane = t & 31;
+  if constexpr (MODE == (int)Epi::kRopeKV) {
+    // pairs j in [0, 64): columns (unit*128 + (j / half) * hd + j % half, + half)
+    const int hd = ep.kv.head_dim, half = hd / 2;
+    int w = 0;
+    for (int blk = rank; blk < 2; blk += S)
+      for (int q4 = 0; q4 < quads; ++q4, ++w) {
+        if ((w & 3) != warp) continue;
+        const int j = blk * 32 + lane;
+        const int ia = (j / half) * hd + j % half, ib = ia + half;
+        float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
+        for (int c = 0; c < S; ++c) {
+          const float4 a = ld_dsmem_v4(part + (uint32_t)(((ia * Mp) + q4 * 4) * 4), c);
+          const float4 b = ld_dsmem_v4(part + (uint32_t)(((ib * Mp) + q4 * 4) * 4), c);
+          sa.x += a.x; sa.y += a.y; sa.z += a.z; sa.w += a.w;
+          sb.x += b.x; sb.y += b.y; sb.z += b.z; sb.w += b.w;
+        }
+        float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
+        rope_store(args, ep, unit * kRows + ia, q4, va, vb, row_scale);
+      }
+  } else {
+    int w = 0;
+    for (int blk = rank; blk < kRows / 32; blk += S)
+      for (int q4 = 0; q4 < quads; ++q4, ++w) {
+        if ((w & 3) != warp) continue;
+        const int i = blk * 32 + lane;
+        float4 sum[NB];
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb) sum[jb] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < S; ++c)
+#pragma unroll
+          for (int jb = 0; jb < NB; ++jb) {
+            const float4 a = ld_dsmem_v4(part + (uint32_t)((((jb * kRows + i) * Mp) + q4 * 4) * 4), c);
+            sum[jb].x += a.x; sum[jb].y += a.y; sum[jb].z += a.z; sum[jb].w += a.w;
+          }
+        fixup_store<MODE>(args, ep, unit, i, q4, sum, row_scale);
+      }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_a,
@@ -139,7 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int Mp = args.Mp, G = gridDim.x, total = args.total_iters;
   const int kbs = args.kbs, sub = args.sub, kBK = kBox * sub;
   const uint32_t a_off = NB * sub * kW_BYTES, a_box = args.Mp * kBox * 2;
-  const int it0 = it_begin(blockIdx.x, G, total), it1 = it_begin(blockIdx.x + 1, G, total);
+  // stream-K: equal contiguous ranges of the (unit, k-block) space; cluster
+  // split: CTA rank s of cluster u takes k-slice s of unit u
+  const int cs = args.csplit;
+  const int it0 = cs > 1 ? (blockIdx.x / cs) * kbs + (blockIdx.x % cs) * kbs / cs : it_begin(blockIdx.x, G, total);
+  const int it1 = cs > 1 ? (blockIdx.x / cs) * kbs + (blockIdx.x % cs + 1) * kbs / cs
+                         : it_begin(blockIdx.x + 1, G, total);
   const uint32_t acc_cols = NB * Mp;
   uint32_t tmem_cols = 32;
   while (tmem_cols < 2 * acc_cols) tmem_cols <<= 1;
@@ -280,7 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(tfull(acc), acc_phase);
       tc::fence_after();
       const uint32_t tacc = trow + acc * acc_cols;
-      float* mine = args.partial + ((int64_t)blockIdx.x * 2 + (seg == 0 ? 0 : 1)) * slot_floats;
+      // cluster split: the partial stays in this CTA's shared memory (the TMA
+      // ring, idle once the unit's last stage was consumed) for cluster_reduce
+      float* mine = cs > 1 ? reinterpret_cast<float*>(smem_raw + (base - raw))
+                           : args.partial + ((int64_t)blockIdx.x * 2 + (seg == 0 ? 0 : 1)) * slot_floats;
       for (int c = 0; c < Mp; c += 16) {
         uint32_t v[NB][16];
 #pragma unroll
@@ -300,9 +463,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < NB; ++j) {
             float4* dst = reinterpret_cast<float4*>(mine + ((int64_t)j * kRows + i) * Mp + c);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              __stcg(dst + q, make_float4(__uint_as_float(v[j][4 * q]), __uint_as_float(v[j][4 * q + 1]),
-                                          __uint_as_float(v[j][4 * q + 2]), __uint_as_float(v[j][4 * q + 3])));
+            for (int q = 0; q < 4; ++q) {
+              const float4 o = make_float4(__uint_as_float(v[j][4 * q]), __uint_as_float(v[j][4 * q + 1]),
+                                           __uint_as_float(v[j][4 * q + 2]), __uint_as_float(v[j][4 * q + 3]));
+              if (cs > 1)
+                dst[q] = o;
+              else
+                __stcg(dst + q, o);
+            }
           }
         }
       }
@@ -320,6 +488,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
+  if (cs > 1) {
+    cluster_sync();  // every k-slice's partial is in its CTA's shared memory
+    if (warp >= 4) {
+      const float* s_row = reinterpret_cast<const float*>(smem_raw + (bars + 8 * (2 * S + 6) - raw));
+      cluster_reduce<MODE>(args, ep, blockIdx.x / cs, blockIdx.x % cs, base, s_row, threadIdx.x - 128);
+    }
+    cluster_sync();  // no CTA leaves while its partial may still be read
+  }
 }
 
 // Split-K fix-up for the units no single CTA covered: out = epilogue(sum of
@@ -363,44 +539,8 @@ __device__ __forceinline__ void fixup_columns(const SkinnyArgs& args, const TcEp
         sum[j].w += p[k][j].w;
       }
   }
-  float v[4] = {sum[0].x, sum[0].y, sum[0].z, sum[0].w};
-  float u[4] = {sum[NB - 1].x, sum[NB - 1].y, sum[NB - 1].z, sum[NB - 1].w};
-  if (ep.norm_role == 2) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float sc = q4 * 4 + k < args.M ? ep.row_scale[q4 * 4 + k] : 0.f;
-      v[k] *= sc;
-      u[k] *= sc;
-    }
-  }
-  if constexpr (NB == 2) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
-  }
-  const int row = unit * kRows + i;
-  if (row >= (MODE == (int)Epi::kSwiGLU ? args.N / 2 : args.N)) return;  // ragged last unit
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int b = q4 * 4 + k;
-    if (b >= args.M) break;
-    if constexpr (MODE == (int)Epi::kAddF32) {
-      float* dst = static_cast<float*>(ep.C) + (int64_t)b * args.N + row;
-      if (ep.norm_role == 1)
-        norm_produce(ep, args.N, b, row, *dst + v[k], dst);
-      else
-        *dst += v[k];
-    } else if constexpr (MODE == (int)Epi::kStoreF32) {
-      static_cast<float*>(ep.C)[(int64_t)b * args.N + row] = v[k];
-    } else if constexpr (MODE == (int)Epi::kSwiGLU) {
-      static_cast<bf16*>(ep.C)[(int64_t)b * (args.N / 2) + row] = f2bf(v[k]);
-    } else {
-      float x = v[k];
-      if constexpr (MODE == (int)Epi::kBiasBf16) x += bf2f(ep.bias[row]);
-      static_cast<bf16*>(ep.C)[(int64_t)b * args.N + row] = f2bf(x);
-    }
-  }
+  fixup_store<MODE>(args, ep, unit, i, q4, sum, ep.row_scale);
 }
-
 template <int MODE>
 __global__ void __launch_bounds__(256) skinny_fixup_kernel(const __grid_constant__ SkinnyArgs args,
                                                            const __grid_constant__ TcEpilogue ep, int G) {
@@ -456,43 +596,7 @@ __global__ void __launch_bounds__(256) skinny_rope_fixup_kernel(const __grid_con
     }
   }
   float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
-  if (ep.norm_role == 2) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float sc = q4 * 4 + k < args.M ? ep.row_scale[q4 * 4 + k] : 0.f;
-      va[k] *= sc;
-      vb[k] *= sc;
-    }
-  }
-  const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
-  const int hs = col_a / hd;  // head slot in [0, H + 2KV)
-  const bool is_v = hs >= ep.heads + kv.kv_heads, is_k = !is_v && hs >= ep.heads;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int b = q4 * 4 + k;
-    if (b >= args.M) break;
-    const int pos = ep.pos_arr ? ep.pos_arr[b] : ep.pos0 + b;
-    float x = va[k] + bias_a, y = vb[k] + bias_b;
-    if (!is_v) {
-      const float2 c = ep.rope[(int64_t)pos * half + dd];
-      const float rx = x * c.x - y * c.y, ry = y * c.x + x * c.y;
-      x = rx;
-      y = ry;
-    }
-    if (!is_k && !is_v) {
-      bf16* q = static_cast<bf16*>(ep.C) + (int64_t)b * args.N;
-      q[col_a] = f2bf(x);
-      q[col_b] = f2bf(y);
-    } else {
-      const int seq = ep.seq_arr ? ep.seq_arr[b] : ep.seq0;
-      const int32_t page = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
-      const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
-      bf16* dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page * kv.page_size) +
-                  kv.plane(ep.layer, is_v ? 1 : 0, kvh) + (int64_t)(pos % kv.tpb) * hd;
-      dst[dd] = f2bf(x);
-      dst[dd + half] = f2bf(y);
-    }
-  }
+  rope_store(args, ep, col_a, q4, va, vb, ep.row_scale);
 }
 
 bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
@@ -543,6 +647,33 @@ void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs&
     attr = smem;
   }
   count_launch();
+  if (a.csplit > 1) {  // cluster split-K: the reduction runs inside the GEMM, no fix-up launch
+    static bool np = false;
+    if (!np) {
+      cudaFuncSetAttribute(gemm_skinny_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaGetLastError();
+      np = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = a.csplit;
+    attr[n].val.clusterDim.y = 1;
+    attr[n++].val.clusterDim.z = 1;
+    if (pdl_enabled()) {
+      attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    cudaLaunchKernelEx(&cfg, gemm_skinny_kernel<MODE>, mw, ma, a, e);
+    return;
+  }
   launch_pdl(gemm_skinny_kernel<MODE>, dim3(grid), dim3(kThreads), (size_t)smem, st, mw, ma, a, e);
   const int kbs = a.kbs, units = a.total_iters / kbs;
   if constexpr (MODE == (int)Epi::kRopeKV) {
@@ -615,6 +746,21 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // stream-K over all 148 SMs. Below ~90 units whole units lose: one SM pulls
   // ~64 GB/s, so 32-48 CTAs cannot stream at HBM rate (down: 57 vs 25 us).
   if (units * 10 >= kNumSMs * 6 && units <= kNumSMs) grid = units;
+  // Too few units to fill the SMs (decode O / down: 32, QKV: 48): split each
+  // unit's k-range over a thread-block cluster of S CTAs (units x S <= 148,
+  // S = 4, 3 or 2) whose fp32 partials are summed in k order over
+  // distributed shared memory inside the same kernel — deterministic like
+  // the fix-up kernel, without its launch and global round trip.
+  // WS_SKINNY_CLUSTER=0: stream-K + fix-up (A/B).
+  static const bool cl_on = !(getenv("WS_SKINNY_CLUSTER") && getenv("WS_SKINNY_CLUSTER")[0] == '0');
+  a.csplit = 0;
+  if (cl_on && grid != units && a.Mp <= 16)  // B = 64: 5.71 -> 6.24 ms per step with it; B <= 16 gains
+    for (int S_ = 4; S_ >= 2; --S_)
+      if (units * S_ <= kNumSMs && kbs >= 2 * S_) {
+        a.csplit = S_;
+        grid = units * S_;
+        break;
+      }
   if (e.mode == Epi::kRopeKV && units > grid) return false;  // <= 2 segments (partial slots) per CTA
   Scratch s;
   if (!scratch_for(st, &s)) return false;
