@@ -689,6 +689,10 @@ void decode_launch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, cons
   // enough (split, kv head, seq) units to fill the SMs; >= 64 keys per split
   const int units = n_seqs * kv.kv_heads;
   int n_splits = std::max(1, std::min({(kDecTargetCtas + units - 1) / units, (max_ctx + 63) / 64, kMaxSplits}));
+  // up to twice the cluster limit: fold into one cluster's worth of longer
+  // splits rather than add a combine launch (WS_DEC_SPLIT_CAP=0: A/B)
+  static const bool cap = !(std::getenv("WS_DEC_SPLIT_CAP") && std::getenv("WS_DEC_SPLIT_CAP")[0] == '0');
+  if (cap && n_splits > max_cluster && n_splits <= 2 * max_cluster) n_splits = max_cluster;
   const int split_keys = ((max_ctx + n_splits - 1) / n_splits + kDecKeys - 1) / kDecKeys * kDecKeys;
   n_splits = (max_ctx + split_keys - 1) / split_keys;
   // few splits (small batches): one cluster per (kv head, sequence) merges
