@@ -680,7 +680,12 @@ def run_ours(args, rank, world, local_rank):
     }
     w.release()
     w.close()
-    del w
+    # the later legs build their own images: drop this leg's pinned host
+    # copies first (host memory peaks per rank, N ranks per node)
+    del w, entry, slot, host, packed, prompts, prompt_pinned, B, A, Cm
+    import gc
+
+    gc.collect()
     torch.cuda.empty_cache()
     if args.config3_switches > 0:
         # BASELINE configs[2]: 4 models co-prewarmed, weight<->KV switch burst
