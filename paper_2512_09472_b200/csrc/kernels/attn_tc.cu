@@ -19,6 +19,8 @@
 //              softmax of tile j. TMEM: S0 [0,128) S1 [128,256) O [256,256+hd).
 #include <cuda.h>
 
+#include <mutex>
+
 #include "../common.h"
 #include "../driver.h"
 #include "device.cuh"
@@ -1053,6 +1055,8 @@ bool kv_window_tmap(const KvGeom& kv, int hd, CUtensorMap* out) {
   };
   static Entry cache[4];
   static int next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
   for (const Entry& e : cache)
     if (e.window == kv.window && e.pages == kv.n_pages && e.hd == hd) {
       *out = e.map;

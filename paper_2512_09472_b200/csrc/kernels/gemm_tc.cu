@@ -1052,9 +1052,12 @@ bool use_pair(int M) {
   return g_pair_mode == 1 && M >= 256;
 }
 
+bool gemm_tc_pair_enabled(int M) { return use_pair(M); }
+
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,
                         cudaStream_t st) {
   if (!gemm_tc_supported(M, N, K) || !gemm_tc_epilogue_supported(e, N, e.kv.head_dim)) return false;
+  if (e.tile_flags && !use_pair(M)) return false;  // only the pair kernel publishes its blocks
   CUtensorMap ma, mb;
   if (use_pair(M)) {
     if (!make_map(&ma, A, M, K, P_BM) || !make_map(&mb, B, N, K, P_BNH)) return false;

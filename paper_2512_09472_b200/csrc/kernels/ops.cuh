@@ -113,6 +113,9 @@ void launch_gemm_mma(const bf16* A, const bf16* B, int M, int N, int K, Epi epi,
 // tcgen05/TMEM/TMA GEMM (gemm_tc.cu): needs M >= 16, N % 256 == 0, K % 64 == 0;
 // returns false (nothing launched) otherwise.
 bool gemm_tc_supported(int M, int N, int K);
+// The CTA-pair kernel serves this M (M >= 256 unless WS_GEMM_PAIR=0); only it
+// honours TcEpilogue::tile_flags.
+bool gemm_tc_pair_enabled(int M);
 bool launch_gemm_tc(const bf16* A, const bf16* B, int M, int N, int K, Epi epi, void* C,
                     const bf16* bias, cudaStream_t st);
 // Decode-shaped tcgen05 GEMM (gemm_skinny.cu): M <= 128, N % 128 == 0

@@ -417,7 +417,8 @@ int ws_peer_gemm_reduce_add(ws_peer* p, const void* A, const void* W, int32_t M,
   const bf16_t* a = static_cast<const bf16_t*>(A);
   const bf16_t* w = static_cast<const bf16_t*>(W);
   const int mb = (M + 255) / 256;
-  const bool fused = p->world > 1 && M >= 256 && N % 256 == 0 && K % 64 == 0 && mb * 2 * (N / 256) <= kMaxBlocks;
+  const bool fused = p->world > 1 && ws::gemm_tc_pair_enabled(M) && N % 256 == 0 && K % 64 == 0 &&
+                     mb * 2 * (N / 256) <= kMaxBlocks;
   if (!fused) {  // unfused: fp32 partial into the slot, then one reduce-add kernel
     float* slot = nullptr;
     if (int e = ws_peer_next_slot(p, &slot)) return e;
