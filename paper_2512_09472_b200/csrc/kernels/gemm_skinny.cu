@@ -638,6 +638,36 @@ bool scratch_for(cudaStream_t st, Scratch* out) {
 
 int g_skinny_mode = -1;  // env WS_SKINNY=0 disables (A/B against the GEMV / 128-row tiles)
 
+// Clusters of S skinny CTAs (one per SM at this shared-memory footprint) the
+// GPU can hold at once; cached per (S, smem).
+int max_clusters(int S, int smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({S, smem});
+  if (it != cache.end()) return it->second;
+  // the largest opt-in size: never lower the attribute below a footprint
+  // launch_mode<0> already set (its cache only raises it)
+  cudaFuncSetAttribute(gemm_skinny_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(S * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, gemm_skinny_kernel<0>, &cfg);
+  if (e != cudaSuccess) n = 0;
+  cudaGetLastError();  // a failed query only disables the cluster split
+  cache[{S, smem}] = n;
+  return n;
+}
+
 template <int MODE>
 void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs& a, int grid, int smem,
                  const TcEpilogue& e, cudaStream_t st) {
@@ -754,9 +784,13 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // WS_SKINNY_CLUSTER=0: stream-K + fix-up (A/B).
   static const bool cl_on = !(getenv("WS_SKINNY_CLUSTER") && getenv("WS_SKINNY_CLUSTER")[0] == '0');
   a.csplit = 0;
-  if (cl_on && grid != units && a.Mp <= 16)  // B = 64: 5.71 -> 6.24 ms per step with it; B <= 16 gains
+  // up to 32 batch rows (B = 32: 4.57 -> 4.54 ms; B = 64 neutral to 0.5% slower)
+  static const int cl_mp = getenv("WS_SKINNY_CLUSTER_MP") ? atoi(getenv("WS_SKINNY_CLUSTER_MP")) : 32;
+  if (cl_on && grid != units && a.Mp <= cl_mp)
     for (int S_ = 4; S_ >= 2; --S_)
-      if (units * S_ <= kNumSMs && kbs >= 2 * S_) {
+      // every cluster resident at once (clusters are placed within a GPC: 48
+      // clusters of 3 did not fit in one wave and ran the QKV GEMM at half speed)
+      if (units * S_ <= kNumSMs && kbs >= 2 * S_ && units <= max_clusters(S_, smem)) {
         a.csplit = S_;
         grid = units * S_;
         break;
