@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(256, 4) peer_tile_reduce_kernel(const __grid_c
   // only published after the GEMM passed its own wait, i.e. after every
   // earlier kernel of the stream completed)
   const int nb = a.N / 256, blocks = a.mb * 2 * nb;
-  __shared__ bool ready;
   auto rows_of = [&](int b, int& r0, int& c0) {
     const int tile = b >> 1;
     r0 = (tile % a.mb) * 256 + (b & 1) * 128;
@@ -257,9 +256,8 @@ __global__ void __launch_bounds__(256, 4) peer_tile_reduce_kernel(const __grid_c
       xp[0] = x0;
       xp[1] = x1;
     }
-    __syncthreads();  // `ready`-free: the next block's wait is issued after every thread left this one
+    __syncthreads();  // the next block's wait is issued after every thread left this one
   }
-  (void)ready;
 }
 
 }  // namespace
