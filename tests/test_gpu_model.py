@@ -292,12 +292,15 @@ def _swiglu_ref(A, W):
 
 @pytest.mark.parametrize("M", [1, 7, 16, 40, 128])
 @pytest.mark.parametrize("N,K", [(256, 512), (4096, 4096), (1024, 14336), (6144, 256), (12800, 512), (25600, 256),
-                                 (1024, 320), (32064, 3072), (1000, 512), (129, 256)])
+                                 (1024, 320), (32064, 3072), (1000, 512), (129, 256), (28672, 4096), (14336, 1024)])
 def test_gemm_skinny_against_fp32(lib, M, N, K):
     """impl 4 forces the decode-shaped swap-AB split-K tcgen05 kernel; every
     epilogue, and the split-K reduction is deterministic (bit-identical reruns).
     12800 / 25600 rows = 100 units: one whole unit per CTA, no fix-up.
-    32064 / 1000 / 129 rows: a ragged last 128-row unit (Phi-3's lm_head)."""
+    32064 / 1000 / 129 rows: a ragged last 128-row unit (Phi-3's lm_head).
+    28672 x 4096 SwiGLU (8B gate/up, 112 units) and 14336 x 1024 (112 plain
+    units): several units per thread-block cluster at M <= 32 (cluster-local
+    stream-K, partials in shared memory and global slots)."""
     import ctypes as C
 
     g = torch.Generator(device="cuda").manual_seed(M * 31 + N + K)
