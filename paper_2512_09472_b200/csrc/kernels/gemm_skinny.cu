@@ -221,58 +221,144 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t local, int cta) {
   return v;
 }
 
+// Shared-memory slot of (row, quad) in a cluster split's fp32 partial
+// [NB*128][Mp]: quads XOR-swizzled by the row, so the 32 rows a warp touches
+// at one logical quad spread over all bank groups (unswizzled, a row stride
+// of 128 B or more put every lane of a 16 B access in the same banks:
+// 32-way conflicts on both the epilogue's stores and the reduce's remote loads).
+__device__ __forceinline__ uint32_t part_off(int row, int q4, int Mp) {
+  const int quads = Mp >> 2, group = quads & -quads;  // XOR inside aligned power-of-two groups of quads
+  return (uint32_t)((row * Mp + ((q4 ^ (row & (group - 1))) << 2)) << 2);
+}
+
 // Cluster split-K reduction: the S CTAs of a cluster computed k-slices of one
 // unit and left their fp32 partials [NB][128][Mp] at shared address `part` in
-// their own shared memory. Each CTA's epilogue warps (t = 0..127) sum, in
-// k (= cluster rank) order over distributed shared memory, the 32-row blocks
-// b of the unit with b mod S == rank (rotate-half pair blocks for RoPE) and
-// apply the epilogue — the fix-up pass without a launch or a global round trip.
-template <int MODE>
+// their own shared memory (part_off layout). All 8 warps of each CTA (t =
+// 0..255) sum, in k (= cluster rank) order over distributed shared memory,
+// the 32-row blocks b of the unit with b mod S == rank (rotate-half pair
+// blocks for RoPE) and apply the epilogue — the fix-up pass without a launch
+// or a global round trip. An item is (block, 4 batch rows), lanes = 32
+// consecutive rows (the folded-norm producer's warp sums need that); a thread
+// issues the remote loads of UC items before any add, so one DSMEM round trip
+// covers UC x S loads (serial per-item round trips made the 64-row reduce
+// longer than the GEMM).
+template <int MODE, bool kWide>
 __device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcEpilogue& ep, int unit, int rank,
                                                uint32_t part, const float* row_scale, int t) {
   constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  constexpr int kMaxS = 4, kWarps = kThreads / 32;
+  constexpr int UC = MODE == (int)Epi::kRopeKV || NB == 2 ? 2 : 4;  // items per batch (~64 registers of loads)
   const int S = args.csplit, Mp = args.Mp, quads = Mp / 4;
   const int warp = t >> 5, lane = t & 31;
-  if constexpr (MODE == (int)Epi::kRopeKV) {
-    // pairs j in [0, 64): columns (unit*128 + (j / half) * hd + j % half, + half)
-    const int hd = ep.kv.head_dim, half = hd / 2;
+  constexpr int kBlocks = MODE == (int)Epi::kRopeKV ? 2 : kRows / 32;
+  const int nblk = (kBlocks - rank + S - 1) / S;  // blocks rank, rank + S, ...
+  const int n_items = nblk * quads;
+  auto add4 = [](float4& a, const float4& b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  };
+  if constexpr (!kWide) {
+    // <= 16 batch rows (at most 2 items per epilogue warp): the 4 epilogue
+    // warps, one DSMEM load at a time. A separate kernel instantiation: with
+    // the batched form below compiled into the same kernel, the decode step
+    // at B = 1 measured 3.34 -> 3.41 ms even where that code never ran.
+    if (t < 128) return;
+    const int ew = warp - 4;
     int w = 0;
-    for (int blk = rank; blk < 2; blk += S)
+    for (int blk = rank; blk < kBlocks; blk += S)
       for (int q4 = 0; q4 < quads; ++q4, ++w) {
-        if ((w & 3) != warp) continue;
-        const int j = blk * 32 + lane;
-        const int ia = (j / half) * hd + j % half, ib = ia + half;
-        float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
-        for (int c = 0; c < S; ++c) {
-          const float4 a = ld_dsmem_v4(part + (uint32_t)(((ia * Mp) + q4 * 4) * 4), c);
-          const float4 b = ld_dsmem_v4(part + (uint32_t)(((ib * Mp) + q4 * 4) * 4), c);
-          sa.x += a.x; sa.y += a.y; sa.z += a.z; sa.w += a.w;
-          sb.x += b.x; sb.y += b.y; sb.z += b.z; sb.w += b.w;
+        if ((w & 3) != ew) continue;
+        if constexpr (MODE == (int)Epi::kRopeKV) {
+          const int hd = ep.kv.head_dim, half = hd / 2;
+          const int j = blk * 32 + lane;
+          const int ia = (j / half) * hd + j % half, ib = ia + half;
+          float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
+          for (int c = 0; c < S; ++c) {
+            add4(sa, ld_dsmem_v4(part + part_off(ia, q4, Mp), c));
+            add4(sb, ld_dsmem_v4(part + part_off(ib, q4, Mp), c));
+          }
+          float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
+          rope_store(args, ep, unit * kRows + ia, q4, va, vb, row_scale);
+        } else {
+          const int i = blk * 32 + lane;
+          float4 sum[NB];
+#pragma unroll
+          for (int jb = 0; jb < NB; ++jb) sum[jb] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int c = 0; c < S; ++c)
+#pragma unroll
+            for (int jb = 0; jb < NB; ++jb) add4(sum[jb], ld_dsmem_v4(part + part_off(jb * kRows + i, q4, Mp), c));
+          fixup_store<MODE>(args, ep, unit, i, q4, sum, row_scale);
         }
+      }
+    return;
+  } else {
+  for (int w0 = warp; w0 < n_items; w0 += UC * kWarps) {
+    if constexpr (MODE == (int)Epi::kRopeKV) {
+      // pairs j in [0, 64): columns (unit*128 + (j / half) * hd + j % half, + half)
+      const int hd = ep.kv.head_dim, half = hd / 2;
+      float4 pa[UC][kMaxS], pb[UC][kMaxS];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int w = w0 + u * kWarps;
+        if (w >= n_items) break;
+        const int j = (rank + (w / quads) * S) * 32 + lane, q4 = w % quads;
+        const int ia = (j / half) * hd + j % half, ib = ia + half;
+#pragma unroll
+        for (int c = 0; c < kMaxS; ++c)
+          if (c < S) {
+            pa[u][c] = ld_dsmem_v4(part + part_off(ia, q4, Mp), c);
+            pb[u][c] = ld_dsmem_v4(part + part_off(ib, q4, Mp), c);
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int w = w0 + u * kWarps;
+        if (w >= n_items) break;
+        const int j = (rank + (w / quads) * S) * 32 + lane, q4 = w % quads;
+        const int ia = (j / half) * hd + j % half;
+        float4 sa = pa[u][0], sb = pb[u][0];
+#pragma unroll
+        for (int c = 1; c < kMaxS; ++c)
+          if (c < S) {
+            add4(sa, pa[u][c]);
+            add4(sb, pb[u][c]);
+          }
         float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
         rope_store(args, ep, unit * kRows + ia, q4, va, vb, row_scale);
       }
-  } else {
-    int w = 0;
-    for (int blk = rank; blk < kRows / 32; blk += S)
-      for (int q4 = 0; q4 < quads; ++q4, ++w) {
-        if ((w & 3) != warp) continue;
-        const int i = blk * 32 + lane;
+    } else {
+      float4 p[UC][kMaxS][NB];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int w = w0 + u * kWarps;
+        if (w >= n_items) break;
+        const int i = (rank + (w / quads) * S) * 32 + lane, q4 = w % quads;
+#pragma unroll
+        for (int c = 0; c < kMaxS; ++c)
+          if (c < S)
+#pragma unroll
+            for (int jb = 0; jb < NB; ++jb) p[u][c][jb] = ld_dsmem_v4(part + part_off(jb * kRows + i, q4, Mp), c);
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int w = w0 + u * kWarps;
+        if (w >= n_items) break;
+        const int i = (rank + (w / quads) * S) * 32 + lane, q4 = w % quads;
         float4 sum[NB];
 #pragma unroll
-        for (int jb = 0; jb < NB; ++jb) sum[jb] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int c = 0; c < S; ++c)
+        for (int jb = 0; jb < NB; ++jb) sum[jb] = p[u][0][jb];
 #pragma unroll
-          for (int jb = 0; jb < NB; ++jb) {
-            const float4 a = ld_dsmem_v4(part + (uint32_t)((((jb * kRows + i) * Mp) + q4 * 4) * 4), c);
-            sum[jb].x += a.x; sum[jb].y += a.y; sum[jb].z += a.z; sum[jb].w += a.w;
-          }
+        for (int c = 1; c < kMaxS; ++c)
+          if (c < S)
+#pragma unroll
+            for (int jb = 0; jb < NB; ++jb) add4(sum[jb], p[u][c][jb]);
         fixup_store<MODE>(args, ep, unit, i, q4, sum, row_scale);
       }
+    }
   }
+}  // kWide
 }
 
-template <int MODE>
+template <int MODE, bool kWide = false>  // kWide: cluster reduce for > 16 batch rows
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ SkinnyArgs args, const __grid_constant__ TcEpilogue ep) {
@@ -466,8 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 4; ++q) {
               const float4 o = make_float4(__uint_as_float(v[j][4 * q]), __uint_as_float(v[j][4 * q + 1]),
                                            __uint_as_float(v[j][4 * q + 2]), __uint_as_float(v[j][4 * q + 3]));
-              if (cs > 1)
-                dst[q] = o;
+              if (cs > 1)  // swizzled shared-memory slot (part_off)
+                *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(mine) + part_off(j * kRows + i, c / 4 + q, Mp)) = o;
               else
                 __stcg(dst + q, o);
             }
@@ -490,9 +576,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
   if (cs > 1) {
     cluster_sync();  // every k-slice's partial is in its CTA's shared memory
-    if (warp >= 4) {
+    {  // every warp: the producer / MMA / allocator warps are idle by now
       const float* s_row = reinterpret_cast<const float*>(smem_raw + (bars + 8 * (2 * S + 6) - raw));
-      cluster_reduce<MODE>(args, ep, blockIdx.x / cs, blockIdx.x % cs, base, s_row, threadIdx.x - 128);
+      cluster_reduce<MODE, kWide>(args, ep, blockIdx.x / cs, blockIdx.x % cs, base, s_row, threadIdx.x);
     }
     cluster_sync();  // no CTA leaves while its partial may still be read
   }
@@ -671,18 +757,22 @@ int max_clusters(int S, int smem) {
 template <int MODE>
 void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs& a, int grid, int smem,
                  const TcEpilogue& e, cudaStream_t st) {
-  static int attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(gemm_skinny_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
+  // the opt-in shared-memory size only ever rises (a lower value set later
+  // would make an earlier, larger configuration fail to launch)
+  const bool wide = a.csplit > 1 && a.Mp > 16;
+  auto kern = wide ? gemm_skinny_kernel<MODE, true> : gemm_skinny_kernel<MODE, false>;
+  static int attr[2] = {0, 0};
+  if (smem > attr[wide]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr[wide] = smem;
   }
   count_launch();
   if (a.csplit > 1) {  // cluster split-K: the reduction runs inside the GEMM, no fix-up launch
-    static bool np = false;
-    if (!np) {
-      cudaFuncSetAttribute(gemm_skinny_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    static bool np[2] = {false, false};
+    if (!np[wide]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaGetLastError();
-      np = true;
+      np[wide] = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -701,7 +791,7 @@ void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs&
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
-    cudaLaunchKernelEx(&cfg, gemm_skinny_kernel<MODE>, mw, ma, a, e);
+    cudaLaunchKernelEx(&cfg, kern, mw, ma, a, e);
     return;
   }
   launch_pdl(gemm_skinny_kernel<MODE>, dim3(grid), dim3(kThreads), (size_t)smem, st, mw, ma, a, e);
@@ -784,17 +874,30 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // WS_SKINNY_CLUSTER=0: stream-K + fix-up (A/B).
   static const bool cl_on = !(getenv("WS_SKINNY_CLUSTER") && getenv("WS_SKINNY_CLUSTER")[0] == '0');
   a.csplit = 0;
-  // up to 32 batch rows (B = 32: 4.57 -> 4.54 ms; B = 64 neutral to 0.5% slower)
-  static const int cl_mp = getenv("WS_SKINNY_CLUSTER_MP") ? atoi(getenv("WS_SKINNY_CLUSTER_MP")) : 32;
+  // Above 32 batch rows the fp32 partials the stream-K fix-up moves through
+  // L2 grow with the rows; the cluster form wins where they are large next
+  // to the weights and the clusters still cover >= 120 SMs (same-box per-GEMM
+  // A/B, us, cluster vs stream-K + fix-up): SwiGLU up to 128 rows (Phi-3
+  // gate/up as 64 pairs: 24 vs 36 at 64 rows, 29 vs 46 at 128), other
+  // epilogues up to 64 rows in clusters of 4 (Llama-3-8B O / down: 14.6 /
+  // 30.9 vs 15.5 / 31.8; decode B = 64 5.77 -> 5.66 ms) but not in pairs
+  // (Phi-3 QKV as 72 pairs: 19.3 vs 17.4) nor above 64 rows (Llama down at
+  // 128 rows: 39.4 vs 36.2).
+  static const int cl_mp = getenv("WS_SKINNY_CLUSTER_MP") ? atoi(getenv("WS_SKINNY_CLUSTER_MP")) : 128;
+  const bool swiglu = e.mode == Epi::kSwiGLU;
   if (cl_on && grid != units && a.Mp <= cl_mp)
     for (int S_ = 4; S_ >= 2; --S_)
       // every cluster resident at once (clusters are placed within a GPC: 48
       // clusters of 3 did not fit in one wave and ran the QKV GEMM at half speed)
       if (units * S_ <= kNumSMs && kbs >= 2 * S_ && units <= max_clusters(S_, smem)) {
+        if (a.Mp > 32 && (units * S_ < 120 || (!swiglu && (S_ < 4 || a.Mp > 64)))) break;
         a.csplit = S_;
         grid = units * S_;
         break;
       }
+  static const bool dbg = getenv("WS_SKINNY_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "[skinny] M=%d N=%d K=%d mode=%d units=%d kbs=%d grid=%d cluster=%d\n", M, N, K, (int)e.mode,
+                   units, kbs, grid, a.csplit);
   if (e.mode == Epi::kRopeKV && units > grid) return false;  // <= 2 segments (partial slots) per CTA
   Scratch s;
   if (!scratch_for(st, &s)) return false;
@@ -808,6 +911,10 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
     case Epi::kStoreF32: launch_mode<3>(mw, ma, a, grid, smem, e, st); break;
     case Epi::kSwiGLU: launch_mode<4>(mw, ma, a, grid, smem, e, st); break;
     case Epi::kRopeKV: launch_mode<5>(mw, ma, a, grid, smem, e, st); break;
+  }
+  if (dbg) {
+    const cudaError_t err = cudaPeekAtLastError();
+    if (err != cudaSuccess) fprintf(stderr, "[skinny] launch failed: %s (smem %d)\n", cudaGetErrorString(err), smem);
   }
   return true;
 }

@@ -162,7 +162,8 @@ bool qkv_rope(const ws_model* m, const ws::bf16* h, const ws::bf16* w, const ws:
     // a few decode rows: skinny split-K GEMM with RoPE/KV-append in its fix-up
     // (one launch less; for more rows the plain fix-up + rope kernel is faster)
     static const bool fuse = !(getenv("WS_FUSE_ROPE") && getenv("WS_FUSE_ROPE")[0] == '0');
-    if (fuse && rows <= 8 && launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return true;
+    static const int fuse_rows = getenv("WS_FUSE_ROPE_ROWS") ? atoi(getenv("WS_FUSE_ROPE_ROWS")) : 8;
+    if (fuse && rows <= fuse_rows && launch_gemm_skinny(h, w, rows, q, c.hidden, e, st)) return true;
     if (norm) {  // folded RMSNorm: the skinny GEMM applies the row scales, then RoPE / KV append
       e.mode = b ? Epi::kBiasBf16 : Epi::kStoreBf16;
       e.C = qkv;

@@ -122,10 +122,11 @@ def replay_gpu(trace: dict, policy: str, gid: int, device: int, images: HostImag
                     w.wait_resident(name)
                     del prewarm_t[name]
 
-        def timed(kind, fn):
+        def timed(kind, fn, sync=True):
             t0 = time.perf_counter()
             r = fn()
-            torch.cuda.synchronize(device)
+            if sync:
+                torch.cuda.synchronize(device)
             out["op_us"].setdefault(kind, []).append((time.perf_counter() - t0) * 1e6)
             return r
 
@@ -152,7 +153,10 @@ def replay_gpu(trace: dict, policy: str, gid: int, device: int, images: HostImag
             settle(o["t"])
             op = o["op"]
             if op == "prewarm":
-                timed("prewarm_issue", lambda: w.prewarm(o["model"], layers=o["required"], full=True, wait=None))
+                # host cost of the call (slot + copy queueing): the copies land
+                # in the background, as the engine's prewarm does
+                timed("prewarm_issue", lambda: w.prewarm(o["model"], layers=o["required"], full=True, wait=None),
+                      sync=False)
                 prewarm_t[o["model"]] = o["t"]
                 check(o)
             elif op == "evict":

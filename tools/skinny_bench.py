@@ -1,8 +1,8 @@
 """Decode-shaped (skinny) GEMMs back to back at M = 1, 16 and 64 for the
 8B QKV, O, gate/up (SwiGLU) and down shapes (impl 4): us per call and weight
-GB/s. Env WS_SKINNY_CLUSTER=0 / WS_SKINNY_CLUSTER_MAX=C for A/B.
+GB/s (--phi: the Phi-3-mini shapes). Env WS_SKINNY_CLUSTER=0 / WS_SKINNY_CLUSTER_MAX=C for A/B.
 
-    python tools/skinny_bench.py
+    python tools/skinny_bench.py [--phi] [M,M,...]
 """
 import ctypes as C
 import json
@@ -15,8 +15,11 @@ from paper_2512_09472_b200 import _native as N  # noqa: E402
 from paper_2512_09472_b200 import models  # noqa: E402,F401  (registers ws_gemm)
 
 SHAPES = {"qkv": (6144, 4096, 2), "o": (4096, 4096, 2), "gateup": (28672, 4096, 4), "down": (4096, 14336, 2)}
+if "--phi" in sys.argv:  # Phi-3-mini
+    SHAPES = {"qkv": (9216, 3072, 2), "o": (3072, 3072, 2), "gateup": (16384, 3072, 4), "down": (3072, 8192, 2)}
 out = {}
-for M in (1, 16, 64):
+MS = [int(x) for x in next((a for a in sys.argv[1:] if a[0].isdigit()), "1,16,64").split(",")]
+for M in MS:
     for name, (n, k, epi) in SHAPES.items():
         A = torch.randn(M, k, device="cuda").bfloat16()
         B = (torch.randn(n, k, device="cuda") * 0.02).bfloat16()
