@@ -8,6 +8,12 @@ namespace ws {
 namespace dev {
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+// silu(x) = x * sigmoid(x) with the fast division (2 ulp). IEEE `x / (1 + e)`
+// leaves its fast path for a zero numerator among others, and zero
+// accumulators are common (padded batch rows, rows past M): the pair SwiGLU
+// GEMM at 256 x 28672 x 4096 took 80 us with one zero row of A, 60 us with
+// none, 55 us with this form; decode B = 1 3.31 -> 3.27 ms.
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 __device__ __forceinline__ __nv_bfloat16 f2bf(float v) { return __float2bfloat16_rn(v); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const bf16* __restrict__ 
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     float2 gv = unpack_bf16x2(gp[k]), uv = unpack_bf16x2(up[k]);
-    float s0 = gv.x / (1.f + __expf(-gv.x)), s1 = gv.y / (1.f + __expf(-gv.y));
+    float s0 = silu(gv.x), s1 = silu(gv.y);
     op[k] = pack_bf16x2(s0 * uv.x, s1 * uv.y);
   }
   reinterpret_cast<uint4*>(act + (int64_t)r * ffn)[i] = o;

@@ -136,7 +136,7 @@ __device__ __forceinline__ void fixup_store(const SkinnyArgs& args, const TcEpil
   }
   if constexpr (NB == 2) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = v[k] / (1.f + __expf(-v[k])) * u[k];
+    for (int k = 0; k < 4; ++k) v[k] = silu(v[k]) * u[k];
   }
   const int row = unit * kRows + i;
   if (row >= (MODE == (int)Epi::kSwiGLU ? args.N / 2 : args.N)) return;  // ragged last unit
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int q = 0; q < 16; ++q) {
             const float sc = ep.norm_role == 2 ? (c + q < args.M ? s_row[c + q] : 0.f) : 1.f;
             f[q] = __uint_as_float(v[0][q]) * sc;
-            if constexpr (NB == 2) f[q] = f[q] / (1.f + __expf(-f[q])) * (__uint_as_float(v[NB - 1][q]) * sc);
+            if constexpr (NB == 2) f[q] = silu(f[q]) * (__uint_as_float(v[NB - 1][q]) * sc);
           }
           store_out<MODE>(ep, args, out_row, f, c);
         } else {

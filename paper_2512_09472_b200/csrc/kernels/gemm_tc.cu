@@ -140,7 +140,7 @@ __device__ __forceinline__ void epilogue_tile(const TcEpilogue& ep, uint32_t tac
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float x = __uint_as_float(g[j]);
-        f[j] = x / (1.f + __expf(-x)) * __uint_as_float(u[j]);
+        f[j] = silu(x) * __uint_as_float(u[j]);
       }
       store_bf16x32(out + c * 32, f);
     }
@@ -482,7 +482,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const TcEpilogue& ep, const CU
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float x = __uint_as_float(g[j]);
-          f[j] = x / (1.f + __expf(-x)) * __uint_as_float(u[j]);
+          f[j] = silu(x) * __uint_as_float(u[j]);
         }
         stage_bf16(buf, lane, h, f);
       }
@@ -1049,7 +1049,11 @@ bool use_pair(int M) {
     const char* v = getenv("WS_GEMM_PAIR");
     g_pair_mode = (v && v[0] == '0') ? 0 : 1;
   }
-  return g_pair_mode == 1 && M >= 256;
+  // From 129 rows (the skinny kernel serves <= 128): one 256-row pair tile
+  // streams the weights once where two 128-row tiles of the 1-CTA kernel
+  // stream them twice (192-token prefill 8.6 -> see DESIGN §5).
+  static const int min_m = getenv("WS_PAIR_MIN_M") ? atoi(getenv("WS_PAIR_MIN_M")) : 129;
+  return g_pair_mode == 1 && M >= min_m;
 }
 
 bool gemm_tc_pair_enabled(int M) { return use_pair(M); }

@@ -1,7 +1,8 @@
 """Time the prefill GEMM shapes on the tcgen05 pair kernel (impl 3) with CUDA
 events: back-to-back launches of one shape, TFLOP/s per shape.
 
-    python tools/gemm_bench.py [--m 2048] [--reps 20]   (WS_STREAMK=0 to A/B)
+    python tools/gemm_bench.py [--m 2048] [--reps 20] [--only gate_up,o] [--zero-rows=a:b] [--const-rows=a:b]
+      (WS_STREAMK=0 to A/B; --zero-rows probes data-dependent epilogue cost)
 """
 
 from __future__ import annotations
@@ -25,14 +26,21 @@ def main():
     ap.add_argument("--m", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--only", default="")
-    a = ap.parse_args()
+    a, _ = ap.parse_known_args()
     M = a.m
     shapes = {"qkv": (6144, 4096, 5), "o": (4096, 4096, 2), "gate_up": (28672, 4096, 4), "down": (4096, 14336, 2)}
     out = {}
     for name, (n, k, epi) in shapes.items():
         if a.only and name not in a.only.split(","):
             continue
-        A = torch.randn(M, k, device="cuda").bfloat16()
+        A = torch.randn((M + 255) // 256 * 256, k, device="cuda").bfloat16()  # rows past M: --zero-rows probes
+        for arg in sys.argv:  # --zero-rows=a:b  zero rows [a, b) of A (data-dependence probe)
+            if arg.startswith("--zero-rows="):
+                a0, a1 = map(int, arg.split("=")[1].split(":"))
+                A[a0:a1] = 0
+            if arg.startswith("--const-rows="):
+                a0, a1 = map(int, arg.split("=")[1].split(":"))
+                A[a0:a1] = 0.01
         B = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
         if epi == 2:
             Cm = torch.zeros(M, n, device="cuda")

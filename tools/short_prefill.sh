@@ -1,9 +1,7 @@
 #!/bin/bash
-# Launch lists of short-prompt prefills under two skinny plans.
-for v in "X=0" "WS_SKINNY_CLUSTER_MP=64"; do
-  for spec in "phi3-mini 64" "llama3-8b 64"; do
-    set -- $spec
-    env $v timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pre_$1_$2_${v%%=*}.csv \
-      python tools/prefill_profile.py --model $1 --tokens $2 --iters 2 > /dev/null 2>&1
-  done
+for t in 255 256; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pre_l_$t.csv \
+    python tools/prefill_profile.py --tokens $t --iters 2 > /dev/null 2>&1
+  echo "== $t"; python tools/summarize_launches.py gpurun_out/pre_l_$t.csv | head -6
+  echo -n "live: "; python tools/prefill_profile.py --tokens $t --iters 8 | tail -1
 done
