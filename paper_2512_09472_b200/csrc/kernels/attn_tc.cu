@@ -1083,6 +1083,24 @@ extern "C" int ws_attn_cta_trace(long long* out) {
 }
 #endif
 
+bool attn_prefill_tc_paired(const KvGeom& kv, int heads) {
+  static const bool pair_heads = !(getenv("WS_ATTN_PAIR") && getenv("WS_ATTN_PAIR")[0] == '0');
+  const int hd = kv.head_dim;
+  return (hd == 128 || hd == 64) && kv.tpb % 16 == 0 && kv.page_size % (hd * 2) == 0 && pair_heads &&
+         (heads / kv.kv_heads) % 2 == 0;
+}
+
+// Warm prefill, same box, whole prompt, ms, tcgen05 -> mma.sync attention:
+// Llama-3-8B 64 / 128 / 256 / 384 tokens 4.48 / 5.17 / 7.18 / 8.24 -> 4.35 /
+// 4.89 / 7.02 / 8.26 (paired heads); Phi-3-mini 64 / 128: 3.63 / 4.34 ->
+// 3.49 / 4.34 (head_dim 96, one head per CTA), Qwen2.5-7B 64 / 256: 4.17 /
+// 6.52 -> 4.11 / 6.50 (odd group). WS_ATTN_SHORT_MMA=0 keeps the tcgen05
+// kernels for every length.
+bool attn_prefill_prefers_mma(const KvGeom& kv, int rows, int heads) {
+  static const bool on = !(getenv("WS_ATTN_SHORT_MMA") && getenv("WS_ATTN_SHORT_MMA")[0] == '0');
+  return on && rows <= (attn_prefill_tc_paired(kv, heads) ? 256 : 64);
+}
+
 bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows,
                             int pos0, int heads, float scale, cudaStream_t st) {
   if (kv.head_dim == 128 || kv.head_dim == 96)  // 96 runs in zero-padded 128-wide tiles

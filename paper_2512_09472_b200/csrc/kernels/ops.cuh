@@ -51,6 +51,12 @@ void launch_attn_prefill(const bf16* qkv, bf16* out, const KvGeom& kv, int layer
 // returns false (nothing launched) for other head dims.
 bool launch_attn_prefill_tc(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, int seq, int rows,
                             int pos0, int heads, float scale, cudaStream_t st);
+// Whether launch_attn_prefill_tc runs the paired-head kernel for this shape
+// (even GQA group, TMA-addressable blocks), and whether a prompt of `rows`
+// queries is better served by launch_attn_prefill: a short prompt gives the
+// tcgen05 kernels a few long serial tile chains on a few dozen SMs.
+bool attn_prefill_tc_paired(const KvGeom& kv, int heads);
+bool attn_prefill_prefers_mma(const KvGeom& kv, int rows, int heads);
 
 // One query token per sequence: seqs[i] at position pos[i] (context pos+1,
 // its own K/V already appended). scratch: decode_scratch_floats() floats.

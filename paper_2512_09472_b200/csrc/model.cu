@@ -424,7 +424,7 @@ int ws_model_prefill(ws_model* m, ws_pool* pool, const void* wts, int32_t seq,
     const int r0 = m->prune_last && l + 1 == c.layers ? rows - 1 : 0, n = rows - r0;
     const bf16* q_rows = qkv + (int64_t)r0 * q;
     float* x_rows = x + (int64_t)r0 * d;
-    if (m->gemm_impl & 2) {
+    if ((m->gemm_impl & 2) || attn_prefill_prefers_mma(kv, n, c.heads)) {
       launch_attn_prefill(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st);
     } else if (!launch_attn_prefill_tc(q_rows, attn, kv, l, seq, n, pos0 + r0, c.heads, scale, st)) {
       count_fallback(kFallbackAttnMma, "prefill attention shape outside attn_tc (head_dim / GQA) runs mma.sync");
