@@ -477,11 +477,14 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
   // eps) — two launches fewer per layer. Graph-replayed 8B steps, ctx 1024:
   // B = 1 / 4 / 16 3.96 / 4.12 / 4.31 -> 3.79 / 4.05 / 4.23 ms; no gain at
   // B = 32 and 0.6% slower at B = 64 (the load-add-store residual and the
-  // wider fix-up epilogues cost what the launches saved), so up to 16 rows. Off for TP (the
+  // wider fix-up epilogues cost what the launches saved), so up to 16 rows at first. Off for TP (the
   // residual is summed across ranks first), the legacy GEMMs, shapes outside
   // the skinny kernel, and WS_FOLD_NORM=0 (A/B).
   static const bool fold_env = !(getenv("WS_FOLD_NORM") && getenv("WS_FOLD_NORM")[0] == '0');
-  const bool fold = fold_env && n <= 16 && !m->comm && !(m->gemm_impl & 1) &&
+  // since the cluster reduce serves 17-32 rows too, up to 32 (B = 17 / 32
+  // 4.08 / 4.38 -> 4.03 / 4.31 ms; B = 48 / 64 still 1.2% / 0.2% slower)
+  static const int fold_rows = getenv("WS_FOLD_ROWS") ? atoi(getenv("WS_FOLD_ROWS")) : 32;
+  const bool fold = fold_env && n <= fold_rows && !m->comm && !(m->gemm_impl & 1) &&
                     gemm_skinny_supported(n, d, o, Epi::kAddF32) &&
                     gemm_skinny_supported(n, d, c.ffn, Epi::kAddF32) &&
                     gemm_skinny_supported(n, q, d, Epi::kStoreBf16) &&
