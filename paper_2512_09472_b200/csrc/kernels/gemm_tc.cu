@@ -964,23 +964,35 @@ void launch_mode(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int
 // Tail slicing for residual GEMMs (see TailSched): the slice count with the
 // shortest tail, only when every slice keeps >= 48 k-blocks (long enough to
 // hide the slice's reduce-add epilogue behind the next slice's mainloop).
-TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks, cudaStream_t st) {
+TailSched tail_schedule(int mode, int tiles, int& n_pairs, int k_blocks, cudaStream_t st) {
   TailSched p{};
   p.dp_tiles = tiles;
   p.slices = 1;
   static const bool on = !(getenv("WS_TAIL_SLICES") && getenv("WS_TAIL_SLICES")[0] == '0');
-  if (!on || mode != (int)Epi::kAddF32 || tiles <= n_pairs || tiles % n_pairs == 0) return p;
-  const int dp = tiles / n_pairs * n_pairs, tail = tiles - dp;
-  double best = 1.0;  // tail time in whole-tile units without slicing
-  int best_s = 1;
-  for (int s = 2; s <= 4 && k_blocks / s >= 48; ++s) {
-    const double t = (double)((tail * s + n_pairs - 1) / n_pairs) / s;
-    if (t < best - 0.01) {
-      best = t;
-      best_s = s;
+  if (!on || mode != (int)Epi::kAddF32) return p;
+  int dp, best_s = 1;
+  if (tiles < kNumSMs / 2) {
+    // Less than one wave (O / down below ~1k prompt rows: 16 x 256-column
+    // tiles per 256 rows): k-slice every tile so the pairs cover the GPU;
+    // the slices reduce-add in k order. Llama-3-8B at 256 rows: O on 16
+    // pairs of 74 read 33.5 MB in 26 us, down 117 MB in 70 us.
+    dp = 0;
+    best_s = std::min(8, (kNumSMs / 2) / tiles);
+    while (best_s > 1 && k_blocks / best_s < 16) --best_s;
+  } else {
+    if (tiles <= n_pairs || tiles % n_pairs == 0) return p;
+    dp = tiles / n_pairs * n_pairs;
+    const int tail = tiles - dp;
+    double best = 1.0;  // tail time in whole-tile units without slicing
+    for (int s = 2; s <= 4 && k_blocks / s >= 48; ++s) {
+      const double t = (double)((tail * s + n_pairs - 1) / n_pairs) / s;
+      if (t < best - 0.01) {
+        best = t;
+        best_s = s;
+      }
     }
   }
-  if (best_s == 1 || tail > 4096) return p;
+  if (best_s == 1 || tiles - dp > 4096) return p;
   // one flag array per (device, stream): launches on a stream are ordered, so
   // they can share it; concurrent streams must not (a waiter compares for equality)
   struct Flags {
@@ -1005,6 +1017,7 @@ TailSched tail_schedule(int mode, int tiles, int n_pairs, int k_blocks, cudaStre
   p.slices = best_s;
   p.flags = fl.f;
   p.epoch = fl.epoch;
+  if (dp == 0) n_pairs = std::min(tiles * best_s, kNumSMs / 2);
   return p;
 }
 
@@ -1017,7 +1030,7 @@ bool launch_mode2(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, in
     attr = true;
   }
   const int tiles = ((M + 255) / 256) * (N / P_BN);
-  const int n_pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+  int n_pairs = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;  // raised by tail_schedule when it k-slices
   CUtensorMap mc = ma;  // RoPE mode stores directly; the map is unused there
   if constexpr (MODE == (int)Epi::kAddF32 || MODE == (int)Epi::kStoreF32) {
     if (!make_out_map(&mc, e.C, M, N, 4)) return false;
