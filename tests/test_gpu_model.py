@@ -87,6 +87,38 @@ def test_gemm_tcgen05_against_fp32(lib, M, N, K):
         assert _rel(out.float(), want) < tol, (epi, _rel(out.float(), want))
 
 
+@pytest.mark.parametrize("M,K", [(129, 4096), (256, 4096), (300, 14336), (777, 4096)])
+def test_gemm_pair_ksliced_residual(lib, M, K):
+    """Residual (x += A.W^T) GEMMs below one wave of CTA pairs k-slice every
+    256x256 tile (<= 8 slices reduce-added in k order, flag-ordered): matches
+    fp32 and reruns are bit-identical. The SwiGLU epilogue on the same rows,
+    with an all-zero row of A (padded rows take the fast division)."""
+    import ctypes as C
+
+    N = 4096
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    A[M // 2] = 0
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    x0 = torch.randn(M, N, device="cuda", generator=g)
+    want = x0 + A.float() @ B.float().T
+    outs = []
+    for _ in range(2):
+        x = x0.clone()
+        lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 2,
+                 C.c_void_p(x.data_ptr()), None, 3, None)
+        torch.cuda.synchronize()
+        outs.append(x)
+    assert _rel(outs[0], want) < 1e-5
+    assert torch.equal(outs[0], outs[1])
+    act = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    lib.call("ws_gemm", C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K, 4,
+             C.c_void_p(act.data_ptr()), None, 3, None)
+    torch.cuda.synchronize()
+    assert _rel(act.float(), _swiglu_ref(A, B)) < 1e-2
+    assert not act[M // 2].float().abs().any()
+
+
 @pytest.mark.parametrize("M", [1, 3, 8, 16])
 def test_gemv_against_fp32(lib, M):
     import ctypes as C
