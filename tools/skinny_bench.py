@@ -2,7 +2,7 @@
 8B QKV, O, gate/up (SwiGLU) and down shapes (impl 4): us per call and weight
 GB/s (--phi: the Phi-3-mini shapes). Env WS_SKINNY_CLUSTER=0 / WS_SKINNY_CLUSTER_MAX=C for A/B.
 
-    python tools/skinny_bench.py [--phi] [M,M,...]
+    python tools/skinny_bench.py [--phi] [M,M,...] [--only=qkv,o,gateup,down]
 """
 import ctypes as C
 import json
@@ -19,8 +19,11 @@ if "--phi" in sys.argv:  # Phi-3-mini
     SHAPES = {"qkv": (9216, 3072, 2), "o": (3072, 3072, 2), "gateup": (16384, 3072, 4), "down": (3072, 8192, 2)}
 out = {}
 MS = [int(x) for x in next((a for a in sys.argv[1:] if a[0].isdigit()), "1,16,64").split(",")]
+ONLY = next((a.split("=")[1].split(",") for a in sys.argv[1:] if a.startswith("--only=")), None)
 for M in MS:
     for name, (n, k, epi) in SHAPES.items():
+        if ONLY and name not in ONLY:
+            continue
         A = torch.randn(M, k, device="cuda").bfloat16()
         B = (torch.randn(n, k, device="cuda") * 0.02).bfloat16()
         Cm = torch.zeros(M, n // 2, device="cuda", dtype=torch.bfloat16) if epi == 4 else torch.zeros(M, n, device="cuda")
