@@ -45,6 +45,7 @@ using namespace dev;
 constexpr int kRows = 128, kBox = 64, kThreads = 256;
 constexpr int kW_BYTES = kRows * kBox * 2;  // 16 KiB weight box (128 rows x 128 B, SW128)
 constexpr int kSmemBudget = 216 * 1024;     // TMA ring, one CTA per SM
+constexpr int kMaxSmem = 227 * 1024;        // opt-in dynamic shared memory per CTA
 
 // An iteration covers sub (1, 2 or 4) boxes of 64 k-columns: the producer
 // fetches sub x 128 contiguous bytes of every weight row per issue.
@@ -140,16 +141,33 @@ __device__ __forceinline__ void fixup_store(const SkinnyArgs& args, const TcEpil
   }
   const int row = unit * kRows + i;
   if (row >= (MODE == (int)Epi::kSwiGLU ? args.N / 2 : args.N)) return;  // ragged last unit
+  if constexpr (MODE == (int)Epi::kAddF32) {
+    // every load before any store: one L2 round trip for the 4 batch rows
+    // (and the norm weight), not one per row behind the previous row's stores
+    float* x = static_cast<float*>(ep.C) + row;
+    float old[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) old[k] = q4 * 4 + k < args.M ? x[(int64_t)(q4 * 4 + k) * args.N] : 0.f;
+    const float g = ep.norm_role == 1 ? bf2f(ep.norm_g[row]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int b = q4 * 4 + k;
+      if (b >= args.M) break;
+      const float x_new = old[k] + v[k];
+      x[(int64_t)b * args.N] = x_new;
+      if (ep.norm_role == 1) {  // folded RMSNorm producer (see norm_produce)
+        ep.norm_out[(int64_t)b * args.N + row] = f2bf(x_new * g);
+        const float sq = warp_sum(x_new * x_new);
+        if ((threadIdx.x & 31) == 0) ep.row_ss[(int64_t)b * (args.N / 32) + row / 32] = sq;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int b = q4 * 4 + k;
     if (b >= args.M) break;
     if constexpr (MODE == (int)Epi::kAddF32) {
-      float* dst = static_cast<float*>(ep.C) + (int64_t)b * args.N + row;
-      if (ep.norm_role == 1)
-        norm_produce(ep, args.N, b, row, *dst + v[k], dst);
-      else
-        *dst += v[k];
     } else if constexpr (MODE == (int)Epi::kStoreF32) {
       static_cast<float*>(ep.C)[(int64_t)b * args.N + row] = v[k];
     } else if constexpr (MODE == (int)Epi::kSwiGLU) {
@@ -179,15 +197,29 @@ __device__ __forceinline__ void rope_store(const SkinnyArgs& args, const TcEpilo
   const float bias_a = ep.bias ? bf2f(ep.bias[col_a]) : 0.f, bias_b = ep.bias ? bf2f(ep.bias[col_b]) : 0.f;
   const int hs = col_a / hd;  // head slot in [0, H + 2KV)
   const bool is_v = hs >= ep.heads + kv.kv_heads, is_k = !is_v && hs >= ep.heads;
+  // loads of all 4 batch rows first (positions, then the rotations and pages
+  // they index), stores after: two L2 round trips, not two per row
+  int pos[4], page[4];
+  float2 cs[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = q4 * 4 + k;
+    pos[k] = b < args.M ? (ep.pos_arr ? ep.pos_arr[b] : ep.pos0 + b) : 0;
+    page[k] = b < args.M && (is_k || is_v) ? (ep.seq_arr ? ep.seq_arr[b] : ep.seq0) : 0;  // seq for now
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool ok = q4 * 4 + k < args.M;
+    cs[k] = ok && !is_v ? ep.rope[(int64_t)pos[k] * half + dd] : make_float2(1.f, 0.f);
+    page[k] = ok && (is_k || is_v) ? kv.block_tables[(int64_t)page[k] * kv.max_blocks + pos[k] / kv.tpb] : 0;
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int b = q4 * 4 + k;
     if (b >= args.M) break;
-    const int pos = ep.pos_arr ? ep.pos_arr[b] : ep.pos0 + b;
     float x = va[k] + bias_a, y = vb[k] + bias_b;
     if (!is_v) {
-      const float2 c = ep.rope[(int64_t)pos * half + dd];
-      const float rx = x * c.x - y * c.y, ry = y * c.x + x * c.y;
+      const float rx = x * cs[k].x - y * cs[k].y, ry = y * cs[k].x + x * cs[k].y;
       x = rx;
       y = ry;
     }
@@ -196,11 +228,9 @@ __device__ __forceinline__ void rope_store(const SkinnyArgs& args, const TcEpilo
       q[col_a] = f2bf(x);
       q[col_b] = f2bf(y);
     } else {
-      const int seq = ep.seq_arr ? ep.seq_arr[b] : ep.seq0;
-      const int32_t page = kv.block_tables[(int64_t)seq * kv.max_blocks + pos / kv.tpb];
       const int kvh = is_v ? hs - ep.heads - kv.kv_heads : hs - ep.heads;
-      bf16* dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page * kv.page_size) +
-                  kv.plane(ep.layer, is_v ? 1 : 0, kvh) + (int64_t)(pos % kv.tpb) * hd;
+      bf16* dst = reinterpret_cast<bf16*>(kv.window + (int64_t)page[k] * kv.page_size) +
+                  kv.plane(ep.layer, is_v ? 1 : 0, kvh) + (int64_t)(pos[k] % kv.tpb) * hd;
       dst[dd] = f2bf(x);
       dst[dd + half] = f2bf(y);
     }
@@ -231,6 +261,39 @@ __device__ __forceinline__ uint32_t part_off(int row, int q4, int Mp) {
   return (uint32_t)((row * Mp + ((q4 ^ (row & (group - 1))) << 2)) << 2);
 }
 
+__device__ __forceinline__ void st_dsmem_v4(uint32_t local, int cta, float4 v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(cta));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// Push form of the cluster split (<= 16 batch rows): block b of a unit's 128
+// rows (RoPE: rotate-half pair block b) is reduced by cluster rank b mod S.
+// Every CTA stores its partial rows straight into their owner's push region
+// ([source rank][owner-local row][NB][Mp], part_off swizzle) with remote
+// shared-memory stores, so after one cluster barrier each owner sums S local
+// copies — no DSMEM round trip per load and no second barrier (the pull form
+// spent ~1.6 us reducing and ~0.8 us in the closing barrier of an O GEMM
+// whose weights took 3.4 us to stream).
+__host__ __device__ constexpr int push_rows_per_owner(bool rope, int S) {
+  return rope ? (2 + S - 1) / S * 64 : (kRows / 32 + S - 1) / S * 32;
+}
+template <int MODE>
+__device__ __forceinline__ void push_slot(const TcEpilogue& ep, int i, int S, int& owner, int& local) {
+  if constexpr (MODE == (int)Epi::kRopeKV) {
+    const int hd = ep.kv.head_dim, half = hd / 2;
+    const int j = (i / hd) * half + (i % hd) % half, side = (i % hd) >= half ? 1 : 0, blk = j / 32;
+    owner = blk % S;
+    local = (blk / S) * 64 + (j % 32) * 2 + side;
+  } else {
+    const int b = i / 32;
+    owner = b % S;
+    local = (b / S) * 32 + (i % 32);
+  }
+}
+
 // Cluster split-K reduction: the S CTAs of a cluster computed k-slices of one
 // unit and left their fp32 partials [NB][128][Mp] at shared address `part` in
 // their own shared memory (part_off layout). All 8 warps of each CTA (t =
@@ -244,7 +307,7 @@ __device__ __forceinline__ uint32_t part_off(int row, int q4, int Mp) {
 // longer than the GEMM).
 template <int MODE, bool kWide>
 __device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcEpilogue& ep, int unit, int rank,
-                                               uint32_t part, const float* row_scale, int t) {
+                                               uint32_t part, const float* push_ptr, const float* row_scale, int t) {
   constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
   constexpr int kMaxS = 4, kWarps = kThreads / 32;
   constexpr int UC = MODE == (int)Epi::kRopeKV || NB == 2 ? 2 : 4;  // items per batch (~64 registers of loads)
@@ -263,6 +326,11 @@ __device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcE
     // at B = 1 measured 3.34 -> 3.41 ms even where that code never ran.
     if (t < 128) return;
     const int ew = warp - 4;
+    const int rpo = push_rows_per_owner(MODE == (int)Epi::kRopeKV, S);
+    auto at = [&](int c, int local, int jb, int q4) -> float4 {
+      return *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(push_ptr) +
+                                              part_off((c * rpo + local) * NB + jb, q4, Mp));
+    };
     int w = 0;
     for (int blk = rank; blk < kBlocks; blk += S)
       for (int q4 = 0; q4 < quads; ++q4, ++w) {
@@ -270,22 +338,23 @@ __device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcE
         if constexpr (MODE == (int)Epi::kRopeKV) {
           const int hd = ep.kv.head_dim, half = hd / 2;
           const int j = blk * 32 + lane;
-          const int ia = (j / half) * hd + j % half, ib = ia + half;
+          const int ia = (j / half) * hd + j % half;
+          const int la = (blk / S) * 64 + lane * 2;
           float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
           for (int c = 0; c < S; ++c) {
-            add4(sa, ld_dsmem_v4(part + part_off(ia, q4, Mp), c));
-            add4(sb, ld_dsmem_v4(part + part_off(ib, q4, Mp), c));
+            add4(sa, at(c, la, 0, q4));
+            add4(sb, at(c, la + 1, 0, q4));
           }
           float va[4] = {sa.x, sa.y, sa.z, sa.w}, vb[4] = {sb.x, sb.y, sb.z, sb.w};
           rope_store(args, ep, unit * kRows + ia, q4, va, vb, row_scale);
         } else {
-          const int i = blk * 32 + lane;
+          const int i = blk * 32 + lane, li = (blk / S) * 32 + lane;
           float4 sum[NB];
 #pragma unroll
           for (int jb = 0; jb < NB; ++jb) sum[jb] = make_float4(0.f, 0.f, 0.f, 0.f);
           for (int c = 0; c < S; ++c)
 #pragma unroll
-            for (int jb = 0; jb < NB; ++jb) add4(sum[jb], ld_dsmem_v4(part + part_off(jb * kRows + i, q4, Mp), c));
+            for (int jb = 0; jb < NB; ++jb) add4(sum[jb], at(c, li, jb, q4));
           fixup_store<MODE>(args, ep, unit, i, q4, sum, row_scale);
         }
       }
@@ -358,11 +427,31 @@ __device__ __forceinline__ void cluster_reduce(const SkinnyArgs& args, const TcE
 }  // kWide
 }
 
+// WS_SKINNY_TRACE build: per-CTA globaltimer timeline of the last launch
+// [cta][0 entry, 1 setup done, 2 producer past the PDL wait, 3 first stage
+// landed (MMA), 4 last MMA committed, 5 first accumulator ready (epilogue),
+// 6 epilogue done, 7 past the first cluster barrier, 8 reduce done, 9 exit]
+// (tools/skinny_trace.py).
+__device__ long long g_skinny_trace[148][10];
+#ifdef WS_SKINNY_TRACE
+constexpr bool kSkTrace = true;
+#else
+constexpr bool kSkTrace = false;
+#endif
+__device__ __forceinline__ void sk_mark(int ev) {
+  if constexpr (kSkTrace) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 148) g_skinny_trace[blockIdx.x][ev] = t;
+  }
+}
+
 template <int MODE, bool kWide = false>  // kWide: cluster reduce for > 16 batch rows
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ SkinnyArgs args, const __grid_constant__ TcEpilogue ep) {
   constexpr int NB = MODE == (int)Epi::kSwiGLU ? 2 : 1;
+  if (threadIdx.x == 0) sk_mark(0);
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -374,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tfull = [&](int b) { return bars + 8 * (2 * S + b); };
   auto tempty = [&](int b) { return bars + 8 * (2 * S + 2 + b); };
   const uint32_t tmem_slot = bars + 8 * (2 * S + 4);
+  const uint32_t push_base = bars + 1024;  // push-form cluster split region (launcher sizes it)
   volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (tmem_slot - raw));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -413,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  if (threadIdx.x == 0) sk_mark(1);
   const uint32_t tmem = *tmem_slot_ptr;
   // Weights are immutable: the producer fills the first ring stages with W
   // tiles before waiting for the previous kernel (PDL), so a short GEMM's
@@ -432,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   pdl_wait();  // global data produced by earlier kernels from here on
+  if (threadIdx.x == 0) sk_mark(2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -475,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = it; i < seg_end; ++i) {
           tc::mbar_wait(full(stage), phase);
           tc::fence_after();
+          if (i == it0) sk_mark(3);
           const uint32_t sa = base + stage * args.stage_bytes;
           for (int h = 0; h < sub; ++h) {
             const uint64_t db = tc::sdesc_sw128(sa + a_off + h * a_box);
@@ -499,6 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         it = seg_end;
       }
+      sk_mark(4);
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -517,6 +611,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int acc = 0, seg = 0;
     uint32_t acc_phase = 0;
+    const int rank = cs > 1 ? (int)(blockIdx.x % cs) : 0;
+    const int rpo = push_rows_per_owner(MODE == (int)Epi::kRopeKV, cs > 1 ? cs : 1);
+    int p_owner = 0, p_local = 0;
+    if (cs > 1 && !kWide) push_slot<MODE>(ep, i, cs, p_owner, p_local);
     for (int it = it0; it < it1; ++seg) {
       const int unit = it / kbs;
       const int seg_end = min(it1, (unit + 1) * kbs);
@@ -525,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int out_row = unit * kRows + i;  // output column (SwiGLU: act column)
       tc::mbar_wait(tfull(acc), acc_phase);
       tc::fence_after();
+      if (i == 0 && seg == 0) sk_mark(5);
       const uint32_t tacc = trow + acc * acc_cols;
       // cluster split: the partial stays in this CTA's shared memory (the TMA
       // ring, idle once the unit's last stage was consumed) for cluster_reduce
@@ -552,10 +651,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 4; ++q) {
               const float4 o = make_float4(__uint_as_float(v[j][4 * q]), __uint_as_float(v[j][4 * q + 1]),
                                            __uint_as_float(v[j][4 * q + 2]), __uint_as_float(v[j][4 * q + 3]));
-              if (cs > 1)  // swizzled shared-memory slot (part_off)
+              if (cs > 1 && !kWide) {  // push into the owner's region (remote shared-memory store)
+                st_dsmem_v4(push_base + part_off((rank * rpo + p_local) * NB + j, c / 4 + q, Mp), p_owner, o);
+              } else if (cs > 1) {  // own swizzled shared-memory slot (part_off), pulled by cluster_reduce
                 *reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(mine) + part_off(j * kRows + i, c / 4 + q, Mp)) = o;
-              else
+              } else {
                 __stcg(dst + q, o);
+              }
             }
           }
         }
@@ -569,19 +671,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       it = seg_end;
     }
   }
+  if (threadIdx.x == 128) sk_mark(6);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
   if (cs > 1) {
-    cluster_sync();  // every k-slice's partial is in its CTA's shared memory
+    cluster_sync();  // every k-slice's partial is in its owner's (push) / its own (pull) shared memory
+    if (threadIdx.x == 0) sk_mark(7);
     {  // every warp: the producer / MMA / allocator warps are idle by now
       const float* s_row = reinterpret_cast<const float*>(smem_raw + (bars + 8 * (2 * S + 6) - raw));
-      cluster_reduce<MODE, kWide>(args, ep, blockIdx.x / cs, blockIdx.x % cs, base, s_row, threadIdx.x);
+      const float* push_ptr = reinterpret_cast<const float*>(smem_raw + (push_base - raw));
+      cluster_reduce<MODE, kWide>(args, ep, blockIdx.x / cs, blockIdx.x % cs, base, push_ptr, s_row, threadIdx.x);
     }
-    cluster_sync();  // no CTA leaves while its partial may still be read
+    if (threadIdx.x == 128) sk_mark(8);
+    // pull form: no CTA leaves while its partial may still be read; the push
+    // form's remote stores all landed before the barrier above
+    if constexpr (kWide) cluster_sync();
   }
+  if (threadIdx.x == 0) sk_mark(9);
 }
 
 // Split-K fix-up for the units no single CTA covered: out = epilogue(sum of
@@ -857,7 +966,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   a.stage_bytes = sub * (NB * kW_BYTES + a.Mp * kBox * 2);
   a.stages = std::max(2, std::min(12, kSmemBudget / a.stage_bytes));
   a.total_iters = units * kbs;
-  const int smem = a.stages * a.stage_bytes + 1024 + 1024;  // align slack + barriers + TMEM slot + [128] row scales
+  int smem = a.stages * a.stage_bytes + 1024 + 1024;  // align slack + barriers + TMEM slot + [128] row scales
   // one CTA per SM, >= 2 k-blocks each
   int grid = std::max(1, std::min(kNumSMs, a.total_iters / 2));
   // Enough units to occupy most SMs (gate/up: 112): one whole unit per CTA.
@@ -895,6 +1004,12 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
         grid = units * S_;
         break;
       }
+  if (a.csplit > 1 && a.Mp <= 16) {  // push-form cluster split: the owners' receive region after the barriers
+    const int push = a.csplit * push_rows_per_owner(e.mode == Epi::kRopeKV, a.csplit) * NB * a.Mp * 4;
+    while (a.stages > 2 && a.stages * a.stage_bytes + 2048 + push > kMaxSmem) --a.stages;
+    smem = a.stages * a.stage_bytes + 2048 + push;
+    if (smem > kMaxSmem) return false;
+  }
   static const bool dbg = getenv("WS_SKINNY_DEBUG") != nullptr;
   if (dbg) fprintf(stderr, "[skinny] M=%d N=%d K=%d mode=%d units=%d kbs=%d grid=%d cluster=%d\n", M, N, K, (int)e.mode,
                    units, kbs, grid, a.csplit);
@@ -920,3 +1035,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
 }
 
 }  // namespace ws
+
+extern "C" int ws_skinny_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, ws::g_skinny_trace, sizeof(ws::g_skinny_trace)) == cudaSuccess ? 0 : 6;
+}
