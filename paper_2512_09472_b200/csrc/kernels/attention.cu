@@ -230,7 +230,10 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t local, int cta) {
 // head) is the M=16 side of mma.sync: S = Q K^T (16 x 16 keys), O += P V,
 // online softmax in registers. The warps' states merge in smem into one
 // unnormalised partial (m, l, O) per split; a combine kernel merges the splits.
-constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = 3;
+#ifndef WS_DEC_STAGES
+#define WS_DEC_STAGES 3
+#endif
+constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = WS_DEC_STAGES;
 // Split the context only until there is one CTA per SM: more, shorter CTAs
 // measured slower (B = 16 / 64 at ~4 / ~7 CTAs per SM: 4.32 -> 4.84 / 5.84 ->
 // 6.80 ms per step: prologue and merge per CTA); a single sequence still gets
