@@ -308,8 +308,11 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* out, int rows, int d, f
   } else if (d <= 1024) {
     launch_pdl(rmsnorm_kernel<128, 2>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
   } else if (d <= 4096) {
-    // 256 threads x 4 float4 (ncu, 2048 x 4096 rows: 11.7 -> 10.1 us vs 128 x 8; 512 x 2: 10.8)
-    launch_pdl(rmsnorm_kernel<256, 4>, dim3(rows), dim3(256), 0, st, x, w, out, d, eps);
+    // 128 threads x 8 float4. 256 x 4 measured 11.7 -> 10.1 us per 2048-row
+    // launch (ncu) but sums each row's squares in a different order, which
+    // flipped two bf16 near-tie greedy tokens of the parity suite (Llama-3-8B
+    // full depth seed 8, Phi-3 full width): not worth 0.4% of a prefill.
+    launch_pdl(rmsnorm_kernel<128, 8>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
   } else {
     launch_pdl(rmsnorm_kernel<128, 16>, dim3(rows), dim3(128), 0, st, x, w, out, d, eps);
   }
