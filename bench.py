@@ -58,6 +58,15 @@ def bench_config(args, world: int) -> dict:
             "parallelism": "replicas" if world > 1 else "single"}
 
 
+_T0 = time.perf_counter()
+
+
+def blog(msg: str) -> None:
+    """Progress on stderr with WS_BENCH_LOG=1 (the JSON line stays the only stdout)."""
+    if os.environ.get("WS_BENCH_LOG"):
+        print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def pct(xs, q):
     xs = sorted(xs)
     if not xs:
@@ -364,6 +373,7 @@ def run_ours(args, rank, world, local_rank):
     prompt = torch.randint(0, cfg.vocab, (S,), generator=torch.Generator().manual_seed(7), dtype=torch.int32)
     prompt_pinned = prompt.pin_memory()
     setup_s = time.perf_counter() - t_setup
+    blog("setup done")
 
     # clocks are sampled across every timed region below (cold, warm, value)
     clk = Clocks(dev).__enter__()
@@ -392,20 +402,24 @@ def run_ours(args, rank, world, local_rank):
     k0 = args.prewarm_layers
     # cold, plain bf16 stream: layers k..L + lm_head over PCIe
     cold = leg(k0)
+    blog("cold plain leg")
     # cold (e2e), packed stream: the same ranges losslessly packed on the host
     # (~34% fewer PCIe bytes), unpacked on the GPU per layer
     w.set_packed(cfg.name, packed)
     cold_packed = leg(k0)
+    blog("cold packed leg")
     w.models[cfg.name].packed = None
     # cold from an HBM-resident image on this GPU: the stand-in for a peer
     # GPU's copy, showing what layer streaming hides once the
     # link keeps up with the forward
     dev_src = host.to(f"cuda:{dev}")
     cold_hbm = leg(k0, source=dev_src)
+    blog("cold hbm leg")
     del dev_src
     torch.cuda.empty_cache()
     # warm: every layer resident
     warm = leg(None)
+    blog("warm leg")
     # the reference's own policy: k = required_prewarm_layers (cluster.py:145-166)
     # at the MEASURED stream bandwidth and per-token prefill cost, plain and packed
     spec = entry.spec
@@ -418,8 +432,10 @@ def run_ours(args, rank, world, local_rank):
     packed_bw = cold[0].streamed_bytes / (statistics.median(r.stream_ms for r in cold_packed) / 1e3) / 1e3
     k_req_packed = required_prewarm_layers(spec_m, packed_bw, S)
     cold_kreq = leg(k_req)
+    blog("k_req leg")
     w.set_packed(cfg.name, packed)
     cold_kreq_packed = leg(k_req_packed)
+    blog("k_req packed leg")
     w.models[cfg.name].packed = None
     # the same policy at the reference's BYTE budget: its uniform layer_bytes
     # (cluster.py:85-88) folds the embedding and lm_head into every layer, so
@@ -430,6 +446,7 @@ def run_ours(args, rank, world, local_rank):
     head_b = lay.total - lay.final_norm
     m_budget = max(m for m in range(cfg.layers + 1) if m == 0 or lay.prefix_bytes(m) + head_b <= budget)
     cold_budget = leg(m_budget, head=True)
+    blog("byte-budget leg")
 
     # ---- value: warm prefill throughput, prompt + weights resident in HBM
     w.switch_memory(cfg.name)
@@ -458,6 +475,7 @@ def run_ours(args, rank, world, local_rank):
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     value = world * K * S / (elapsed_ms / 1e3)
     prefill_ms = elapsed_ms / K
+    blog("value")
 
     # ---- memory switch burst: promote (weight->KV), reclaim (KV->free), release
     w.release()
@@ -482,6 +500,7 @@ def run_ours(args, rank, world, local_rank):
         rc_done.append((t3 - t2) * 1e6)
         rel_done.append((t4 - t3) * 1e6)
 
+    blog("switch burst")
     # ---- decode: every sequence prefilled to decode_ctx, then B tokens per step
     #      (HBM bound: all weights but the embedding table + each sequence's KV)
     decode = []
@@ -561,6 +580,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         gemm_ms[impl] = g0.elapsed_time(g1) / 20
     achieved = gemm_flops / (gemm_ms[0] / 1e3) / 1e12
+    blog("roofline GEMM")
 
     # ---- the reference's analytic model, evaluated with MEASURED inputs
     stall_pred = catchup_stall_ms(spec_m, args.prewarm_layers, bw_bytes_ms, S)
@@ -694,7 +714,9 @@ def run_ours(args, rank, world, local_rank):
         sys.path.insert(0, str(ROOT / "tools"))
         from config3_switch_burst import run_burst
 
+        blog("config 3 start")
         line["config3_switch_burst"] = run_burst(switches=args.config3_switches, device=dev)
+        blog("config 3 done")
         torch.cuda.empty_cache()
     if args.config5_policies:
         # BASELINE configs[4]: the reference engine's 8-worker decision log
@@ -712,6 +734,7 @@ def run_ours(args, rank, world, local_rank):
         images = HostImages(need, dev)
         c5 = {"setup_s": time.perf_counter() - t_c5, "logical_gpus_per_rank": len(mine)}
         for p_ in pols:
+            blog(f"config 5 {p_}")
             res = [replay_gpu(trace, p_, g, dev, images) for g in mine]
             if world > 1:
                 allres = [None] * world
