@@ -276,8 +276,11 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
     const bf16* __restrict__ qkv, KvGeom kv, int layer, const int32_t* __restrict__ seqs,
     const int32_t* __restrict__ pos, int heads, float scale_log2, float* __restrict__ part,
     int n_splits, int split_keys, bf16* __restrict__ out, int in_cluster,
-    const __grid_constant__ CUtensorMap kvmap) {
+    const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ L2Pf pf) {
   pdl_trigger();
+  if (threadIdx.x == 32)  // a later kernel's weights into L2 while this latency-bound one runs
+    l2_prefetch(pf, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                gridDim.x * gridDim.y * gridDim.z);
   using S = DecodeSmem<HD, TMA>;
   constexpr int ST = S::kStride, CH = HD / 8;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -680,7 +683,7 @@ void launch_decode(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
 template <int HD, bool TMA>
 void decode_launch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
                    const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
-                   const CUtensorMap& map, cudaStream_t st) {
+                   const CUtensorMap& map, cudaStream_t st, const L2Pf& pf) {
   using S = DecodeSmem<HD, TMA>;
   static bool attr = false;
   if (!attr) {
@@ -705,7 +708,7 @@ void decode_launch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, cons
   count_launch();
   launch_decode(attn_decode_kernel<HD, TMA>, grid, dim3(kDecWarps * 32), S::kBytes, in_cluster ? n_splits : 0, st,
                 qkv, kv, layer, seqs, ctx, heads, scale * 1.4426950408889634f, scratch, n_splits, split_keys, out,
-                in_cluster, map);
+                in_cluster, map, pf);
   if (n_splits > 1 && !in_cluster) {
     count_launch();
     launch_pdl(attn_combine_kernel<HD>, dim3(heads, n_seqs), dim3(HD), 0, st, scratch, out, heads, n_splits);
@@ -715,18 +718,18 @@ void decode_launch(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, cons
 template <int HD>
 void decode_impl(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
                  const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale, float* scratch,
-                 cudaStream_t st) {
+                 cudaStream_t st, const L2Pf& pf) {
   // TMA tiles need whole 16-token runs per block and the window addressable
   // as HD-wide rows; WS_DEC_TMA=0 forces the cp.async gather (A/B)
   static const bool tma_env = !(std::getenv("WS_DEC_TMA") && std::getenv("WS_DEC_TMA")[0] == '0');
   CUtensorMap map{};
   if constexpr (HD % 64 == 0) {
     if (tma_env && kv.tpb % kDecKeys == 0 && kv_window_tmap(kv, HD, &map)) {
-      decode_launch<HD, true>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st);
+      decode_launch<HD, true>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st, pf);
       return;
     }
   }
-  decode_launch<HD, false>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st);
+  decode_launch<HD, false>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, map, st, pf);
 }
 
 }  // namespace
@@ -743,11 +746,11 @@ void launch_attn_prefill(const bf16* qkv, bf16* out, const KvGeom& kv, int layer
 
 void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer, const int32_t* seqs,
                         const int32_t* ctx, int n_seqs, int heads, int max_ctx, float scale,
-                        float* scratch, cudaStream_t st) {
+                        float* scratch, cudaStream_t st, const L2Pf& pf) {
   switch (kv.head_dim) {
-    case 64: decode_impl<64>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st); break;
-    case 96: decode_impl<96>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st); break;
-    case 128: decode_impl<128>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st); break;
+    case 64: decode_impl<64>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st, pf); break;
+    case 96: decode_impl<96>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st, pf); break;
+    case 128: decode_impl<128>(qkv, out, kv, layer, seqs, ctx, n_seqs, heads, max_ctx, scale, scratch, st, pf); break;
     default: break;
   }
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "ops.cuh"
+
 namespace ws {
 namespace dev {
 
@@ -80,6 +82,20 @@ __device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, cons
       "{%8,%9}, {%0,%1,%2,%3};\n"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// Issue this CTA's share of an L2 prefetch hint (one calling thread).
+__device__ __forceinline__ void l2_prefetch(const L2Pf& f, int cta, int n_cta) {
+  if (!f.p) return;
+  const int items = f.rows * f.nseg;
+  for (int i = cta; i < items; i += n_cta) {
+    const int r = i / f.nseg, s = i - r * f.nseg;
+    const int64_t off = (int64_t)r * f.pitch + (int64_t)s * f.seg_stride;
+    if (off >= f.limit) continue;
+    const int64_t n = f.limit - off < f.seg_bytes ? f.limit - off : f.seg_bytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(f.p + off), "r"((uint32_t)(n & ~15ll))
+                 : "memory");
+  }
 }
 
 }  // namespace dev

@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox, (unit * NB + j) * kRows);
     }
   }
+  if (warp == 3 && lane == 0 && ep.l2pf_at == 0) l2_prefetch(ep.l2pf, blockIdx.x, gridDim.x);
   pdl_wait();  // global data produced by earlier kernels from here on
   if (threadIdx.x == 0) sk_mark(2);
 
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
+      if (ep.l2pf_at == 1) l2_prefetch(ep.l2pf, blockIdx.x, gridDim.x);
     }
     __syncwarp();
   } else if (warp == 1) {

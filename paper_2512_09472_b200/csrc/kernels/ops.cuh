@@ -11,6 +11,18 @@ namespace ws {
 
 using bf16 = __nv_bfloat16;
 
+// L2 prefetch hint for a decode kernel: the weights of a LATER kernel of the
+// step, pulled into L2 while this one is latency-bound and leaves HBM
+// bandwidth idle (weights are immutable, so the prefetch may run before the
+// PDL wait). Items = rows x nseg byte ranges [p + r*pitch + s*seg_stride,
+// + seg_bytes) clipped at `limit` bytes from p, spread round-robin over the
+// launch's CTAs (cp.async.bulk.prefetch.L2, one issuing thread per CTA).
+struct L2Pf {
+  const char* p = nullptr;
+  int64_t pitch = 0, seg_stride = 0, limit = 0;
+  int rows = 0, nseg = 1, seg_bytes = 0;
+};
+
 // Paged KV cache geometry: block = one pool page holding `tpb` tokens of every
 // layer; inside a page: [layer][k|v][kv_head][tpb][head_dim] bf16.
 struct KvGeom {
@@ -62,7 +74,8 @@ bool attn_prefill_prefers_mma(const KvGeom& kv, int rows, int heads);
 // its own K/V already appended). scratch: decode_scratch_floats() floats.
 void launch_attn_decode(const bf16* qkv, bf16* out, const KvGeom& kv, int layer,
                         const int32_t* seqs, const int32_t* pos, int n_seqs, int heads,
-                        int max_ctx, float scale, float* scratch, cudaStream_t st);
+                        int max_ctx, float scale, float* scratch, cudaStream_t st,
+                        const L2Pf& pf = L2Pf{});
 int decode_scratch_floats(int n_seqs, int heads, int kv_heads, int head_dim);
 
 // C[M,N] = A[M,K] * B[N,K]^T with epilogue:
@@ -106,6 +119,10 @@ struct TcEpilogue {
   // rows can leave as TMA boxes of 16 tokens into the page window (prefill of
   // one sequence, block-aligned pos0, 16-token runs per block)
   int kv_tma = 0;
+  // skinny decode GEMMs: L2 prefetch of a later kernel's weights (see L2Pf),
+  // issued at the start (l2pf_at 0) or after the producer's last load (1)
+  L2Pf l2pf{};
+  int l2pf_at = 0;
 };
 bool gemm_tc_epilogue_supported(const TcEpilogue& e, int N, int head_dim);
 bool launch_gemm_tc_epi(const bf16* A, const bf16* B, int M, int N, int K, const TcEpilogue& e,

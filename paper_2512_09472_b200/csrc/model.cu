@@ -505,26 +505,63 @@ int ws_model_decode(ws_model* m, ws_pool* pool, const void* wts, const int32_t* 
     nc.row_ss = np.row_ss;
     nc.row_scale = reinterpret_cast<float*>(wsb + w.norm_scale);
   }
+  // L2 prefetch hints (WS_L2PF bit mask, A/B): a latency-bound kernel pulls a
+  // later kernel's weights into L2 — 1: attention -> the O weights, 2: QKV ->
+  // the O weights, 4: O -> a prefix of every gate/up row, 8: gate/up -> a
+  // prefix of every quarter-row of down, 16: down -> the next QKV's half-rows.
+  static const int pf_mask = getenv("WS_L2PF") ? atoi(getenv("WS_L2PF")) : 0;
+  static const int pf_frac = getenv("WS_L2PF_FRAC") ? atoi(getenv("WS_L2PF_FRAC")) : 50;
+  static const int pf_at = getenv("WS_L2PF_AT") ? atoi(getenv("WS_L2PF_AT")) : 0;
+  static const int pf_rows = getenv("WS_L2PF_ROWS") ? atoi(getenv("WS_L2PF_ROWS")) : 16;
+  const int pfm = fold && n <= pf_rows ? pf_mask : 0;
+  auto pf_whole = [](const void* p, int64_t bytes) {
+    L2Pf f;
+    f.p = static_cast<const char*>(p);
+    f.pitch = 1 << 16;
+    f.seg_bytes = 1 << 16;
+    f.rows = (int)((bytes + f.pitch - 1) / f.pitch);
+    f.limit = bytes;
+    return f;
+  };
+  auto pf_prefix = [&](const void* p, int rows, int K, int nseg) {  // prefix of each of nseg slices of every row
+    L2Pf f;
+    f.p = static_cast<const char*>(p);
+    f.pitch = (int64_t)K * 2;
+    f.rows = rows;
+    f.nseg = nseg;
+    f.seg_stride = f.pitch / nseg;
+    f.seg_bytes = (int)(f.seg_stride * pf_frac / 100) & ~15;
+    f.limit = f.pitch * rows;
+    return f;
+  };
   launch_embed(tokens, W<bf16>(wts, L.embed), x, n, d, st);
   launch_rmsnorm(x, W<bf16>(wts, L.layers[0].attn_norm), h, n, d, c.rms_eps, st);
+  nc.l2pf_at = np.l2pf_at = pf_at;
   for (int l = 0; l < c.layers; ++l) {
     const auto& Ly = L.layers[l];
+    const bool last = l + 1 == c.layers;
+    nc.l2pf = (pfm & 2) ? pf_whole(W<bf16>(wts, Ly.wo), (int64_t)d * o * 2) : L2Pf{};
     if (!qkv_rope(m, h, W<bf16>(wts, Ly.wqkv), c.qkv_bias ? W<bf16>(wts, Ly.bqkv) : nullptr, n, kv, l, 0, 0, seqs,
                   pos, qkv, st, fold && l > 0 ? &nc : nullptr))
       WS_FAIL(WS_ERR_CUDA, "folded-norm QKV GEMM declined");
-    launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st);
-    const bool last = l + 1 == c.layers;
+    launch_attn_decode(qkv, attn, kv, l, seqs, pos, n, c.heads, max_ctx, scale, scratch, st,
+                       (pfm & 1) ? pf_whole(W<bf16>(wts, Ly.wo), (int64_t)d * o * 2) : L2Pf{});
     if (fold) {
       np.norm_g = W<bf16>(wts, Ly.ffn_norm);
+      np.l2pf = (pfm & 4) ? pf_prefix(W<bf16>(wts, Ly.wgu), 2 * c.ffn, d, 1) : L2Pf{};
       if (!launch_gemm_skinny(attn, W<bf16>(wts, Ly.wo), n, d, o, np, st)) WS_FAIL(WS_ERR_CUDA, "folded O GEMM");
+      nc.l2pf = (pfm & 8) ? pf_prefix(W<bf16>(wts, Ly.wdown), d, c.ffn, 4) : L2Pf{};
       if (!gate_up_swiglu(m, h, W<bf16>(wts, Ly.wgu), n, gu, act, st, &nc))
         WS_FAIL(WS_ERR_CUDA, "folded-norm gate/up GEMM declined");
       if (!last) {
         np.norm_g = W<bf16>(wts, L.layers[l + 1].attn_norm);
+        np.l2pf = (pfm & 16) ? pf_prefix(W<bf16>(wts, L.layers[l + 1].wqkv), q, d, 2) : L2Pf{};
         if (!launch_gemm_skinny(act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, np, st))
           WS_FAIL(WS_ERR_CUDA, "folded down GEMM");
         continue;
       }
+      np.l2pf = L2Pf{};
+      nc.l2pf = L2Pf{};
       // last layer: plain residual + the final norm kernel for the lm_head rows
       if (int e = row_parallel_norm(m, act, W<bf16>(wts, Ly.wdown), n, d, c.ffn, x, partial,
                                     W<bf16>(wts, L.final_norm), hl, st))
