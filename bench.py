@@ -89,10 +89,16 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        # samples go to a file, not a pipe: nobody reads a pipe until __exit__,
+        # and once its 64 KB buffer fills (~2 min of samples) nvidia-smi blocks
+        # inside its sampling loop, which can stall this process's own driver
+        # calls behind it
+        import tempfile
+        self.out = tempfile.TemporaryFile(mode="w+")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
-                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-i", str(self.device)], stdout=self.out, stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -102,7 +108,14 @@ class Clocks:
         if self.proc is None:
             return
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            self.proc.wait()
+        self.out.seek(0)
+        out = self.out.read()
+        self.out.close()
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
@@ -911,6 +924,14 @@ def _cpu_model():
 
 
 def main():
+    # a stuck run leaves every thread's Python stack on stderr (WS_BENCH_WATCHDOG
+    # seconds, default 1200; the whole default run takes ~4-5 min) instead of
+    # an opaque timeout
+    import faulthandler
+    faulthandler.enable()
+    wd = float(os.environ.get("WS_BENCH_WATCHDOG", "1200"))
+    if wd > 0:
+        faulthandler.dump_traceback_later(wd, exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

@@ -53,6 +53,7 @@ struct SkinnyArgs {
   int M, N, K, Mp, stages, stage_bytes, total_iters, sub, kbs;
   float* partial;      // [grid][2][NB*128][Mp]
   int csplit;          // >= 2: cluster split-K (see launch_gemm_skinny); 0: stream-K
+  int evict_first;     // weight tiles loaded with an L2 evict_first policy (WS_SK_EVF, A/B)
 };
 
 // Residual producer of a folded RMSNorm (norm_role 1): x_new is final (one
@@ -511,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (the previous kernel's output) are loaded after the wait. Every other
   // thread waits up front.
   const int pre = (warp == 0 && lane == 0) ? min(S, it1 - it0) : 0;
+  const uint64_t wpol = args.evict_first ? tc::policy_evict_first() : 0;
   if (warp == 0 && lane == 0) {
     for (int k = 0; k < pre; ++k) {
       const int it = it0 + k, unit = it / kbs, kb = it % kbs;
@@ -519,7 +521,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < NB; ++j)
         for (int h = 0; h < sub; ++h)
-          tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox, (unit * NB + j) * kRows);
+          if (args.evict_first)
+            tc::tma_load_2d_hint(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox,
+                                 (unit * NB + j) * kRows, wpol);
+          else
+            tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox, (unit * NB + j) * kRows);
     }
   }
   if (warp == 3 && lane == 0 && ep.l2pf_at == 0) l2_prefetch(ep.l2pf, blockIdx.x, gridDim.x);
@@ -543,8 +549,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NB; ++j)
           for (int h = 0; h < sub; ++h)
-            tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
-                            (unit * NB + j) * kRows);
+            if (args.evict_first)
+              tc::tma_load_2d_hint(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
+                                   (unit * NB + j) * kRows, wpol);
+            else
+              tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
+                              (unit * NB + j) * kRows);
         for (int h = 0; h < sub; ++h)
           tc::tma_load_2d(sa + a_off + h * a_box, &map_a, full(stage), kb * kBK + h * kBox, 0);
         if (++stage == S) {
@@ -985,6 +995,13 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // WS_SKINNY_CLUSTER=0: stream-K + fix-up (A/B).
   static const bool cl_on = !(getenv("WS_SKINNY_CLUSTER") && getenv("WS_SKINNY_CLUSTER")[0] == '0');
   a.csplit = 0;
+  // Weight tiles stream through L2 as evict_first: each is read once per step,
+  // and at the normal priority the stream evicts what the step reuses (the
+  // activations, partials, norm rows, K/V). Graphed decode steps, ctx 1024,
+  // same box, WS_SK_EVF=0 -> 1: B = 1 / 4 / 16 3.37 / 3.56 / 3.88 -> 3.22-3.32 /
+  // 3.35 / 3.68 ms (tools/ab_l2pf2.sh).
+  static const int evf = getenv("WS_SK_EVF") ? atoi(getenv("WS_SK_EVF")) : 1;
+  a.evict_first = evf;
   // Above 32 batch rows the fp32 partials the stream-K fix-up moves through
   // L2 grow with the rows; the cluster form wins where they are large next
   // to the weights and the clusters still cover >= 120 SMs (same-box per-GEMM
