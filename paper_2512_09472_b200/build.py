@@ -34,6 +34,8 @@ if os.environ.get("WS_ATTN_POLY"):  # pairs of every 8 whose exp2 runs on the FM
     CUDA_ONLY.append(f"-DWS_ATTN_POLY={int(os.environ['WS_ATTN_POLY'])}")
 if os.environ.get("WS_ATTN_SPLIT"):  # 0: one softmax warp per 32 query rows of a tile (A/B builds)
     CUDA_ONLY.append(f"-DWS_ATTN_SPLIT={int(os.environ['WS_ATTN_SPLIT'])}")
+if os.environ.get("WS_DEC_KVPOL"):  # decode-attention K/V L2 policy: 1 evict_first, 2 evict_last (A/B builds)
+    CUDA_ONLY.append(f"-DWS_DEC_KVPOL={int(os.environ['WS_DEC_KVPOL'])}")
 if os.environ.get("WS_DEC_STAGES"):  # decode-attention ring depth per warp (A/B builds)
     CUDA_ONLY.append(f"-DWS_DEC_STAGES={int(os.environ['WS_DEC_STAGES'])}")
 if os.environ.get("WS_SKINNY_TRACE"):  # per-CTA globaltimer timeline of the skinny GEMM (debugging only)

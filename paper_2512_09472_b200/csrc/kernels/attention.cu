@@ -234,6 +234,15 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t local, int cta) {
 #define WS_DEC_STAGES 3
 #endif
 constexpr int kDecWarps = 4, kDecKeys = 16, kDecStages = WS_DEC_STAGES;
+// K/V TMA tiles' L2 policy: 0 default, 1 evict_first, 2 evict_last. A step
+// reads each K/V tile once; as evict_first they stop displacing what the
+// step reuses. Graphed decode, ctx 1024, same box, 0 -> 1 (-> 2): B = 1 / 16
+// / 64 3.22 / 3.68 / 5.45 -> 3.22 / 3.61 / 5.30-5.35 (3.22 / 3.68 / 5.45) ms
+// (tools/ab_kvpol.sh).
+#ifndef WS_DEC_KVPOL
+#define WS_DEC_KVPOL 1
+#endif
+constexpr int kDecKvPolicy = WS_DEC_KVPOL;
 // Split the context only until there is one CTA per SM: more, shorter CTAs
 // measured slower (B = 16 / 64 at ~4 / ~7 CTAs per SM: 4.32 -> 4.84 / 5.84 ->
 // 6.80 ms per step: prologue and merge per CTA); a single sequence still gets
@@ -356,6 +365,23 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
                        : "memory");
 #pragma unroll
           for (int hh = 0; hh < HD / 64; ++hh) {
+            if constexpr (kDecKvPolicy != 0) {  // K/V tiles with an L2 cache policy (A/B build knob)
+              uint64_t pol;
+              if constexpr (kDecKvPolicy == 1)
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+              else
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+                  "[%1, {%3, %4}], [%2], %5;\n" ::"r"(dk + hh * kDecKeys * 128),
+                  "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(k_plane / HD)), "l"(pol)
+                  : "memory");
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+                  "[%1, {%3, %4}], [%2], %5;\n" ::"r"(dv + hh * kDecKeys * 128),
+                  "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(v_plane / HD)), "l"(pol)
+                  : "memory");
+            } else {
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
                 ::"r"(dk + hh * kDecKeys * 128), "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(k_plane / HD))
@@ -364,6 +390,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) attn_decode_kernel(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
                 ::"r"(dv + hh * kDecKeys * 128), "l"(&kvmap), "r"(bar), "r"(hh * 64), "r"(y + (int)(v_plane / HD))
                 : "memory");
+            }
           }
         }
         (void)rows;
