@@ -54,6 +54,9 @@ struct SkinnyArgs {
   float* partial;      // [grid][2][NB*128][Mp]
   int csplit;          // >= 2: cluster split-K (see launch_gemm_skinny); 0: stream-K
   int evict_first;     // weight tiles loaded with an L2 evict_first policy (WS_SK_EVF, A/B)
+  int splitj;          // SwiGLU, whole units only: a stage holds the gate OR the up rows of a
+                       // k-block (kbs counts 2 iterations per k-block), so a stage spans twice
+                       // the k-columns of each weight row (WS_SK_SPLITJ, A/B)
 };
 
 // Residual producer of a folded RMSNorm (norm_role 1): x_new is final (one
@@ -470,7 +473,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Mp = args.Mp, G = gridDim.x, total = args.total_iters;
   const int kbs = args.kbs, sub = args.sub, kBK = kBox * sub;
-  const uint32_t a_off = NB * sub * kW_BYTES, a_box = args.Mp * kBox * 2;
+  const int SJ = (NB == 2 && args.splitj) ? 2 : 1;  // iterations per k-block
+  const uint32_t a_off = (SJ == 2 ? 1 : NB) * sub * kW_BYTES, a_box = args.Mp * kBox * 2;
   // stream-K: equal contiguous ranges of the (unit, k-block) space; cluster
   // split: CTA rank s of cluster u takes k-slice s of unit u
   const int cs = args.csplit;
@@ -513,19 +517,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   // thread waits up front.
   const int pre = (warp == 0 && lane == 0) ? min(S, it1 - it0) : 0;
   const uint64_t wpol = args.evict_first ? tc::policy_evict_first() : 0;
+  // weight boxes of iteration it into the stage at sa: both row blocks of the
+  // unit (SJ = 1) or only row block j = it % 2 (SJ = 2)
+  auto load_w = [&](uint32_t sa, uint32_t bar, int it) {
+    const int unit = it / kbs, r = it % kbs, kb = r / SJ;
+    for (int jj = 0; jj < (SJ == 2 ? 1 : NB); ++jj) {
+      const int j = SJ == 2 ? r % 2 : jj;
+      for (int h = 0; h < sub; ++h) {
+        const uint32_t dst = sa + (jj * sub + h) * kW_BYTES;
+        if (args.evict_first)
+          tc::tma_load_2d_hint(dst, &map_w, bar, kb * kBK + h * kBox, (unit * NB + j) * kRows, wpol);
+        else
+          tc::tma_load_2d(dst, &map_w, bar, kb * kBK + h * kBox, (unit * NB + j) * kRows);
+      }
+    }
+  };
   if (warp == 0 && lane == 0) {
     for (int k = 0; k < pre; ++k) {
-      const int it = it0 + k, unit = it / kbs, kb = it % kbs;
+      const int it = it0 + k;
       const uint32_t sa = base + k * args.stage_bytes;
       tc::mbar_expect_tx(full(k), args.stage_bytes);
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        for (int h = 0; h < sub; ++h)
-          if (args.evict_first)
-            tc::tma_load_2d_hint(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox,
-                                 (unit * NB + j) * kRows, wpol);
-          else
-            tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(k), kb * kBK + h * kBox, (unit * NB + j) * kRows);
+      load_w(sa, full(k), it);
     }
   }
   if (warp == 3 && lane == 0 && ep.l2pf_at == 0) l2_prefetch(ep.l2pf, blockIdx.x, gridDim.x);
@@ -538,23 +550,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < pre; ++k)
         for (int h = 0; h < sub; ++h)
           tc::tma_load_2d(base + k * args.stage_bytes + a_off + h * a_box, &map_a, full(k),
-                          ((it0 + k) % kbs) * kBK + h * kBox, 0);
+                          ((it0 + k) % kbs / SJ) * kBK + h * kBox, 0);
       int stage = pre == S ? 0 : pre;
       uint32_t phase = pre == S ? 1 : 0;
       for (int it = it0 + pre; it < it1; ++it) {
-        const int unit = it / kbs, kb = it % kbs;
+        const int kb = it % kbs / SJ;
         tc::mbar_wait(empty(stage), phase ^ 1);
         const uint32_t sa = base + stage * args.stage_bytes;
         tc::mbar_expect_tx(full(stage), args.stage_bytes);
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          for (int h = 0; h < sub; ++h)
-            if (args.evict_first)
-              tc::tma_load_2d_hint(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
-                                   (unit * NB + j) * kRows, wpol);
-            else
-              tc::tma_load_2d(sa + (j * sub + h) * kW_BYTES, &map_w, full(stage), kb * kBK + h * kBox,
-                              (unit * NB + j) * kRows);
+        load_w(sa, full(stage), it);
         for (int h = 0; h < sub; ++h)
           tc::tma_load_2d(sa + a_off + h * a_box, &map_a, full(stage), kb * kBK + h * kBox, 0);
         if (++stage == S) {
@@ -581,14 +585,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::fence_after();
           if (i == it0) sk_mark(3);
           const uint32_t sa = base + stage * args.stage_bytes;
+          // SJ = 2: segments are whole units, so iterations 0 / 1 open the gate / up accumulators
+          const uint32_t acc_on = SJ == 2 ? (uint32_t)(i - it >= 2) : (uint32_t)(i > it);
           for (int h = 0; h < sub; ++h) {
             const uint64_t db = tc::sdesc_sw128(sa + a_off + h * a_box);
 #pragma unroll
-            for (int j = 0; j < NB; ++j) {
-              const uint64_t da = tc::sdesc_sw128(sa + (j * sub + h) * kW_BYTES);
+            for (int jj = 0; jj < (SJ == 2 ? 1 : NB); ++jj) {
+              const int j = SJ == 2 ? (i % kbs) % 2 : jj;
+              const uint64_t da = tc::sdesc_sw128(sa + (jj * sub + h) * kW_BYTES);
 #pragma unroll
               for (int k = 0; k < kBox / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle row
-                tc::mma_f16(d + j * Mp, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i > it) | h | k);
+                tc::mma_f16(d + j * Mp, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, acc_on | h | k);
             }
           }
           tc::commit(empty(stage));
@@ -1002,6 +1009,7 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
   // 3.35 / 3.68 ms (tools/ab_l2pf2.sh).
   static const int evf = getenv("WS_SK_EVF") ? atoi(getenv("WS_SK_EVF")) : 1;
   a.evict_first = evf;
+  a.splitj = 0;
   // Above 32 batch rows the fp32 partials the stream-K fix-up moves through
   // L2 grow with the rows; the cluster form wins where they are large next
   // to the weights and the clusters still cover >= 120 SMs (same-box per-GEMM
@@ -1023,6 +1031,21 @@ bool launch_gemm_skinny(const bf16* A, const bf16* W, int M, int N, int K, const
         grid = units * S_;
         break;
       }
+  // Split-j SwiGLU stages for whole-unit launches (WS_SK_SPLITJ=1, A/B): a
+  // stage carries one 128-row block (gate or up) over twice the k-columns,
+  // so every TMA issue fetches twice the contiguous bytes of each weight row
+  static const bool sj_env = getenv("WS_SK_SPLITJ") && getenv("WS_SK_SPLITJ")[0] == '1';
+  if (sj_env && swiglu && grid == units && a.csplit == 0) {
+    int sj_sub = 4;
+    while (sj_sub > 1 && (K % (sj_sub * kBox) || 3 * sj_sub * (kW_BYTES + mp * kBox * 2) > kSmemBudget)) sj_sub /= 2;
+    a.splitj = 1;
+    a.sub = sj_sub;
+    a.kbs = 2 * (K / (kBox * sj_sub));
+    a.stage_bytes = sj_sub * (kW_BYTES + a.Mp * kBox * 2);
+    a.stages = std::max(2, std::min(12, kSmemBudget / a.stage_bytes));
+    a.total_iters = units * a.kbs;
+    smem = a.stages * a.stage_bytes + 1024 + 1024;
+  }
   if (a.csplit > 1 && a.Mp <= 16) {  // push-form cluster split: the owners' receive region after the barriers
     const int push = a.csplit * push_rows_per_owner(e.mode == Epi::kRopeKV, a.csplit) * NB * a.Mp * 4;
     while (a.stages > 2 && a.stages * a.stage_bytes + 2048 + push > kMaxSmem) --a.stages;
