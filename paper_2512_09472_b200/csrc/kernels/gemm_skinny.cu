@@ -913,7 +913,7 @@ void launch_mode(const CUtensorMap& mw, const CUtensorMap& ma, const SkinnyArgs&
     attr[n].val.clusterDim.x = a.csplit;
     attr[n].val.clusterDim.y = 1;
     attr[n++].val.clusterDim.z = 1;
-    if (pdl_enabled()) {
+    if (pdl_for_launch()) {
       attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[n++].val.programmaticStreamSerializationAllowed = 1;
     }

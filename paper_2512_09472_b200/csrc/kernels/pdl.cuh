@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <utility>
 
+#include "pdl_flag.h"
+
 namespace ws {
 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
@@ -27,6 +29,15 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// The PDL attribute for one launch: off once after pdl_break_next().
+inline bool pdl_for_launch() {
+  if (t_pdl_break) {
+    t_pdl_break = false;
+    return false;
+  }
+  return pdl_enabled();
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -39,7 +50,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_for_launch() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -8,6 +8,7 @@
 
 #include "common.h"
 #include "kernels/ops.cuh"
+#include "kernels/pdl_flag.h"
 
 struct ws_streamer {
   std::vector<cudaEvent_t> done;    // per range, timing-enabled: the range is usable
@@ -109,6 +110,7 @@ int ws_streamer_wait(ws_streamer* s, int32_t i, void* stream) {
   if (!s) WS_FAIL(WS_ERR_INVALID, "null streamer");
   if (i < 0 || i >= s->started) return WS_OK;
   WS_CUDA(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), s->done[i], 0));
+  ws::pdl_break_next();  // the kernel behind this wait launches without PDL (pdl_flag.h)
   return WS_OK;
 }
 
