@@ -661,7 +661,10 @@ int decode_cluster_limit(K kernel, int smem) {
                             cudaSuccess;
   if (!non_portable) cudaGetLastError();
   if (const char* e = std::getenv("WS_DEC_CLUSTER")) return std::min(std::atoi(e), non_portable ? 16 : 8);
-  if (!non_portable) return 8;
+  // 8 (portable) by default since the L2 evict_first streams: graphed decode,
+  // ctx 1024, same box, 16 -> 8: B = 1 / 4 / 16 3.207 / 3.321 / 3.593 ->
+  // 3.189 / 3.315 / 3.597 ms (profiles/r2h_ab_dec_cluster.txt)
+  if (!non_portable || !std::getenv("WS_DEC_CLUSTER16")) return 8;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(16, 1, 1);
   cfg.blockDim = dim3(kDecWarps * 32);
